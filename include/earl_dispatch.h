@@ -1,0 +1,226 @@
+/*
+ * earl_dispatch.h -- C ABI of the B200-native EARL data dispatcher.
+ *
+ * What it does (§2 "Data Dispatcher"): intermediate RL batches --
+ * variable-length sequences carrying per-token fields ("tokens, log-probabilities, rewards,
+ * returns, and other tensors") -- held by the ranks of one parallel layout
+ * are re-distributed to the ranks of another layout, "adaptive to the current data
+ * distribution layout and parallelism configuration", by sending "data
+ * directly to the target workers from their computation origins": an
+ * all-to-all instead of the centralized all-gather-and-scatter.
+ *
+ * The two calls named by the build's north star are earl_dispatch_plan (device-side
+ * planner: prefix sums over lengths, length-balanced assignment, SP chunking, per-segment
+ * offsets) and earl_dispatch_exec (one fused pass: read each source byte once, store it at
+ * its final offset on every destination replica, over NVLink peer mappings).
+ * earl_dispatch_pack / earl_dispatch_unpack are the staged alternative (gather into
+ * contiguous per-destination-shard messages, scatter from them).  Readings of the paper
+ * are listed in DESIGN.md; the ones that shape this ABI are
+ * repeated at the declarations.
+ *
+ * Conventions
+ *  - Every call returns an earl_status_t; outputs go through out-parameters.  On error,
+ *    earl_last_error() (thread-local) holds a one-line message.
+ *  - Device work is stream-ordered and asynchronous.  `stream` is a cudaStream_t passed
+ *    as void* (NULL = legacy default stream).  Errors found on the device (negative
+ *    length, EXPLICIT group out of range, int32 overflow of cu_seqlens, peer timeout) are
+ *    latched in the plan and reported by the next host-synchronising call
+ *    (earl_plan_local_sizes, earl_plan_stats, earl_plan_export, earl_plan_sync).
+ *  - Collective semantics (like NCCL): in a multi-process comm every rank calls
+ *    earl_dispatch_plan / earl_dispatch_exec in the same order with identical layouts,
+ *    lengths and fields.  Each rank computes the same plan independently (integer-only,
+ *    deterministic); no metadata is exchanged.  A rank in neither layout participates
+ *    with zero bytes.
+ *  - Emulated comm (rank == EARL_ALL_RANKS): one process holds all `world` ranks on one
+ *    device; buffer arrays are then rank-major [world][n_fields] and one launch serves
+ *    all ranks (the 1-GPU measurement mode of SURVEY.md §8(d)).
+ *  - Field base pointers must be 16-byte aligned (cudaMalloc gives 256 B), else
+ *    EARL_ERR_INVALID_ARGUMENT.  Field bytes are opaque and never interpreted (reading
+ *    c10): the result is bit-exact.
+ *  - A comm is not thread-safe.  Planning is pure: the same inputs give the same plan.
+ *
+ * Ownership: the caller owns send/recv/stage buffers, seq_lens and streams.  The plan owns
+ * its device metadata (freed by earl_plan_destroy after the plan's stream work).  The comm
+ * owns its symmetric window, the peer mappings and the signal pad.
+ */
+#ifndef EARL_DISPATCH_H_
+#define EARL_DISPATCH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define EARL_API __attribute__((visibility("default")))
+#else
+#define EARL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EARL_ABI_VERSION 1
+#define EARL_MAX_WORLD 8        /* reading c21: one box, W <= 8 */
+#define EARL_MAX_FIELDS 16
+#define EARL_HANDLE_BYTES 128   /* size of the exported window handle */
+#define EARL_ALL_RANKS (-1)     /* emulated comm: this process holds every rank */
+#define EARL_LPT_MAX_SEQS 8192  /* reading c4: LPT sorts in one CTA's shared memory */
+
+typedef enum {
+  EARL_OK = 0,
+  EARL_ERR_INVALID_ARGUMENT = 1, /* null/misaligned pointer, L_i < 0, bad enum, n_fields > 16 */
+  EARL_ERR_LAYOUT = 2,           /* dp*sp*tp ranks outside the comm, sum(counts) != N,
+                                    EXPLICIT group outside [0, dp)        */
+  EARL_ERR_CAPACITY = 3,         /* window too small, dst rank > INT32_MAX tokens (c12),
+                                    LPT with N > 8192, buffer too small                  */
+  EARL_ERR_CUDA = 4,             /* a CUDA runtime call failed                            */
+  EARL_ERR_NCCL = 5,             /* reserved                                              */
+  EARL_ERR_TIMEOUT = 6,          /* peer signals missing; mask in earl_last_error */
+  EARL_ERR_MISMATCH = 7,         /* plan hash differs across ranks (debug)                */
+  EARL_ERR_UNSUPPORTED = 8       /* world > 8, wrong comm kind for the call               */
+} earl_status_t;
+
+typedef enum {
+  EARL_ASSIGN_GIVEN_COUNTS = 0, /* group g holds seqs [sum_{h<g} counts[h], +counts[g])        */
+  EARL_ASSIGN_CONTIG = 1,       /* g(i) = min(D-1, floor(D*(2*P_i+L_i)/(2*T))), T==0 -> blocks */
+  EARL_ASSIGN_LPT = 2,          /* Graham LPT: (L desc, i asc) to least-loaded group, ties low */
+  EARL_ASSIGN_EXPLICIT = 3      /* g(i) = group_of_seq[i]                                    */
+} earl_assign_t;
+
+/* A parallel layout (reading c1/c3): ranks rank0 .. rank0+dp*sp*tp-1 of the comm, with
+ * rank(g,k,t) = rank0 + (g*sp + k)*tp + t  (TP fastest, then SP, then DP).
+ * DP group g holds the sequences assigned to it in ascending global index (reading c5);
+ * SP rank k holds BLOCK chunk k = [k*q+min(k,r), (k+1)*q+min(k+1,r)) with q = L/sp,
+ * r = L%sp of every such sequence (reading c7); every TP rank of (g,k) holds a full copy
+ * (reading c2).  When the source has several TP replicas, dst replica td is fed by source
+ * replica td mod tp_src (reading c9). */
+typedef struct {
+  int32_t rank0, dp, sp, tp;
+  int32_t assign;               /* earl_assign_t */
+  int32_t sp_split;             /* 0 = BLOCK (the only value in scope) */
+  const int64_t* counts;        /* HOST [dp], GIVEN_COUNTS only */
+  const int32_t* group_of_seq;  /* DEVICE [N], EXPLICIT only */
+} earl_layout_t;
+
+/* One per-token field: bytes_per_elem * elems_per_token bytes per token (opaque). */
+typedef struct {
+  uint32_t bytes_per_elem, elems_per_token;
+} earl_field_t;
+
+typedef struct earl_comm* earl_comm_t;
+typedef struct earl_plan* earl_plan_t;
+
+typedef struct {
+  int32_t world;
+  int32_t n_fields;
+  uint64_t bytes_per_token;               /* B = sum_f B_f */
+  uint64_t total_tokens;                  /* T */
+  uint64_t C[EARL_MAX_WORLD][EARL_MAX_WORLD]; /* payload bytes rank s -> rank d (per replica) */
+  uint64_t egress[EARL_MAX_WORLD];        /* sum_{d != s} C[s][d]   (NVLink out)            */
+  uint64_t ingress[EARL_MAX_WORLD];       /* sum_{s != d} C[s][d]   (NVLink in)             */
+  uint64_t self_bytes[EARL_MAX_WORLD];    /* C[r][r]: local copy                            */
+  uint64_t total_bytes, moved_bytes, max_egress, max_ingress;
+  uint64_t read_bytes[EARL_MAX_WORLD];    /* fused exec: source bytes read once per rank     */
+  uint64_t stage_bytes[EARL_MAX_WORLD];   /* packed message buffer size per source rank      */
+  int64_t n_local_seqs[EARL_MAX_WORLD];   /* per destination rank (0 if not in dst layout)   */
+  int64_t n_local_tokens[EARL_MAX_WORLD];
+  int64_t n_segments;                     /* canonical (uncoalesced) records incl. replicas  */
+  int64_t n_pieces;                       /* (sequence, overlap) pieces before replication   */
+  int64_t n_records;                      /* copy records (piece x sending replica)          */
+} earl_plan_stats_t;
+
+/* ---- comm -------------------------------------------------------------------------- */
+
+/* Create a comm.  rank in [0, world) for one process per GPU, or EARL_ALL_RANKS to emulate
+ * all ranks in this process on `cuda_device`.  window_bytes: size of this rank's symmetric
+ * receive window (per emulated rank in emulated mode); P2P exec writes into it.
+ * Errors: UNSUPPORTED (world outside [1,8]), INVALID_ARGUMENT, CUDA. */
+EARL_API earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t cuda_device,
+                               uint64_t window_bytes, earl_comm_t* comm);
+/* Multi-process bootstrap: export this rank's window handle (EARL_HANDLE_BYTES bytes),
+ * all-gather them out of band (e.g. torch.distributed), then import all `world` handles
+ * (rank-major).  Importing maps every peer's window (CUDA IPC over NVLink P2P). */
+EARL_API earl_status_t earl_comm_export_handle(earl_comm_t comm, void* handle_out);
+EARL_API earl_status_t earl_comm_import_peers(earl_comm_t comm, const void* handles);
+/* Collective bump allocation inside the window: every rank calls it with the same sizes in
+ * the same order and gets the same offset, so peers address it as base_peer + offset.
+ * In emulated mode `rank` selects the emulated rank's window; otherwise it is ignored.
+ * Errors: CAPACITY when the window is exhausted. */
+EARL_API earl_status_t earl_comm_alloc(earl_comm_t comm, int32_t rank, uint64_t bytes, void** dev_ptr);
+EARL_API earl_status_t earl_comm_reset_alloc(earl_comm_t comm);
+EARL_API earl_status_t earl_comm_info(earl_comm_t comm, int32_t* rank, int32_t* world, int32_t* emulated);
+EARL_API earl_status_t earl_comm_destroy(earl_comm_t comm);
+
+/* ---- plan -------------------------------------------------------------------------- */
+
+/* Plan the dispatch of N sequences from layout `src` to layout `dst`.
+ * seq_lens: DEVICE int32 [N], global index order (reading c6); L_i = 0 allowed (c11),
+ * L_i < 0 latches INVALID_ARGUMENT (c20).  fields: HOST [n_fields] (<= 16).
+ * Computes on `stream`, without a host synchronisation: P = exclusive scan of L (int64);
+ * g_src(i), g_dst(i); per-rank local token offsets; every (sequence, overlap, replica)
+ * segment with its source, destination and message offsets; per-(rank, shard) message
+ * sizes; destination metadata.  Host-side checks: layout validity (LAYOUT), N <= 8192 for
+ * LPT (CAPACITY), n_fields (INVALID_ARGUMENT).  The plan owns its device memory. */
+EARL_API earl_status_t earl_dispatch_plan(earl_comm_t comm, const earl_layout_t* src,
+                                 const earl_layout_t* dst, const int32_t* seq_lens,
+                                 int64_t n_seqs, const earl_field_t* fields, int32_t n_fields,
+                                 void* stream, earl_plan_t* plan);
+/* Wait for the plan and report device-latched errors. */
+EARL_API earl_status_t earl_plan_sync(earl_plan_t plan);
+/* Destination rank `rank`'s holding (host; synchronises): sequences and tokens. */
+EARL_API earl_status_t earl_plan_local_sizes(earl_plan_t plan, int32_t rank, int64_t* n_local_seqs,
+                                    int64_t* n_local_tokens);
+/* Destination metadata of rank `rank` written to DEVICE buffers on `stream`:
+ * cu_seqlens int32 [n_local_seqs+1], seq_ids int64 [n_local_seqs] (global index),
+ * tok_start int32 [n_local_seqs] (first token of the chunk inside its sequence).
+ * Any pointer may be NULL to skip it. */
+EARL_API earl_status_t earl_plan_local_meta(earl_plan_t plan, int32_t rank, int32_t* cu_seqlens,
+                                   int64_t* seq_ids, int32_t* tok_start, void* stream);
+/* Byte accounting of SPEC.md:239-247 (host; synchronises). */
+EARL_API earl_status_t earl_plan_stats(earl_plan_t plan, earl_plan_stats_t* stats);
+/* Debug: the canonical, uncoalesced segment table in (s, d, i, x) order (reading c19),
+ * one record per (sequence i, token overlap [x,y), destination replica): source rank s,
+ * destination rank d, source local token offset, destination local token offset.
+ * Pass capacity 0 / NULL arrays to query n_segments only (host; synchronises). */
+EARL_API earl_status_t earl_plan_export(earl_plan_t plan, int64_t capacity, int64_t* n_segments,
+                               int32_t* s, int32_t* d, int64_t* seq, int32_t* x, int32_t* y,
+                               int64_t* src_off, int64_t* dst_off);
+EARL_API earl_status_t earl_plan_destroy(earl_plan_t plan);
+
+/* ---- execution --------------------------------------------------------------------- */
+
+/* Fused dispatch (SURVEY.md §8(a) a6 + a7): every source byte is read once and stored at
+ * its final offset on every destination replica.
+ * send_bufs: DEVICE field arrays this rank holds under `src` ([n_fields]; emulated:
+ *   [world][n_fields], rank-major), each n_src_tokens(rank) * B_f bytes, 16-B aligned.
+ * recv_bufs: DEVICE field arrays under `dst`, sized n_local_tokens * B_f.  Multi-process
+ *   comm with world > 1: each must lie inside this rank's window (earl_comm_alloc) at the
+ *   same offset on every rank -- peers store into it over NVLink.  Ranks not in the dst
+ *   layout may pass NULLs.
+ * Protocol (multi-process): entry barrier (every peer's stream reached exec, so its recv
+ * buffers may be overwritten), stores, system-scope fence, release of an epoch flag into
+ * each peer's signal pad, acquire-wait for every peer's flag.  When the stream passes the
+ * call, this rank's recv buffers are complete.  A peer missing for > 10 s latches TIMEOUT. */
+EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* send_bufs,
+                                 void* const* recv_bufs, void* stream);
+/* Staged path, step a3: gather this rank's segments into one contiguous message per
+ * destination shard (field-major, each field block 16-byte aligned) in stage_bufs
+ * ([1] or emulated [world]; size earl_plan_stats().stage_bytes[rank]). */
+EARL_API earl_status_t earl_dispatch_pack(earl_plan_t plan, const void* const* send_bufs,
+                                 void* const* stage_bufs, void* stream);
+/* Staged path, step a5 (emulated comm): scatter every packed message into every
+ * destination replica's final field arrays (read once, written once per replica). */
+EARL_API earl_status_t earl_dispatch_unpack(earl_plan_t plan, const void* const* stage_bufs,
+                                   void* const* recv_bufs, void* stream);
+
+/* ---- misc -------------------------------------------------------------------------- */
+EARL_API const char* earl_status_string(earl_status_t status);
+EARL_API const char* earl_last_error(void);
+EARL_API int32_t earl_abi_version(void);
+/* Number of device kernels the library launched since load (bench evidence). */
+EARL_API uint64_t earl_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EARL_DISPATCH_H_ */

@@ -1,0 +1,777 @@
+// api.cu -- host side of libearl_dispatch.so: the C ABI of include/earl_dispatch.h.
+//
+// Owns argument validation (SURVEY.md §8(b) error list), the comm (symmetric receive windows,
+// CUDA-IPC peer mappings, signal pads), plan lifetime (stream-ordered allocations from the
+// device memory pool, so a steady-state plan allocates nothing from the driver), and the
+// launches of the planner (planner.cu) and the copy kernels (copy.cu).
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "earl_internal.cuh"
+
+using namespace earl;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+earl_status_t fail(earl_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = std::string(earl_status_string(st)) + ": " + buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(EARL_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+}  // namespace
+
+struct earl_comm {
+  int32_t rank = 0;      // EARL_ALL_RANKS when emulated
+  int32_t world = 1;
+  int32_t device = 0;
+  bool emulated = false;
+  uint64_t window_bytes = 0;
+  uint8_t* win[kMaxWorld] = {};    // local windows (emulated: one per rank; else win[rank])
+  uint8_t* peer[kMaxWorld] = {};   // every rank's window as addressable from this process
+  bool peer_mapped[kMaxWorld] = {};
+  bool peers_ready = false;
+  uint64_t alloc_off[kMaxWorld] = {};
+  uint64_t epoch = 0;
+  unsigned int* done_ctr = nullptr;
+  int sm_count = 148;
+  uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+};
+
+struct earl_plan {
+  earl_comm* comm = nullptr;
+  PlanArgs args{};
+  earl_layout_t lay[2]{};
+  int64_t N = 0;
+  int32_t n_fields = 0;
+  earl_field_t fields[kMaxFields]{};
+  void* mem = nullptr;
+  size_t mem_bytes = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool synced = false;
+  PlanHeader host_hdr{};
+};
+
+// ---------------------------------------------------------------------------------------
+// misc
+// ---------------------------------------------------------------------------------------
+
+extern "C" const char* earl_status_string(earl_status_t st) {
+  switch (st) {
+    case EARL_OK: return "EARL_OK";
+    case EARL_ERR_INVALID_ARGUMENT: return "EARL_ERR_INVALID_ARGUMENT";
+    case EARL_ERR_LAYOUT: return "EARL_ERR_LAYOUT";
+    case EARL_ERR_CAPACITY: return "EARL_ERR_CAPACITY";
+    case EARL_ERR_CUDA: return "EARL_ERR_CUDA";
+    case EARL_ERR_NCCL: return "EARL_ERR_NCCL";
+    case EARL_ERR_TIMEOUT: return "EARL_ERR_TIMEOUT";
+    case EARL_ERR_MISMATCH: return "EARL_ERR_MISMATCH";
+    case EARL_ERR_UNSUPPORTED: return "EARL_ERR_UNSUPPORTED";
+  }
+  return "EARL_ERR_UNKNOWN";
+}
+
+extern "C" const char* earl_last_error(void) { return g_last_error.c_str(); }
+extern "C" int32_t earl_abi_version(void) { return EARL_ABI_VERSION; }
+extern "C" uint64_t earl_kernel_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------------------
+// comm
+// ---------------------------------------------------------------------------------------
+
+extern "C" earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t cuda_device,
+                                          uint64_t window_bytes, earl_comm_t* out) {
+  if (!out) return fail(EARL_ERR_INVALID_ARGUMENT, "comm out-pointer is NULL");
+  *out = nullptr;
+  if (world < 1 || world > kMaxWorld)
+    return fail(EARL_ERR_UNSUPPORTED, "world %d outside [1, %d]", world, kMaxWorld);
+  if (rank != EARL_ALL_RANKS && (rank < 0 || rank >= world))
+    return fail(EARL_ERR_INVALID_ARGUMENT, "rank %d outside [0, %d)", rank, world);
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cuda_device < 0 || cuda_device >= ndev)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "cuda_device %d outside [0, %d)", cuda_device, ndev);
+  DeviceGuard g(cuda_device);
+  earl_comm* c = new earl_comm();
+  c->rank = rank;
+  c->world = world;
+  c->device = cuda_device;
+  c->emulated = (rank == EARL_ALL_RANKS);
+  c->window_bytes = ((window_bytes + 255) & ~255ull) + kPadBytes;
+  cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+  // keep freed plan memory cached in the pool: steady-state planning never calls the driver
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  auto cleanup = [&](earl_status_t st) {
+    earl_comm_destroy(c);
+    return st;
+  };
+  const int nwin = c->emulated ? world : 1;
+  for (int r = 0; r < nwin; ++r) {
+    const int rr = c->emulated ? r : rank;
+    cudaError_t e = cudaMalloc(&c->win[rr], c->window_bytes);
+    if (e != cudaSuccess)
+      return cleanup(fail(EARL_ERR_CUDA, "window cudaMalloc(%llu): %s",
+                          (unsigned long long)c->window_bytes, cudaGetErrorString(e)));
+    e = cudaMemset(c->win[rr], 0, kPadBytes);
+    if (e != cudaSuccess) return cleanup(fail(EARL_ERR_CUDA, "pad memset: %s", cudaGetErrorString(e)));
+    c->peer[rr] = c->win[rr];
+    c->alloc_off[rr] = kPadBytes;
+  }
+  cudaError_t e = cudaMalloc(&c->done_ctr, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cleanup(fail(EARL_ERR_CUDA, "comm init: %s", cudaGetErrorString(e)));
+  c->peers_ready = c->emulated || world == 1;
+  *out = c;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_export_handle(earl_comm_t c, void* handle_out) {
+  if (!c || !handle_out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm has no peers to export to");
+  static_assert(sizeof(cudaIpcMemHandle_t) <= EARL_HANDLE_BYTES, "handle size");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->win[c->rank]));
+  std::memset(handle_out, 0, EARL_HANDLE_BYTES);
+  std::memcpy(handle_out, &h, sizeof(h));
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_import_peers(earl_comm_t c, const void* handles) {
+  if (!c || !handles) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm has no peers to import");
+  DeviceGuard g(c->device);
+  const uint8_t* hb = static_cast<const uint8_t*>(handles);
+  for (int p = 0; p < c->world; ++p) {
+    if (p == c->rank || c->peer_mapped[p]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + (size_t)p * EARL_HANDLE_BYTES, sizeof(h));
+    void* ptr = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer[p] = static_cast<uint8_t*>(ptr);
+    c->peer_mapped[p] = true;
+  }
+  c->peers_ready = true;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_alloc(earl_comm_t c, int32_t rank, uint64_t bytes, void** ptr) {
+  if (!c || !ptr) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  const int r = c->emulated ? rank : c->rank;
+  if (r < 0 || r >= c->world || !c->win[r])
+    return fail(EARL_ERR_INVALID_ARGUMENT, "rank %d has no local window", rank);
+  const uint64_t need = (bytes + 255) & ~255ull;
+  if (c->alloc_off[r] + need > c->window_bytes)
+    return fail(EARL_ERR_CAPACITY, "window of rank %d exhausted: %llu + %llu > %llu", r,
+                (unsigned long long)c->alloc_off[r], (unsigned long long)need,
+                (unsigned long long)c->window_bytes);
+  *ptr = c->win[r] + c->alloc_off[r];
+  c->alloc_off[r] += need;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_reset_alloc(earl_comm_t c) {
+  if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
+  for (int r = 0; r < kMaxWorld; ++r) c->alloc_off[r] = kPadBytes;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_info(earl_comm_t c, int32_t* rank, int32_t* world,
+                                        int32_t* emulated) {
+  if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (rank) *rank = c->rank;
+  if (world) *world = c->world;
+  if (emulated) *emulated = c->emulated ? 1 : 0;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_destroy(earl_comm_t c) {
+  if (!c) return EARL_OK;
+  DeviceGuard g(c->device);
+  cudaDeviceSynchronize();
+  for (int p = 0; p < kMaxWorld; ++p)
+    if (c->peer_mapped[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  for (int r = 0; r < kMaxWorld; ++r)
+    if (c->win[r]) cudaFree(c->win[r]);
+  if (c->done_ctr) cudaFree(c->done_ctr);
+  delete c;
+  return EARL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------------------
+
+namespace {
+
+earl_status_t check_layout(const earl_layout_t* L, const char* which, int64_t N, int world) {
+  if (!L) return fail(EARL_ERR_INVALID_ARGUMENT, "%s layout is NULL", which);
+  if (L->dp < 1 || L->sp < 1 || L->tp < 1)
+    return fail(EARL_ERR_LAYOUT, "%s layout: dp, sp, tp must be >= 1", which);
+  const int64_t nr = (int64_t)L->dp * L->sp * L->tp;
+  if (L->rank0 < 0 || L->rank0 + nr > world)
+    return fail(EARL_ERR_LAYOUT, "%s layout: ranks [%d, %lld) outside the comm of %d", which,
+                L->rank0, (long long)(L->rank0 + nr), world);
+  if (L->sp_split != 0) return fail(EARL_ERR_UNSUPPORTED, "%s layout: only BLOCK SP split", which);
+  switch (L->assign) {
+    case EARL_ASSIGN_GIVEN_COUNTS: {
+      if (!L->counts) return fail(EARL_ERR_LAYOUT, "%s layout: GIVEN_COUNTS without counts", which);
+      int64_t s = 0;
+      for (int g = 0; g < L->dp; ++g) {
+        if (L->counts[g] < 0) return fail(EARL_ERR_LAYOUT, "%s layout: negative count", which);
+        s += L->counts[g];
+      }
+      if (s != N)
+        return fail(EARL_ERR_LAYOUT, "%s layout: counts sum to %lld, N = %lld", which,
+                    (long long)s, (long long)N);
+      break;
+    }
+    case EARL_ASSIGN_CONTIG: break;
+    case EARL_ASSIGN_LPT:
+      if (N > EARL_LPT_MAX_SEQS)
+        return fail(EARL_ERR_CAPACITY, "%s layout: LPT needs N <= %d (N = %lld)", which,
+                    EARL_LPT_MAX_SEQS, (long long)N);
+      break;
+    case EARL_ASSIGN_EXPLICIT:
+      if (N > 0 && !L->group_of_seq)
+        return fail(EARL_ERR_INVALID_ARGUMENT, "%s layout: EXPLICIT without group_of_seq", which);
+      break;
+    default: return fail(EARL_ERR_INVALID_ARGUMENT, "%s layout: unknown assign %d", which, L->assign);
+  }
+  return EARL_OK;
+}
+
+LayoutDesc to_desc(const earl_layout_t& L) {
+  LayoutDesc d{};
+  d.rank0 = L.rank0; d.dp = L.dp; d.sp = L.sp; d.tp = L.tp; d.assign = L.assign;
+  d.group_of_seq = L.group_of_seq;
+  d.count_start[0] = 0;
+  for (int g = 0; g < L.dp; ++g)
+    d.count_start[g + 1] = d.count_start[g] + (L.assign == EARL_ASSIGN_GIVEN_COUNTS ? L.counts[g] : 0);
+  return d;
+}
+
+template <class T>
+T* carve(uint8_t*& p, int64_t count) {
+  T* r = reinterpret_cast<T*>(p);
+  p += ((size_t)count * sizeof(T) + 255) & ~(size_t)255;
+  return r;
+}
+
+earl_status_t plan_wait(earl_plan_t p) {
+  if (p->synced) return EARL_OK;
+  DeviceGuard g(p->comm->device);
+  CUDA_TRY(cudaEventSynchronize(p->ev));
+  CUDA_TRY(cudaMemcpy(&p->host_hdr, p->args.hdr, sizeof(PlanHeader), cudaMemcpyDeviceToHost));
+  p->synced = true;
+  return EARL_OK;
+}
+
+earl_status_t plan_check(earl_plan_t p) {
+  earl_status_t st = plan_wait(p);
+  if (st != EARL_OK) return st;
+  const PlanHeader& h = p->host_hdr;
+  if (h.err != 0) {
+    switch (h.err) {
+      case EARL_ERR_INVALID_ARGUMENT:
+        return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens[%d] < 0", h.err_detail);
+      case EARL_ERR_LAYOUT:
+        return fail(EARL_ERR_LAYOUT, "group_of_seq[%d] outside [0, dp)", h.err_detail);
+      case EARL_ERR_CAPACITY:
+        return fail(EARL_ERR_CAPACITY, "dst shard %d holds more than INT32_MAX tokens", h.err_detail);
+      case EARL_ERR_TIMEOUT:
+        return fail(EARL_ERR_TIMEOUT, "peers missing (mask 0x%x)", h.err_detail);
+      default: return fail((earl_status_t)h.err, "device error %d", h.err_detail);
+    }
+  }
+  return EARL_OK;
+}
+
+// (g, k, t) of `rank` in layout L, or false.
+bool coords(const earl_layout_t& L, int rank, int* g, int* k, int* t) {
+  const int r = rank - L.rank0;
+  if (r < 0 || r >= L.dp * L.sp * L.tp) return false;
+  *t = r % L.tp;
+  *k = (r / L.tp) % L.sp;
+  *g = (r / L.tp) / L.sp;
+  return true;
+}
+
+}  // namespace
+
+extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* src,
+                                            const earl_layout_t* dst, const int32_t* seq_lens,
+                                            int64_t n_seqs, const earl_field_t* fields,
+                                            int32_t n_fields, void* stream, earl_plan_t* out) {
+  if (!c || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm or plan out-pointer");
+  *out = nullptr;
+  if (n_seqs < 0 || n_seqs > 0x7fffffffLL)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "n_seqs %lld outside [0, 2^31)", (long long)n_seqs);
+  if (n_seqs > 0 && !seq_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens is NULL");
+  if (n_fields < 1 || n_fields > kMaxFields || !fields)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "n_fields %d outside [1, %d]", n_fields, kMaxFields);
+  for (int f = 0; f < n_fields; ++f) {
+    const uint64_t b = (uint64_t)fields[f].bytes_per_elem * fields[f].elems_per_token;
+    if (b == 0 || b > (1u << 24))
+      return fail(EARL_ERR_INVALID_ARGUMENT, "field %d has %llu bytes per token", f,
+                  (unsigned long long)b);
+  }
+  earl_status_t st;
+  if ((st = check_layout(src, "src", n_seqs, c->world)) != EARL_OK) return st;
+  if ((st = check_layout(dst, "dst", n_seqs, c->world)) != EARL_OK) return st;
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  earl_plan* p = new earl_plan();
+  p->comm = c;
+  p->N = n_seqs;
+  p->n_fields = n_fields;
+  p->stream = s;
+  p->lay[0] = *src;
+  p->lay[1] = *dst;
+  p->lay[0].counts = p->lay[1].counts = nullptr;  // host arrays are consumed now
+  std::memcpy(p->fields, fields, sizeof(earl_field_t) * n_fields);
+
+  PlanArgs& a = p->args;
+  a.lay[0] = to_desc(*src);
+  a.lay[1] = to_desc(*dst);
+  a.N = n_seqs;
+  a.world = c->world;
+  a.n_fields = n_fields;
+  for (int f = 0; f < n_fields; ++f) a.Bf[f] = fields[f].bytes_per_elem * fields[f].elems_per_token;
+  a.seq_lens = seq_lens;
+  const int64_t N = n_seqs;
+  const int64_t max_pieces = N * (src->sp + dst->sp - 1);
+  const int64_t nts = src->tp < dst->tp ? src->tp : dst->tp;
+  const int64_t max_records = max_pieces * nts;
+  a.max_pieces = max_pieces;
+  a.max_records = max_records;
+
+  // size the single allocation (every array 256-B aligned)
+  auto sz = [](int64_t count, size_t elem) { return ((size_t)count * elem + 255) & ~(size_t)255; };
+  size_t total = sz(1, sizeof(PlanHeader));
+  total += sz(N, 4) + sz(N + 1, 8) + 2 * sz(N, 4) + 2 * sz(N, 4);
+  total += sz((int64_t)src->sp * N, 8) + sz((int64_t)dst->sp * N, 8);
+  total += sz((int64_t)src->sp * (N + 1), 8) + sz((int64_t)dst->sp * (N + 1), 8);
+  total += sz(N + 1, 8);
+  total += 8 * sz(max_pieces, 4) + sz(max_pieces + 1, 8);
+  total += 4 * sz(max_records, 4) + 3 * sz(max_records, 8) + sz(max_records + 1, 8);
+  p->mem_bytes = total;
+  cudaError_t e = cudaMallocAsync(&p->mem, total, s);
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(EARL_ERR_CUDA, "plan cudaMallocAsync(%zu): %s", total, cudaGetErrorString(e));
+  }
+  uint8_t* q = static_cast<uint8_t*>(p->mem);
+  a.hdr = carve<PlanHeader>(q, 1);
+  a.lens = carve<int32_t>(q, N);
+  a.P = carve<int64_t>(q, N + 1);
+  a.grp[0] = carve<int32_t>(q, N);
+  a.grp[1] = carve<int32_t>(q, N);
+  a.perm[0] = carve<int32_t>(q, N);
+  a.perm[1] = carve<int32_t>(q, N);
+  a.off[0] = carve<int64_t>(q, (int64_t)src->sp * N);
+  a.off[1] = carve<int64_t>(q, (int64_t)dst->sp * N);
+  a.cum[0] = carve<int64_t>(q, (int64_t)src->sp * (N + 1));
+  a.cum[1] = carve<int64_t>(q, (int64_t)dst->sp * (N + 1));
+  a.pbase = carve<int64_t>(q, N + 1);
+  a.pc_i = carve<int32_t>(q, max_pieces);
+  a.pc_x = carve<int32_t>(q, max_pieces);
+  a.pc_y = carve<int32_t>(q, max_pieces);
+  a.pc_kk = carve<int32_t>(q, max_pieces);
+  a.ps_i = carve<int32_t>(q, max_pieces);
+  a.ps_x = carve<int32_t>(q, max_pieces);
+  a.ps_y = carve<int32_t>(q, max_pieces);
+  a.ps_kk = carve<int32_t>(q, max_pieces);
+  a.ps_scan = carve<int64_t>(q, max_pieces + 1);
+  a.rec.seq = carve<int32_t>(q, max_records);
+  a.rec.x = carve<int32_t>(q, max_records);
+  a.rec.n = carve<int32_t>(q, max_records);
+  a.rec.code = carve<uint32_t>(q, max_records);
+  a.rec.src_tok = carve<int64_t>(q, max_records);
+  a.rec.dst_tok = carve<int64_t>(q, max_records);
+  a.rec.msg_tok = carve<int64_t>(q, max_records);
+  a.rec.tok_prefix = carve<int64_t>(q, max_records + 1);
+
+  auto abort_plan = [&](earl_status_t code, const char* what, cudaError_t err) {
+    cudaFreeAsync(p->mem, s);
+    delete p;
+    return fail(code, "%s: %s", what, cudaGetErrorString(err));
+  };
+  e = cudaMemsetAsync(a.hdr, 0, sizeof(PlanHeader), s);
+  if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "header memset", e);
+  const bool lpt = src->assign == EARL_ASSIGN_LPT || dst->assign == EARL_ASSIGN_LPT;
+  size_t lpt_smem = 0;
+  if (lpt) {
+    int64_t n2 = 1;
+    while (n2 < N) n2 <<= 1;
+    lpt_smem = (size_t)n2 * sizeof(uint64_t);
+  }
+  e = launch_planner(a, lpt_smem, s);
+  if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "planner launch", e);
+  g_launches.fetch_add(1);
+  e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(p->ev, s);
+  if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "plan event", e);
+  *out = p;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_sync(earl_plan_t p) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  p->synced = false;  // re-read: exec may have latched a TIMEOUT
+  return plan_check(p);
+}
+
+extern "C" earl_status_t earl_plan_local_sizes(earl_plan_t p, int32_t rank, int64_t* n_seqs,
+                                               int64_t* n_tokens) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  int g, k, t;
+  int64_t ns = 0, nt = 0;
+  if (coords(p->lay[1], rank, &g, &k, &t)) {
+    ns = p->host_hdr.group_count[1][g];
+    nt = p->host_hdr.shard_tokens[1][g * p->lay[1].sp + k];
+  }
+  if (n_seqs) *n_seqs = ns;
+  if (n_tokens) *n_tokens = nt;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_local_meta(earl_plan_t p, int32_t rank, int32_t* cu,
+                                              int64_t* ids, int32_t* tok_start, void* stream) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  int g, k, t;
+  if (!coords(p->lay[1], rank, &g, &k, &t)) return EARL_OK;  // not a destination: nothing
+  DeviceGuard dg(p->comm->device);
+  cudaError_t e = launch_local_meta(p->args, g, k, cu, ids, tok_start, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "local_meta launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_stats(earl_plan_t p, earl_plan_stats_t* out) {
+  if (!p || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  const PlanHeader& h = p->host_hdr;
+  const earl_layout_t& S = p->lay[0];
+  const earl_layout_t& D = p->lay[1];
+  const int W = p->comm->world;
+  std::memset(out, 0, sizeof(*out));
+  out->world = W;
+  out->n_fields = p->n_fields;
+  uint64_t B = 0;
+  for (int f = 0; f < p->n_fields; ++f) B += p->args.Bf[f];
+  out->bytes_per_token = B;
+  out->total_tokens = (uint64_t)h.T;
+  const int Sd = D.dp * D.sp;
+  const int nts = S.tp < D.tp ? S.tp : D.tp;
+  int64_t nseg = 0;
+  for (int s = 0; s < W; ++s) {
+    int gs, ks, ts;
+    if (!coords(S, s, &gs, &ks, &ts) || ts >= nts) continue;
+    const int ss = gs * S.sp + ks;
+    out->stage_bytes[s] = (uint64_t)h.stage_bytes_shard[ss];
+    for (int ds = 0; ds < Sd; ++ds) {
+      const uint64_t bytes = (uint64_t)h.key_tokens[ss * Sd + ds] * B;
+      out->read_bytes[s] += bytes;
+      for (int td = ts; td < D.tp; td += S.tp) {
+        const int d = D.rank0 + ds * D.tp + td;
+        out->C[s][d] += bytes;
+        nseg += h.key_pieces[ss * Sd + ds];
+      }
+    }
+  }
+  for (int s = 0; s < W; ++s)
+    for (int d = 0; d < W; ++d) {
+      out->total_bytes += out->C[s][d];
+      if (s == d) out->self_bytes[s] += out->C[s][d];
+      else { out->egress[s] += out->C[s][d]; out->ingress[d] += out->C[s][d]; }
+    }
+  for (int r = 0; r < W; ++r) {
+    out->moved_bytes += out->egress[r];
+    if (out->egress[r] > out->max_egress) out->max_egress = out->egress[r];
+    if (out->ingress[r] > out->max_ingress) out->max_ingress = out->ingress[r];
+    int g, k, t;
+    if (coords(D, r, &g, &k, &t)) {
+      out->n_local_seqs[r] = h.group_count[1][g];
+      out->n_local_tokens[r] = h.shard_tokens[1][g * D.sp + k];
+    }
+  }
+  out->n_segments = nseg;
+  out->n_pieces = h.n_pieces;
+  out->n_records = h.n_records;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_export(earl_plan_t p, int64_t capacity, int64_t* n_segments,
+                                          int32_t* s_out, int32_t* d_out, int64_t* seq_out,
+                                          int32_t* x_out, int32_t* y_out, int64_t* so_out,
+                                          int64_t* do_out) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  earl_plan_stats_t st;
+  earl_status_t r = earl_plan_stats(p, &st);
+  if (r != EARL_OK) return r;
+  if (n_segments) *n_segments = st.n_segments;
+  if (capacity == 0) return EARL_OK;
+  if (capacity < st.n_segments)
+    return fail(EARL_ERR_CAPACITY, "export capacity %lld < %lld segments", (long long)capacity,
+                (long long)st.n_segments);
+  if (!s_out || !d_out || !seq_out || !x_out || !y_out || !so_out || !do_out)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "export arrays must be non-NULL");
+  const PlanHeader& h = p->host_hdr;
+  const int64_t M = h.n_records;
+  DeviceGuard g(p->comm->device);
+  std::vector<int32_t> seq(M), x(M), n(M);
+  std::vector<uint32_t> code(M);
+  std::vector<int64_t> st_(M), dt(M);
+  const Records& R = p->args.rec;
+  if (M > 0) {
+    CUDA_TRY(cudaMemcpy(seq.data(), R.seq, M * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(x.data(), R.x, M * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(n.data(), R.n, M * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(code.data(), R.code, M * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(st_.data(), R.src_tok, M * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(dt.data(), R.dst_tok, M * 8, cudaMemcpyDeviceToHost));
+  }
+  // canonical (s, d, i, x): records are (s, ds, i, x); replicas td of a record follow ds.
+  const earl_layout_t& S = p->lay[0];
+  const earl_layout_t& D = p->lay[1];
+  const int Sd = D.dp * D.sp;
+  int64_t o = 0;
+  for (int s = 0; s < p->comm->world; ++s) {
+    int gs, ks, ts;
+    if (!coords(S, s, &gs, &ks, &ts)) continue;
+    for (int ds = 0; ds < Sd; ++ds) {
+      const int64_t b = h.rec_base[s][ds];
+      const int64_t e = (ds + 1 < Sd) ? h.rec_base[s][ds + 1] : h.rec_begin[s + 1];
+      for (int td = ts; td < D.tp; td += S.tp) {
+        const int d = D.rank0 + ds * D.tp + td;
+        for (int64_t j = b; j < e; ++j) {
+          s_out[o] = s; d_out[o] = d; seq_out[o] = seq[j]; x_out[o] = x[j];
+          y_out[o] = x[j] + n[j]; so_out[o] = st_[j]; do_out[o] = dt[j];
+          ++o;
+        }
+      }
+    }
+  }
+  if (o != st.n_segments)
+    return fail(EARL_ERR_CUDA, "export produced %lld segments, stats say %lld", (long long)o,
+                (long long)st.n_segments);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_destroy(earl_plan_t p) {
+  if (!p) return EARL_OK;
+  DeviceGuard g(p->comm->device);
+  if (p->mem) cudaFreeAsync(p->mem, p->stream);
+  if (p->ev) cudaEventDestroy(p->ev);
+  delete p;
+  return EARL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// execution
+// ---------------------------------------------------------------------------------------
+
+namespace {
+
+earl_status_t fill_copy_args(earl_plan_t p, CopyArgs& a, int mode) {
+  earl_comm* c = p->comm;
+  std::memset(&a, 0, sizeof(a));
+  const earl_layout_t& S = p->lay[0];
+  const earl_layout_t& D = p->lay[1];
+  a.mode = mode;
+  a.n_fields = p->n_fields;
+  a.view_rank = c->emulated ? -1 : c->rank;
+  a.nts = S.tp < D.tp ? S.tp : D.tp;
+  a.rank0_s = S.rank0; a.tp_s = S.tp;
+  a.rank0_d = D.rank0; a.tp_d = D.tp; a.sp_d = D.sp; a.n_dst_shards = D.dp * D.sp;
+  a.Bpre[0] = 0;
+  for (int f = 0; f < p->n_fields; ++f) {
+    a.Bf[f] = p->args.Bf[f];
+    a.Bpre[f + 1] = a.Bpre[f] + a.Bf[f];
+  }
+  a.hdr = p->args.hdr;
+  a.rec = p->args.rec;
+  a.world = c->world;
+  a.me = c->emulated ? -1 : c->rank;
+  a.done_ctr = c->done_ctr;
+  a.timeout_ns = c->timeout_ns;
+  a.err = &p->args.hdr->err;
+  a.err_detail = &p->args.hdr->err_detail;
+  return EARL_OK;
+}
+
+int copy_grid(earl_comm* c) { return c->sm_count * 2; }
+
+// Source arrays (direct/pack): emulated [world][F], else [F] for this rank.
+earl_status_t set_src(earl_plan_t p, CopyArgs& a, const void* const* bufs) {
+  earl_comm* c = p->comm;
+  const int F = p->n_fields;
+  if (!bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "send_bufs is NULL");
+  const int nr = c->emulated ? c->world : 1;
+  for (int r = 0; r < nr; ++r) {
+    const int rr = c->emulated ? r : c->rank;
+    for (int f = 0; f < F; ++f) {
+      const void* ptr = bufs[r * F + f];
+      if (ptr && !aligned16(ptr))
+        return fail(EARL_ERR_INVALID_ARGUMENT, "send buffer rank %d field %d not 16-B aligned", rr, f);
+      a.src[rr][f] = static_cast<const uint8_t*>(ptr);
+    }
+  }
+  return EARL_OK;
+}
+
+}  // namespace
+
+extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* send_bufs,
+                                            void* const* recv_bufs, void* stream) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  earl_comm* c = p->comm;
+  if (!c->peers_ready)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "multi-process comm: earl_comm_import_peers not called");
+  if (!recv_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "recv_bufs is NULL");
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CopyArgs a;
+  fill_copy_args(p, a, kDirect);
+  earl_status_t st = set_src(p, a, send_bufs);
+  if (st != EARL_OK) return st;
+  const int F = p->n_fields;
+  if (c->emulated) {
+    for (int r = 0; r < c->world; ++r)
+      for (int f = 0; f < F; ++f) {
+        void* ptr = recv_bufs[r * F + f];
+        if (ptr && !aligned16(ptr))
+          return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer rank %d field %d not 16-B aligned", r, f);
+        a.dst[r][f] = static_cast<uint8_t*>(ptr);
+      }
+  } else {
+    // peers store into my recv buffers through their mapping of my window: same offset
+    for (int f = 0; f < F; ++f) {
+      uint8_t* ptr = static_cast<uint8_t*>(recv_bufs[f]);
+      if (!ptr) continue;
+      if (!aligned16(ptr))
+        return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer field %d not 16-B aligned", f);
+      uint8_t* base = c->win[c->rank];
+      if (c->world > 1 && (ptr < base + kPadBytes || ptr >= base + c->window_bytes))
+        return fail(EARL_ERR_INVALID_ARGUMENT,
+                    "recv buffer field %d is not inside this rank's window (use earl_comm_alloc)", f);
+      const uint64_t off = (uint64_t)(ptr - base);
+      for (int d = 0; d < c->world; ++d) a.dst[d][f] = c->peer[d] ? c->peer[d] + off : nullptr;
+    }
+    if (c->world == 1)
+      for (int f = 0; f < F; ++f) a.dst[0][f] = static_cast<uint8_t*>(recv_bufs[f]);
+  }
+  if (!c->emulated && c->world > 1) {
+    c->epoch += 1;
+    a.epoch = c->epoch;
+    a.my_pad = reinterpret_cast<uint64_t*>(c->win[c->rank]);
+    uint64_t* pads[kMaxWorld] = {};
+    for (int q = 0; q < c->world; ++q) pads[q] = reinterpret_cast<uint64_t*>(c->peer[q]);
+    for (int q = 0; q < kMaxWorld; ++q) a.peer_pad[q] = pads[q];
+    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, a.epoch, c->timeout_ns,
+                                         a.err, a.err_detail, s);
+    if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
+    g_launches.fetch_add(1);
+  }
+  cudaError_t e = launch_copy(a, copy_grid(c), 512, s);
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "copy launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  p->synced = false;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* send_bufs,
+                                            void* const* stage_bufs, void* stream) {
+  if (!p || !stage_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  earl_comm* c = p->comm;
+  DeviceGuard g(c->device);
+  CopyArgs a;
+  fill_copy_args(p, a, kPack);
+  earl_status_t st = set_src(p, a, send_bufs);
+  if (st != EARL_OK) return st;
+  const int nr = c->emulated ? c->world : 1;
+  for (int r = 0; r < nr; ++r) {
+    const int rr = c->emulated ? r : c->rank;
+    if (stage_bufs[r] && !aligned16(stage_bufs[r]))
+      return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", rr);
+    a.stage[rr] = static_cast<uint8_t*>(stage_bufs[r]);
+  }
+  a.world = 1;  // no completion protocol: pack is rank-local
+  cudaError_t e = launch_copy(a, copy_grid(c), 512, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* stage_bufs,
+                                              void* const* recv_bufs, void* stream) {
+  if (!p || !stage_bufs || !recv_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  earl_comm* c = p->comm;
+  if (!c->emulated)
+    return fail(EARL_ERR_UNSUPPORTED, "unpack of received messages needs an emulated comm");
+  DeviceGuard g(c->device);
+  CopyArgs a;
+  fill_copy_args(p, a, kUnpack);
+  const int F = p->n_fields;
+  for (int r = 0; r < c->world; ++r) {
+    if (stage_bufs[r] && !aligned16(stage_bufs[r]))
+      return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", r);
+    a.stage[r] = const_cast<uint8_t*>(static_cast<const uint8_t*>(stage_bufs[r]));
+    for (int f = 0; f < F; ++f) {
+      void* ptr = recv_bufs[r * F + f];
+      if (ptr && !aligned16(ptr))
+        return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer rank %d field %d not 16-B aligned", r, f);
+      a.dst[r][f] = static_cast<uint8_t*>(ptr);
+    }
+  }
+  a.world = 1;
+  cudaError_t e = launch_copy(a, copy_grid(c), 512, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "unpack launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  return EARL_OK;
+}

@@ -1,0 +1,131 @@
+// earl_internal.cuh -- device-side data structures shared by the planner, the copy kernels
+// and the host glue of libearl_dispatch.so.  (Not part of the C ABI.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/earl_dispatch.h"
+
+namespace earl {
+
+constexpr int kMaxWorld = EARL_MAX_WORLD;   // 8
+constexpr int kMaxFields = EARL_MAX_FIELDS; // 16
+constexpr int kMaxShards = 8;               // dp*sp <= world <= 8 per layout
+constexpr int kMaxKeys = kMaxShards * kMaxShards;  // (src shard, dst shard) message keys
+constexpr int kPlanThreads = 1024;          // the planner is one CTA
+constexpr int kPadBytes = 4096;             // signal pad at the start of every window
+
+// Layout as the device sees it.  shard = g*sp + k ; rank = rank0 + shard*tp + t.
+struct LayoutDesc {
+  int32_t rank0, dp, sp, tp, assign;
+  int32_t pad_;
+  int64_t count_start[kMaxShards + 1];  // GIVEN_COUNTS: prefix of counts
+  const int32_t* group_of_seq;          // EXPLICIT
+};
+
+// Written by the planner into device memory; read by the copy kernels and (after a sync)
+// by the host.  Small fixed-size tables only.
+struct PlanHeader {
+  int32_t err;          // earl_status_t latched on the device (first error wins)
+  int32_t err_detail;   // e.g. peer mask for TIMEOUT, offending index for LAYOUT
+  int64_t T;            // total tokens
+  int64_t n_pieces;
+  int64_t n_records;
+  int64_t rec_tokens;   // tokens over all records
+  int64_t group_count[2][kMaxShards];
+  int64_t group_start[2][kMaxShards + 1];
+  int64_t shard_tokens[2][kMaxShards];      // tokens held per shard (g*sp+k) of each layout
+  int64_t key_pieces[kMaxKeys];
+  int64_t key_piece_start[kMaxKeys + 1];
+  int64_t key_tokens[kMaxKeys];             // tokens of message key (ss, ds)
+  int64_t msg_off[kMaxKeys];                // byte offset of message (ss, ds) in a stage buffer
+  int64_t stage_bytes_shard[kMaxShards];    // stage buffer size of a rank of src shard ss
+  int64_t rec_begin[kMaxWorld + 1];         // records of source comm rank r: [rec_begin[r], rec_begin[r+1])
+  int64_t rec_tok_begin[kMaxWorld + 1];     // tokens of those records (prefix)
+  int64_t rec_base[kMaxWorld][kMaxShards];  // first record of block (s, ds)
+  int64_t rec_tok_base[kMaxWorld][kMaxShards];
+};
+
+// Copy records: one per (piece, sending replica ts < min(tp_src, tp_dst)), ordered by
+// (s, ds, i, x).  A record feeds destination replicas td = ts, ts+tp_src, ... < tp_dst.
+struct Records {
+  int32_t* seq;       // global sequence index i
+  int32_t* x;         // first token of the piece inside sequence i
+  int32_t* n;         // tokens in the piece (y - x)
+  uint32_t* code;     // s | ss<<8 | ds<<16 | ts<<24
+  int64_t* src_tok;   // token offset in the source rank's field arrays
+  int64_t* dst_tok;   // token offset in each destination replica's field arrays
+  int64_t* msg_tok;   // token offset inside message (ss, ds)
+  int64_t* tok_prefix;// [n_records + 1]: token prefix over records (= rec_tok_base + msg_tok)
+};
+
+struct PlanArgs {
+  LayoutDesc lay[2];  // 0 = src, 1 = dst
+  int64_t N;
+  int32_t world;
+  int32_t n_fields;
+  uint32_t Bf[kMaxFields];
+  const int32_t* seq_lens;   // user's device array
+  PlanHeader* hdr;
+  // per-sequence scratch
+  int32_t* lens;             // [N]
+  int64_t* P;                // [N+1]
+  int32_t* grp[2];           // [N]
+  int32_t* perm[2];          // [N] sorted position -> i
+  int64_t* off[2];           // [sp][N] local token offset of chunk k of sequence i
+  int64_t* cum[2];           // [sp][N+1] scan of chunk lengths in sorted order
+  int64_t* pbase;            // [N+1] piece base per sequence
+  // pieces (unsorted, then sorted by key)
+  int32_t* pc_i; int32_t* pc_x; int32_t* pc_y; int32_t* pc_kk;  // kk = ks | kd<<8 | key<<16
+  int32_t* ps_i; int32_t* ps_x; int32_t* ps_y; int32_t* ps_kk;
+  int64_t* ps_scan;          // [max_pieces+1]
+  int64_t max_pieces;
+  int64_t max_records;
+  Records rec;
+};
+
+struct PeerPads {
+  uint64_t* p[kMaxWorld];
+};
+
+enum CopyMode { kDirect = 0, kPack = 1, kUnpack = 2 };
+
+struct CopyArgs {
+  int32_t mode;
+  int32_t n_fields;
+  int32_t view_rank;       // -1: every record (emulated); else records of source rank view_rank
+  int32_t nts;             // min(tp_src, tp_dst)
+  int32_t rank0_s, tp_s, rank0_d, tp_d, sp_d, n_dst_shards;
+  uint32_t Bf[kMaxFields];
+  uint64_t Bpre[kMaxFields + 1];  // prefix of Bf
+  const PlanHeader* hdr;
+  Records rec;
+  const uint8_t* src[kMaxWorld][kMaxFields];  // per source comm rank (direct/pack)
+  uint8_t* dst[kMaxWorld][kMaxFields];        // per destination comm rank (direct/unpack)
+  uint8_t* stage[kMaxWorld];                  // per source comm rank (pack dst / unpack src)
+  // completion protocol for a multi-process comm (view_rank >= 0 && world > 1)
+  int32_t world;
+  int32_t me;
+  unsigned int* done_ctr;                     // device counter for the last-CTA pattern
+  uint64_t* my_pad;                           // this rank's signal pad (local)
+  uint64_t* peer_pad[kMaxWorld];              // peers' signal pads (mapped)
+  uint64_t epoch;
+  uint64_t timeout_ns;
+  int32_t* err;                               // where to latch TIMEOUT (plan header)
+  int32_t* err_detail;
+};
+
+// signal pad slots (uint64 each): [0, 8) ready flags written by peer p at p; [8, 16) done flags
+constexpr int kReadySlot = 0;
+constexpr int kDoneSlot = 8;
+
+// launchers (defined in the .cu files)
+cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
+                                 uint64_t epoch, uint64_t timeout_ns, int32_t* err,
+                                 int32_t* err_detail, cudaStream_t s);
+cudaError_t launch_local_meta(const PlanArgs& a, int rank_g, int rank_k, int32_t* cu, int64_t* ids,
+                              int32_t* tok_start, cudaStream_t s);
+
+}  // namespace earl

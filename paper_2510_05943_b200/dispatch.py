@@ -1,0 +1,143 @@
+"""User-facing dispatch helpers over the C ABI (torch tensors in, torch tensors out).
+
+* ``EmulatedDispatch`` -- one process holds every rank on one GPU (the 1-GPU measurement and
+  test mode of SURVEY.md §8(d)); one launch serves all ranks.
+* ``Dispatcher`` -- one process per GPU under torch.distributed: bootstraps the comm (CUDA-IPC
+  window handles are all-gathered over the process group), all-gathers the local lengths
+  (step a1; plumbing over the process group), plans on the device and runs the fused P2P
+  exchange into symmetric receive windows.
+
+Every byte of the dispatch moves in libearl_dispatch.so's kernels; this module only allocates
+tensors and passes pointers.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import earl
+from .earl import EARL_ALL_RANKS, Comm
+
+
+def field_bytes(fields):
+    return [int(f[1]) * int(f[2]) for f in fields]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of raw device memory (lets torch alias the comm window)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {
+            "shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+            "version": 3, "strides": None,
+        }
+
+
+def window_tensor(ptr: int, nbytes: int, device) -> torch.Tensor:
+    if nbytes == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    return torch.as_tensor(_CudaArray(ptr, nbytes), device=device)
+
+
+def layout_for_device(lay: dict, device) -> dict:
+    """Copy EXPLICIT group_of_seq to the device (the C ABI takes a device pointer)."""
+    out = dict(lay)
+    gos = lay.get("group_of_seq")
+    if lay.get("assign") == "explicit" and gos is not None:
+        t = torch.as_tensor(np.asarray(gos, dtype=np.int32)).to(device)
+        out["group_of_seq_dev"] = t
+    return out
+
+
+class EmulatedDispatch:
+    """All `world` ranks in this process on one device."""
+
+    def __init__(self, world: int, device: int = 0, window_bytes: int = 0):
+        self.world = int(world)
+        self.device = torch.device("cuda", device)
+        self.comm = Comm(EARL_ALL_RANKS, self.world, device, window_bytes)
+
+    def plan(self, src, dst, seq_lens, fields, stream=None):
+        lens = torch.as_tensor(np.asarray(seq_lens, dtype=np.int32)).to(self.device) \
+            if not isinstance(seq_lens, torch.Tensor) else seq_lens
+        self._src = layout_for_device(src, self.device)
+        self._dst = layout_for_device(dst, self.device)
+        return self.comm.plan(self._src, self._dst, lens, fields, stream)
+
+    def alloc_recv(self, plan, fields):
+        """Per-rank, per-field uint8 receive tensors sized from the plan (host sync)."""
+        st = plan.stats()
+        Bf = field_bytes(fields)
+        return [[torch.empty(int(st["n_local_tokens"][r]) * b, dtype=torch.uint8, device=self.device)
+                 for b in Bf] for r in range(self.world)]
+
+    def alloc_stage(self, plan):
+        st = plan.stats()
+        return [torch.empty(max(16, int(st["stage_bytes"][r])), dtype=torch.uint8, device=self.device)
+                for r in range(self.world)]
+
+    @staticmethod
+    def flat(per_rank):
+        return [t for row in per_rank for t in row]
+
+    def meta(self, plan, rank):
+        ns, nt = plan.local_sizes(rank)
+        cu = torch.empty(ns + 1, dtype=torch.int32, device=self.device)
+        ids = torch.empty(max(ns, 1), dtype=torch.int64, device=self.device)
+        ts = torch.empty(max(ns, 1), dtype=torch.int32, device=self.device)
+        plan.local_meta(rank, cu, ids, ts)
+        return cu, ids[:ns], ts[:ns]
+
+
+class Dispatcher:
+    """One process per GPU (torch.distributed initialised).  Fused P2P exchange."""
+
+    def __init__(self, window_bytes: int, device=None, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.comm = Comm(self.rank, self.world, self.device.index, window_bytes)
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.comm.export_handle(), group=group)
+            self.comm.import_peers(handles)
+
+    def allgather_lens(self, local_lens: torch.Tensor):
+        """Step a1: every rank learns the global lengths (counts first, then padded lengths).
+        Returns (global int32 device tensor, per-rank counts list)."""
+        dist = self.dist
+        n = torch.tensor([local_lens.numel()], dtype=torch.int64, device=self.device)
+        counts = [torch.zeros_like(n) for _ in range(self.world)]
+        dist.all_gather(counts, n, group=self.group)
+        counts = [int(c.item()) for c in counts]
+        m = max(counts) if counts else 0
+        pad = torch.zeros(max(m, 1), dtype=torch.int32, device=self.device)
+        pad[: local_lens.numel()] = local_lens.to(torch.int32)
+        allp = [torch.zeros_like(pad) for _ in range(self.world)]
+        dist.all_gather(allp, pad, group=self.group)
+        glob = torch.cat([allp[r][: counts[r]] for r in range(self.world)]) if m else \
+            torch.zeros(0, dtype=torch.int32, device=self.device)
+        return glob, counts
+
+    def plan(self, src, dst, seq_lens: torch.Tensor, fields, stream=None):
+        self._src = layout_for_device(src, self.device)
+        self._dst = layout_for_device(dst, self.device)
+        return self.comm.plan(self._src, self._dst, seq_lens, fields, stream)
+
+    def alloc_recv(self, plan, fields):
+        """Receive tensors inside the symmetric window: same offsets on every rank, sized for
+        the largest destination rank (every rank knows every size: the plan is replicated)."""
+        st = plan.stats()
+        self.comm.reset_alloc()
+        full, views = [], []
+        n_max = max(st["n_local_tokens"]) if st["n_local_tokens"] else 0
+        mine = int(st["n_local_tokens"][self.rank])
+        for b in field_bytes(fields):
+            ptr = self.comm.alloc(max(16, n_max * b))
+            full.append(ptr)
+            views.append(window_tensor(ptr, max(16, n_max * b), self.device)[: mine * b])
+        # exec takes the raw window pointers (valid even when this rank receives 0 bytes)
+        return full, views

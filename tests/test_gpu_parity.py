@@ -1,0 +1,204 @@
+"""GPU parity: libearl_dispatch.so (called through the C ABI) against the CPU oracle.
+
+Bit-exact on every byte of every destination rank, on the destination metadata (cu_seqlens,
+seq_ids, tok_start), on the canonical plan table and on the byte accounting.  Payloads are
+random bits (no float path can hide), receive buffers have 0xA5 guard bands on both sides.
+"""
+import random
+
+import numpy as np
+import pytest
+
+from oracle import earl_oracle as O
+from paper_2510_05943_b200 import workloads as W
+from tests.helpers import random_layout, run_gpu_case
+
+pytestmark = pytest.mark.gpu
+
+GOLD_LENS = W.TINY_LENGTHS.tolist()
+ODD_FIELDS = [("a", 4, 1, "x"), ("m", 1, 1, "x"), ("b", 2, 1, "x"), ("c", 1, 3, "x"),
+              ("h", 2, 8, "x"), ("w", 2, 7, "x")]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+
+
+@pytest.mark.parametrize("mode", ["exec", "stage"])
+def test_c1_tiny_dp2_to_dp1(mode):
+    src = W.rollout_layout(8, 2)
+    dst = W.layout(dp=1, assign="contig")
+    st = run_gpu_case(src, dst, GOLD_LENS, W.field_set("tiny3"), 2, mode=mode)
+    assert st["moved"] == 1368 and st["total"] == 2508  # tests/golden/c1_tiny.json
+
+
+@pytest.mark.parametrize("dst", [
+    dict(dp=2, assign="contig"), dict(dp=2, assign="lpt"), dict(dp=1, sp=2, assign="contig"),
+    dict(dp=1, tp=2, assign="contig"), dict(dp=2, assign="explicit", group_of_seq=[1, 0] * 4),
+])
+def test_c1_variants(dst):
+    run_gpu_case(W.rollout_layout(8, 2), W.layout(**dst), GOLD_LENS, W.field_set("tiny3"), 2)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_layouts(seed):
+    rng = random.Random(seed)
+    world = rng.randint(1, 8)
+    n = rng.choice([0, 1, 3, rng.randint(0, 40), rng.randint(40, 300)])
+    lens = [rng.choice([0, 1, 2, 15, 16, 17, rng.randint(0, 200), rng.randint(0, 3000)])
+            for _ in range(n)]
+    src = random_layout(rng, world, n)
+    dst = random_layout(rng, world, n)
+    fields = rng.sample(ODD_FIELDS, rng.randint(1, len(ODD_FIELDS)))
+    run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
+
+
+@pytest.mark.parametrize("n_gpus", [2, 4, 8])
+def test_c3_layouts_scalar6(n_gpus):
+    """Config 3 shape (DPn -> DP max(1,n/4) x TP min(4,n)) on a 128-sequence slice of config 2."""
+    lens = W.c2_lengths(0)[:128].tolist()
+    src, dst = W.config_layouts("c3", n_gpus, len(lens))
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-fp32"), n_gpus, seed=n_gpus)
+
+
+@pytest.mark.parametrize("n_gpus", [2, 4, 8])
+def test_c4_layouts_sp2(n_gpus):
+    """Config 4 shape (DPn -> DP n/2 x SP2) on 24 long sequences (4K-32K)."""
+    lens = W.c4_lengths(0)[:24].tolist()
+    src, dst = W.config_layouts("c4", n_gpus, len(lens))
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-bf16"), n_gpus, seed=10 + n_gpus,
+                 mode="stage" if n_gpus == 4 else "exec")
+
+
+def test_c2_full_scalar6_exec_and_stage():
+    """BASELINE.json configs[1] at full size (512 episodes) with the scalar6 fields, 8-rank
+    emulation of rollout DP8 -> train DP2 x TP4, element by element against the oracle."""
+    lens = W.c2_lengths(0).tolist()
+    src, dst = W.config_layouts("c2", 8, len(lens))
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-fp32"), 8, mode="exec", seed=1)
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-fp32"), 8, mode="stage", seed=2)
+
+
+def test_c2_lpt_rebalance():
+    lens = W.c2_lengths(0).tolist()
+    src, dst = W.config_layouts("c2-lpt", 8, len(lens))
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-bf16"), 8, seed=3)
+
+
+def test_lpt_max_size_groups_match_oracle():
+    """LPT at its maximum N (8192): the plan (hence g(i)) equals the oracle's."""
+    rng = np.random.default_rng(4)
+    lens = rng.integers(0, 5000, size=8192).tolist()
+    src = W.rollout_layout(8192, 8)
+    dst = W.layout(dp=8, assign="lpt")
+    run_gpu_case(src, dst, lens, [("m", 1, 1, "x")], 8, seed=4)
+
+
+def test_uniform_sweep_round_robin():
+    """Config 5 shape: DP8 -> EXPLICIT round-robin (uniform all-to-allv)."""
+    lens = [4096] * 64
+    src, dst = W.config_layouts("c5", 8, len(lens))
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-fp32"), 8, seed=5)
+
+
+def test_alignment_fuzz_many_short_sequences():
+    """Every (src mod 16, dst mod 16) combination: 1-byte and odd-width fields over many
+    sequences of lengths 0..40 regrouped with LPT (scrambles offsets on both sides)."""
+    rng = np.random.default_rng(6)
+    lens = rng.integers(0, 41, size=700).tolist()
+    src = W.layout(dp=3, sp=2, assign="contig")
+    dst = W.layout(rank0=1, dp=5, tp=1, assign="lpt")
+    run_gpu_case(src, dst, lens, [("m", 1, 1, "x"), ("c", 1, 3, "x"), ("w", 2, 7, "x")], 7,
+                 seed=6, mode="exec")
+    run_gpu_case(src, dst, lens, [("m", 1, 1, "x"), ("c", 1, 3, "x"), ("w", 2, 7, "x")], 7,
+                 seed=7, mode="stage")
+
+
+def test_round_trip_identity_on_gpu():
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    lens = W.c2_lengths(1)[:96].tolist()
+    fields = W.field_set("scalar6-fp32")
+    src = W.rollout_layout(96, 8)
+    dst = W.layout(dp=2, sp=2, tp=2, assign="contig")
+    glob = W.gen_global_fields(fields, sum(lens), random_bits=True)
+    src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+    ed = EmulatedDispatch(8)
+    p1 = ed.plan(src, dst, lens, fields)
+    send = [torch.from_numpy(src_arrays[r][f]).cuda() for r in range(8) for f in range(6)]
+    mid = ed.alloc_recv(p1, fields)
+    p1.exec(send, ed.flat(mid))
+    inv_src, inv_dst = O.inverse_layouts(src, dst, lens)
+    p2 = ed.plan(inv_src, inv_dst, lens, fields)
+    back = ed.alloc_recv(p2, fields)
+    p2.exec(ed.flat(mid), ed.flat(back))
+    torch.cuda.synchronize()
+    for r in range(8):
+        for f in range(6):
+            assert np.array_equal(back[r][f].cpu().numpy(), src_arrays[r][f])
+
+
+def test_plan_is_deterministic():
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    lens = W.c4_lengths(2).tolist()
+    ed = EmulatedDispatch(8)
+    src, dst = W.config_layouts("c4", 8, len(lens))
+    f = W.field_set("scalar6-fp32")
+    a = ed.plan(src, dst, lens, f).export()
+    b = ed.plan(src, dst, lens, f).export()
+    assert a == b == O.route(src, dst, lens, 8)
+
+
+# ---------------------------------------------------------------------------------------
+# errors
+# ---------------------------------------------------------------------------------------
+
+def test_device_latched_errors():
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    ed = EmulatedDispatch(2)
+    f = W.field_set("tiny3")
+    p = ed.plan(W.layout(dp=1), W.layout(dp=2), [3, -1, 2], f)
+    with pytest.raises(EarlError) as e:
+        p.local_sizes(0)
+    assert e.value.name == "EARL_ERR_INVALID_ARGUMENT"
+    p = ed.plan(W.layout(dp=1), W.layout(dp=2, assign="explicit", group_of_seq=[0, 5, 1]),
+                [3, 1, 2], f)
+    with pytest.raises(EarlError) as e:
+        p.stats()
+    assert e.value.name == "EARL_ERR_LAYOUT"
+
+
+@pytest.mark.parametrize("bad,name", [
+    (dict(dp=3), "EARL_ERR_LAYOUT"),
+    (dict(dp=2, assign="given_counts", counts=[1, 1]), "EARL_ERR_LAYOUT"),
+    (dict(rank0=1, dp=2), "EARL_ERR_LAYOUT"),
+])
+def test_host_layout_errors(bad, name):
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    ed = EmulatedDispatch(2)
+    with pytest.raises(EarlError) as e:
+        ed.plan(W.layout(dp=1), W.layout(**bad), [3, 1, 2, 5], W.field_set("tiny3"))
+    assert e.value.name == name
+
+
+def test_lpt_capacity_and_misaligned_buffers():
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    ed = EmulatedDispatch(2)
+    with pytest.raises(EarlError) as e:
+        ed.plan(W.layout(dp=1), W.layout(dp=2, assign="lpt"), [1] * 8193, W.field_set("tiny3"))
+    assert e.value.name == "EARL_ERR_CAPACITY"
+    f = [("a", 4, 1, "x")]
+    p = ed.plan(W.layout(dp=1), W.layout(dp=2), [4, 4], f)
+    buf = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(EarlError) as e:
+        p.exec([buf[4:], None], [buf[16:], buf[32:]])
+    assert e.value.name == "EARL_ERR_INVALID_ARGUMENT"
