@@ -642,10 +642,49 @@ earl_status_t fill_copy_args(earl_plan_t p, CopyArgs& a, int mode) {
   a.timeout_ns = c->timeout_ns;
   a.err = &p->args.hdr->err;
   a.err_detail = &p->args.hdr->err_detail;
+  a.work_ctr = &p->args.hdr->work_ctr;
+  a.fin_ctr = &p->args.hdr->fin_ctr;
   return EARL_OK;
 }
 
-int copy_grid(earl_comm* c) { return c->sm_count * 2; }
+int copy_grid(earl_comm* c) { return c->sm_count; }
+
+// Debug trace (EARL_COPY_TRACE=<file>): per-warp start/end timestamps of every copy launch,
+// appended to <file> as text after a synchronising copy-back.  Never enabled in benchmarks.
+struct CopyTrace {
+  uint64_t* dev = nullptr;
+  size_t n = 0;
+  const char* path = nullptr;
+};
+CopyTrace& trace_state() {
+  static CopyTrace t;
+  static bool init = false;
+  if (!init) { t.path = getenv("EARL_COPY_TRACE"); init = true; }
+  return t;
+}
+cudaError_t traced_launch(CopyArgs& a, earl_comm* c, cudaStream_t s) {
+  CopyTrace& t = trace_state();
+  if (!t.path) return launch_copy(a, copy_grid(c), 0, s);
+  const size_t n = (size_t)c->sm_count * 64 * 4;
+  if (!t.dev) { cudaMalloc(&t.dev, n * 8); t.n = n; }
+  cudaMemsetAsync(t.dev, 0, n * 8, s);
+  a.trace = t.dev;
+  cudaError_t e = launch_copy(a, copy_grid(c), 0, s);
+  if (e != cudaSuccess) return e;
+  std::vector<uint64_t> h(n);
+  cudaMemcpyAsync(h.data(), t.dev, n * 8, cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  FILE* fp = fopen(t.path, "a");
+  if (fp) {
+    fprintf(fp, "launch mode=%d\n", a.mode);
+    for (size_t w = 0; w < n / 4; ++w)
+      if (h[4 * w + 1]) fprintf(fp, "%zu %llu %llu %llu %llu\n", w, (unsigned long long)h[4 * w],
+                               (unsigned long long)h[4 * w + 1], (unsigned long long)h[4 * w + 2],
+                               (unsigned long long)h[4 * w + 3]);
+    fclose(fp);
+  }
+  return cudaSuccess;
+}
 
 // Source arrays (direct/pack): emulated [world][F], else [F] for this rank.
 earl_status_t set_src(earl_plan_t p, CopyArgs& a, const void* const* bufs) {
@@ -718,7 +757,7 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1);
   }
-  cudaError_t e = launch_copy(a, copy_grid(c), 512, s);
+  cudaError_t e = traced_launch(a, c, s);
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "copy launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
   p->synced = false;
@@ -742,7 +781,7 @@ extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* se
     a.stage[rr] = static_cast<uint8_t*>(stage_bufs[r]);
   }
   a.world = 1;  // no completion protocol: pack is rank-local
-  cudaError_t e = launch_copy(a, copy_grid(c), 512, static_cast<cudaStream_t>(stream));
+  cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
   return EARL_OK;
@@ -770,7 +809,7 @@ extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* 
     }
   }
   a.world = 1;
-  cudaError_t e = launch_copy(a, copy_grid(c), 512, static_cast<cudaStream_t>(stream));
+  cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "unpack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
   return EARL_OK;

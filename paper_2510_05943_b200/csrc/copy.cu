@@ -19,27 +19,10 @@ namespace earl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kUnroll = 4;
-
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
+constexpr uint64_t kUnitsPerWarp = 8;
 
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   *reinterpret_cast<uint4*>(p) = v;
-}
-
-__device__ __forceinline__ uint4 shfl_down4(const uint4& v, int d) {
-  return make_uint4(__shfl_down_sync(kFull, v.x, d), __shfl_down_sync(kFull, v.y, d),
-                    __shfl_down_sync(kFull, v.z, d), __shfl_down_sync(kFull, v.w, d));
-}
-__device__ __forceinline__ uint4 shfl_idx4(const uint4& v, int src) {
-  return make_uint4(__shfl_sync(kFull, v.x, src), __shfl_sync(kFull, v.y, src),
-                    __shfl_sync(kFull, v.z, src), __shfl_sync(kFull, v.w, src));
 }
 
 // 16 bytes starting at byte sh (1..15) of the 32-byte pair (A, B).  s4 = sh/4 and
@@ -54,77 +37,6 @@ __device__ __forceinline__ uint4 realign(const uint4& A, const uint4& B, int s4,
   }
   return make_uint4(__funnelshift_r(v0, v1, bits), __funnelshift_r(v1, v2, bits),
                     __funnelshift_r(v2, v3, bits), __funnelshift_r(v3, v4, bits));
-}
-
-// Copy len bytes from src to each of dst[0..R) (all destinations share the same alignment
-// mod 16 -- field bases are 16-B aligned and replicas use the same token offset).
-// Called by a whole warp with warp-uniform arguments.
-__device__ __forceinline__ void warp_copy(const uint8_t* __restrict__ src, uint8_t* const* dst,
-                                          int R, int64_t len, int lane) {
-  if (len <= 0) return;
-  int64_t head = (16 - ((uintptr_t)dst[0] & 15)) & 15;
-  if (head > len) head = len;
-  if (lane < head) {
-    const uint8_t v = src[lane];
-    for (int r = 0; r < R; ++r) dst[r][lane] = v;
-  }
-  const uint8_t* s = src + head;
-  const int64_t dofs = head;
-  const int64_t rest = len - head;
-  const int64_t nvec = rest >> 4;
-  if (nvec > 0) {
-    const int sh = (int)((uintptr_t)s & 15);
-    if (sh == 0) {
-      const uint4* sp = reinterpret_cast<const uint4*>(s);
-      for (int64_t base = 0; base < nvec; base += 32 * kUnroll) {
-        uint4 v[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t c = base + u * 32 + lane;
-          if (c < nvec) v[u] = ld_stream(sp + c);
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t c = base + u * 32 + lane;
-          if (c < nvec)
-            for (int r = 0; r < R; ++r) st_v4(dst[r] + dofs + c * 16, v[u]);
-        }
-      }
-    } else {
-      // Source words sal[c] and sal[c+1] hold destination chunk c.  Word nvec contains valid
-      // source bytes whenever sh > 0, so loading it never leaves the source allocation.
-      const uint4* sal = reinterpret_cast<const uint4*>(s - sh);
-      const int s4 = sh >> 2, bits = (sh & 3) * 8;
-      for (int64_t base = 0; base < nvec; base += 32 * kUnroll) {
-        uint4 A[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const int64_t c = base + u * 32 + lane;
-          A[u] = (c <= nvec) ? ld_stream(sal + c) : make_uint4(0, 0, 0, 0);
-        }
-        uint4 extra = make_uint4(0, 0, 0, 0);
-        const int64_t ce = base + 32 * kUnroll;
-        if (lane == 31 && ce <= nvec) extra = ld_stream(sal + ce);
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-          const uint4 dn = shfl_down4(A[u], 1);
-          const uint4 nx = (u + 1 < kUnroll) ? shfl_idx4(A[(u + 1) % kUnroll], 0) : extra;
-          const uint4 B = (lane == 31) ? nx : dn;
-          const int64_t c = base + u * 32 + lane;
-          if (c < nvec) {
-            const uint4 o = realign(A[u], B, s4, bits);
-            for (int r = 0; r < R; ++r) st_v4(dst[r] + dofs + c * 16, o);
-          }
-        }
-      }
-    }
-  }
-  const int64_t done = nvec << 4;
-  const int64_t tail = rest - done;
-  if (lane < tail) {
-    const uint8_t v = s[done + lane];
-    for (int r = 0; r < R; ++r) dst[r][dofs + done + lane] = v;
-  }
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -167,11 +79,261 @@ __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world,
   }
 }
 
-__global__ void __launch_bounds__(512, 2) copy_kernel(const CopyArgs a) {
+// ---------------------------------------------------------------------------------------
+// TMA-pipelined copy engine.  Each warp owns a ring of STAGES shared-memory buffers of CHUNK
+// bytes.  Lane 0 walks the warp's byte slice (records x fields, cut into source-aligned
+// chunks), writes a chunk descriptor and issues one cp.async.bulk global->shared per chunk
+// (mbarrier complete_tx), STAGES-1 chunks ahead.  When a chunk lands, the warp stores it:
+// if source and destination are congruent mod 16 the 16-B-aligned interior leaves shared
+// memory by one cp.async.bulk shared->global per destination replica; otherwise all lanes
+// realign it (two 16-B shared loads + funnel shift per 16-B output) into 16-B global stores.
+// The <16-byte head and tail go byte by byte.  No data passes through registers on the
+// congruent path, so the bytes in flight per SM are set by the ring, not by occupancy.
+// ---------------------------------------------------------------------------------------
+
+struct __align__(16) ChunkDesc {
+  const uint8_t* src_al;  // 16-B aligned source address of the load
+  uint32_t load_bytes;    // multiple of 16
+  uint32_t off;           // first chunk byte inside the stage (src & 15)
+  uint32_t len;           // chunk bytes
+  uint32_t R;             // destination replicas
+  uint8_t* dst[kMaxWorld];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Lane-0-only walker over a warp's slice of the launch's work.  Work is measured in a cost
+// space, not in bytes: piece (record j, field f) costs its n_j * B_f bytes plus c0, the
+// byte-equivalent of one chunk round trip, so a warp whose slice holds thousands of small
+// scalar pieces gets proportionally fewer bytes (equal-byte slices made those warps the
+// stragglers: profiles/r01_trace.txt).  Cost offsets [0, n_j*B_f) of a piece map 1:1 to its
+// bytes; the trailing c0 maps to no bytes, so slices partition the bytes exactly.
+struct Walker {
+  const CopyArgs* a;
+  const PlanHeader* h;
+  int64_t rbeg, rend, tbeg;
+  uint64_t ntok, nrec, c0, x1, xpos;
+  int64_t j;
+  int f;
+  const uint8_t* psrc;
+  uint8_t* pdst[kMaxWorld];
+  uint32_t R;
+  uint64_t prem;
+
+  __device__ uint64_t field_cost(int ff) const {
+    return ntok * a->Bpre[ff] + (uint64_t)ff * nrec * c0;
+  }
+  __device__ uint64_t rec_cost(int64_t jj, int ff) const {
+    return field_cost(ff) + (uint64_t)(a->rec.tok_prefix[jj] - tbeg) * a->Bf[ff] +
+           (uint64_t)(jj - rbeg) * c0;
+  }
+
+  // dynamic scheduling: further units of `unit` cost come from a plan-owned counter
+  uint64_t unit, n_units, first_dyn;
+  unsigned int* work_ctr;
+
+  __device__ void setup(const CopyArgs* a_, int64_t rbeg_, int64_t rend_, int64_t tbeg_,
+                        uint64_t ntok_, uint64_t c0_, uint64_t unit_, uint64_t n_units_,
+                        uint64_t first_dyn_) {
+    a = a_; h = a_->hdr; rbeg = rbeg_; rend = rend_; tbeg = tbeg_; ntok = ntok_;
+    nrec = (uint64_t)(rend_ - rbeg_); c0 = c0_; unit = unit_; n_units = n_units_;
+    first_dyn = first_dyn_; work_ctr = a_->work_ctr; prem = 0; R = 0; xpos = x1 = 0;
+  }
+
+  // Claim the next unit: returns false when the launch's work is exhausted.
+  __device__ bool claim() {
+    const uint64_t u = first_dyn + atomicAdd(work_ctr, 1u);
+    if (u >= n_units) return false;
+    start(u * unit, (u + 1) * unit);
+    return true;
+  }
+
+  __device__ void start(uint64_t x0, uint64_t x1_) {
+    const uint64_t total = field_cost(a->n_fields);
+    x1 = x1_ < total ? x1_ : total;
+    xpos = x0;
+    prem = 0;
+    f = 0;
+    j = rbeg;
+    if (xpos >= x1) return;
+    while (xpos >= field_cost(f + 1)) ++f;
+    int64_t lo = rbeg, hi = rend - 1;  // last record whose cost interval starts <= xpos
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (rec_cost(mid, f) <= xpos) lo = mid; else hi = mid - 1;
+    }
+    j = lo;
+  }
+
+  __device__ bool next_piece() {
+    const int Sd = a->n_dst_shards;
+    while (xpos < x1) {
+      const uint64_t Bf = a->Bf[f];
+      const uint64_t cj = rec_cost(j, f);
+      const uint64_t nb = (uint64_t)(a->rec.tok_prefix[j + 1] - a->rec.tok_prefix[j]) * Bf;
+      const uint64_t cend = cj + nb + c0;
+      const uint64_t lo = xpos - cj;
+      const uint64_t hi = (x1 < cend ? x1 : cend) - cj;
+      const uint64_t u0 = lo < nb ? lo : nb;
+      const uint64_t u1 = hi < nb ? hi : nb;
+      bool found = false;
+      if (u1 > u0) {
+        const uint32_t code = a->rec.code[j];
+        const int s = code & 0xff, ss = (code >> 8) & 0xff, ds = (code >> 16) & 0xff, ts = code >> 24;
+        int64_t msg_field = 0;
+        if (a->mode != kDirect) {
+          const int key = ss * Sd + ds;
+          const int64_t kt = h->key_tokens[key];
+          int64_t fb = 0;
+          for (int ff = 0; ff < f; ++ff) fb += (kt * a->Bf[ff] + 15) & ~15LL;
+          msg_field = h->msg_off[key] + fb + a->rec.msg_tok[j] * (int64_t)Bf + (int64_t)u0;
+        }
+        psrc = (a->mode == kUnpack) ? a->stage[s] + msg_field
+                                    : a->src[s][f] + a->rec.src_tok[j] * (int64_t)Bf + (int64_t)u0;
+        R = 0;
+        if (a->mode == kPack) {
+          pdst[R++] = a->stage[s] + msg_field;
+        } else {
+          const int64_t doff = a->rec.dst_tok[j] * (int64_t)Bf + (int64_t)u0;
+          for (int td = ts; td < a->tp_d; td += a->tp_s) {
+            uint8_t* base = a->dst[a->rank0_d + ds * a->tp_d + td][f];
+            if (base != nullptr) pdst[R++] = base + doff;
+          }
+        }
+        prem = u1 - u0;
+        found = R > 0;
+      }
+      if (x1 >= cend) {
+        xpos = cend;
+        ++j;
+        if (j == rend) { j = rbeg; ++f; }
+      } else {
+        xpos = x1;
+      }
+      if (found) return true;
+    }
+    return false;
+  }
+
+  template <int CHUNK>
+  __device__ bool next_chunk(ChunkDesc& d) {
+    while (prem == 0 && !next_piece())
+      if (!claim()) return false;
+    const uint32_t off = (uint32_t)((uintptr_t)psrc & 15);
+    const uint64_t room = CHUNK - off;
+    const uint32_t len = (uint32_t)(prem < room ? prem : room);
+    d.src_al = psrc - off;
+    d.off = off;
+    d.len = len;
+    d.load_bytes = (off + len + 15) & ~15u;
+    d.R = R;
+    for (uint32_t r = 0; r < R; ++r) { d.dst[r] = pdst[r]; pdst[r] += len; }
+    psrc += len;
+    prem -= len;
+    return true;
+  }
+};
+
+// Store one landed chunk (whole warp).
+__device__ __forceinline__ void store_chunk(const ChunkDesc& D, uint8_t* stage, int lane) {
+  const uint32_t len = D.len, R = D.R, off = D.off;
+  const uint8_t* sm = stage + off;
+  uint8_t* d0 = D.dst[0];
+  uint32_t head = (16 - (uint32_t)((uintptr_t)d0 & 15)) & 15;
+  if (head > len) head = len;
+  if (lane < (int)head) {
+    const uint8_t v = sm[lane];
+    for (uint32_t r = 0; r < R; ++r) D.dst[r][lane] = v;
+  }
+  const uint32_t rest = len - head;
+  const uint32_t nvec = rest >> 4;
+  if (nvec > 0) {
+    const uint32_t smo = off + head;
+    if ((smo & 15) == 0) {
+      if (lane == 0)
+        for (uint32_t r = 0; r < R; ++r) tma_store(D.dst[r] + head, stage + smo, nvec * 16);
+    } else {
+      const uint32_t base16 = smo & ~15u, sh = smo & 15;
+      const int s4 = (int)(sh >> 2), bits = (int)(sh & 3) * 8;
+      for (uint32_t k = lane; k < nvec; k += 32) {
+        const uint4 w0 = *reinterpret_cast<const uint4*>(stage + base16 + 16 * k);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(stage + base16 + 16 * k + 16);
+        const uint4 o = realign(w0, w1, s4, bits);
+        for (uint32_t r = 0; r < R; ++r) st_v4(D.dst[r] + head + 16 * k, o);
+      }
+    }
+  }
+  const uint32_t t0 = head + nvec * 16;
+  if (lane < (int)(len - t0)) {
+    const uint8_t v = sm[t0 + lane];
+    for (uint32_t r = 0; r < R; ++r) D.dst[r][t0 + lane] = v;
+  }
+}
+
+template <int WARPS, int STAGES, int CHUNK>
+constexpr size_t copy_smem_bytes() {
+  return (size_t)WARPS * STAGES * CHUNK + (size_t)WARPS * STAGES * (sizeof(ChunkDesc) + 8);
+}
+
+template <int WARPS, int STAGES, int CHUNK>
+__global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_constant__ CopyArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint8_t* data = smem + (size_t)w * STAGES * CHUNK;
+  ChunkDesc* desc = reinterpret_cast<ChunkDesc*>(smem + (size_t)WARPS * STAGES * CHUNK) + w * STAGES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CHUNK +
+                                              (size_t)WARPS * STAGES * sizeof(ChunkDesc)) + w * STAGES;
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
   const PlanHeader* h = a.hdr;
-  const int lane = threadIdx.x & 31;
-  const int F = a.n_fields;
   if (h->err == 0) {
     int64_t rbeg, rend, tbeg, tend;
     if (a.view_rank < 0) {
@@ -181,75 +343,73 @@ __global__ void __launch_bounds__(512, 2) copy_kernel(const CopyArgs a) {
       tbeg = h->rec_tok_begin[a.view_rank]; tend = h->rec_tok_begin[a.view_rank + 1];
     }
     const uint64_t ntok = (uint64_t)(tend - tbeg);
-    const uint64_t total = ntok * a.Bpre[F];
-    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint64_t wid = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const uint64_t chunk = (((total + nwarps - 1) / nwarps) + 511) & ~511ull;
-    const uint64_t b0 = wid * chunk;
-    const uint64_t b1 = (b0 + chunk < total) ? b0 + chunk : total;
-    if (b0 < b1) {
-      int f = 0;
-      while (b0 >= ntok * a.Bpre[f + 1]) ++f;
-      const int64_t tok = tbeg + (int64_t)((b0 - ntok * a.Bpre[f]) / a.Bf[f]);
-      // last record j in [rbeg, rend) with tok_prefix[j] <= tok
-      int64_t lo = rbeg, hi = rend - 1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (a.rec.tok_prefix[mid] <= tok) lo = mid; else hi = mid - 1;
+    const uint64_t c0 = CHUNK;
+    const uint64_t total = ntok * a.Bpre[a.n_fields] + (uint64_t)a.n_fields * (rend - rbeg) * c0;
+    const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
+    const uint64_t wid = (uint64_t)blockIdx.x * WARPS + w;
+    // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
+    uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
+    if (unit < 4 * (uint64_t)CHUNK) unit = 4 * (uint64_t)CHUNK;
+    const uint64_t n_units = (total + unit - 1) / unit;
+    const uint64_t b0 = wid * unit, b1 = b0 + unit;
+    Walker wk;
+    uint64_t t_start = 0;
+    if (lane == 0) {
+      if (a.trace) t_start = globaltimer();
+      wk.setup(&a, rbeg, rend, tbeg, ntok, c0, unit, n_units, nwarps);
+      if (wid < n_units) wk.start(b0, b1);
+    }
+    int nprod = 0;
+    for (int s = 0; s < STAGES - 1; ++s) {
+      int ok = 0;
+      if (lane == 0 && wk.next_chunk<CHUNK>(desc[s])) {
+        mbar_expect_tx(&bar[s], desc[s].load_bytes);
+        tma_load(data + (size_t)s * CHUNK, desc[s].src_al, desc[s].load_bytes, &bar[s]);
+        ok = 1;
       }
-      int64_t j = lo;
-      uint64_t pos = b0;
-      const int Sd = a.n_dst_shards;
-      while (pos < b1) {
-        const uint64_t Bf = a.Bf[f];
-        const uint64_t fs = ntok * a.Bpre[f];
-        const int64_t tp0 = a.rec.tok_prefix[j] - tbeg;
-        const int64_t tp1 = a.rec.tok_prefix[j + 1] - tbeg;
-        const uint64_t rlo = fs + (uint64_t)tp0 * Bf;
-        const uint64_t rhi = fs + (uint64_t)tp1 * Bf;
-        const uint64_t cend = rhi < b1 ? rhi : b1;
-        if (cend > pos) {
-          const uint32_t code = a.rec.code[j];
-          const int s = code & 0xff, ss = (code >> 8) & 0xff, ds = (code >> 16) & 0xff,
-                    ts = code >> 24;
-          const uint64_t u0 = pos - rlo;
-          const int64_t len = (int64_t)(cend - pos);
-          const uint8_t* sp;
-          uint8_t* dp[kMaxWorld];
-          int R = 0;
-          int64_t msg_field = 0;
-          if (a.mode != kDirect) {
-            const int key = ss * Sd + ds;
-            const int64_t kt = h->key_tokens[key];
-            int64_t fb = 0;
-            for (int ff = 0; ff < f; ++ff) fb += (kt * a.Bf[ff] + 15) & ~15LL;
-            msg_field = h->msg_off[key] + fb + a.rec.msg_tok[j] * (int64_t)Bf + (int64_t)u0;
-          }
-          if (a.mode == kUnpack) sp = a.stage[s] + msg_field;
-          else sp = a.src[s][f] + a.rec.src_tok[j] * (int64_t)Bf + (int64_t)u0;
-          if (a.mode == kPack) {
-            dp[0] = a.stage[s] + msg_field;
-            R = 1;
-          } else {
-            const int64_t doff = a.rec.dst_tok[j] * (int64_t)Bf + (int64_t)u0;
-            for (int td = ts; td < a.tp_d; td += a.tp_s) {
-              const int d = a.rank0_d + ds * a.tp_d + td;
-              uint8_t* base = a.dst[d][f];
-              if (base != nullptr) dp[R++] = base + doff;
-            }
-          }
-          if (R > 0) warp_copy(sp, dp, R, len, lane);
-          pos = cend;
-        }
-        if (pos >= rhi) {
-          ++j;
-          if (j == rend) { j = rbeg; ++f; }
+      ok = __shfl_sync(kFull, ok, 0);
+      if (!ok) break;
+      ++nprod;
+    }
+    for (int c = 0; c < nprod; ++c) {
+      const int st = c % STAGES;
+      mbar_wait(&bar[st], (uint32_t)((c / STAGES) & 1));
+      store_chunk(desc[st], data + (size_t)st * CHUNK, lane);
+      if (lane == 0) { bulk_commit(); bulk_wait_read1(); }
+      __syncwarp();
+      int ok = 0;
+      if (lane == 0) {
+        const int ns = (c + STAGES - 1) % STAGES;
+        fence_proxy_async_smem();
+        if (wk.next_chunk<CHUNK>(desc[ns])) {
+          mbar_expect_tx(&bar[ns], desc[ns].load_bytes);
+          tma_load(data + (size_t)ns * CHUNK, desc[ns].src_al, desc[ns].load_bytes, &bar[ns]);
+          ok = 1;
         }
       }
+      ok = __shfl_sync(kFull, ok, 0);
+      if (ok) ++nprod;
+    }
+    if (lane == 0) bulk_wait_all();
+    if (lane == 0 && a.trace) {
+      uint64_t* t = a.trace + 4 * wid;
+      t[0] = t_start; t[1] = globaltimer(); t[2] = b1 - b0; t[3] = (uint64_t)nprod;
+    }
+    __syncwarp();
+  }
+  // the last CTA to finish resets the plan's scheduling counters for the next launch
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(a.fin_ctr, 1u) == gridDim.x - 1) {
+      *a.work_ctr = 0;
+      *a.fin_ctr = 0;
+      __threadfence();
     }
   }
   // completion (multi-process comm): last CTA releases this epoch to every peer and waits
   if (a.world > 1 && a.view_rank >= 0) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -269,11 +429,41 @@ __global__ void __launch_bounds__(512, 2) copy_kernel(const CopyArgs a) {
   }
 }
 
+template <int WARPS, int STAGES, int CHUNK>
+cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
+  constexpr size_t smem = copy_smem_bytes<WARPS, STAGES, CHUNK>();
+  static bool configured = false;
+  auto kern = copy_kernel<WARPS, STAGES, CHUNK>;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+  if (per_sm < 1) per_sm = 1;
+  kern<<<sm_count * per_sm, WARPS * 32, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
-cudaError_t launch_copy(const CopyArgs& a, int grid, int block, cudaStream_t s) {
-  copy_kernel<<<grid, block, 0, s>>>(a);
-  return cudaGetLastError();
+// Copy-engine shape (warps per CTA, ring stages, chunk bytes).  The default was chosen by
+// measurement (profiles/); EARL_COPY_CFG selects another compiled shape for tuning.
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int /*unused*/, cudaStream_t s) {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("EARL_COPY_CFG");
+    cfg = e ? atoi(e) : 0;
+  }
+  switch (cfg) {
+    case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
+    case 2: return launch_cfg<4, 6, 8192>(a, sm_count, s);
+    case 3: return launch_cfg<8, 3, 8192>(a, sm_count, s);
+    case 4: return launch_cfg<2, 8, 8192>(a, sm_count, s);
+    case 5: return launch_cfg<16, 2, 4096>(a, sm_count, s);
+    default: return launch_cfg<4, 4, 8192>(a, sm_count, s);
+  }
 }
 
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,

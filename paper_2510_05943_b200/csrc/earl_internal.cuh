@@ -44,6 +44,8 @@ struct PlanHeader {
   int64_t rec_tok_begin[kMaxWorld + 1];     // tokens of those records (prefix)
   int64_t rec_base[kMaxWorld][kMaxShards];  // first record of block (s, ds)
   int64_t rec_tok_base[kMaxWorld][kMaxShards];
+  uint32_t work_ctr;    // copy kernels: dynamic work-unit counter (reset by the last CTA)
+  uint32_t fin_ctr;     // copy kernels: finished-CTA counter
 };
 
 // Copy records: one per (piece, sending replica ts < min(tp_src, tp_dst)), ordered by
@@ -113,6 +115,9 @@ struct CopyArgs {
   uint64_t timeout_ns;
   int32_t* err;                               // where to latch TIMEOUT (plan header)
   int32_t* err_detail;
+  uint64_t* trace;                            // debug: per-warp (t_start, t_end, bytes, chunks)
+  unsigned int* work_ctr;                     // plan-owned dynamic scheduling counters
+  unsigned int* fin_ctr;
 };
 
 // signal pad slots (uint64 each): [0, 8) ready flags written by peer p at p; [8, 16) done flags
@@ -121,7 +126,7 @@ constexpr int kDoneSlot = 8;
 
 // launchers (defined in the .cu files)
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, cudaStream_t s);
-cudaError_t launch_copy(const CopyArgs& a, int grid, int block, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int unused, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
                                  uint64_t epoch, uint64_t timeout_ns, int32_t* err,
                                  int32_t* err_detail, cudaStream_t s);

@@ -180,6 +180,41 @@ def rollout_holdings(global_fields, fields, lengths, counts):
     return out
 
 
+def gen_field_device(field, n_tokens: int, seed: int, device):
+    """Device-side draw of one field for a rank holding n_tokens tokens (same distributions as
+    gen_field_bytes, drawn with a seeded torch CUDA generator; used where host generation of
+    multi-GB payloads would dominate).  Returns a uint8 tensor [n_tokens * Bf]."""
+    import torch
+    _, bpe, ept, kind = field
+    n = int(n_tokens) * ept
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    if kind == "ids":
+        t = torch.randint(0, VOCAB, (n,), dtype=torch.int32, device=device, generator=g)
+    elif kind in ("logprob_f32", "logprob_bf16"):
+        t = -torch.empty(n, dtype=torch.float32, device=device).exponential_(1.0, generator=g)
+        if kind == "logprob_bf16":
+            t = t.to(torch.bfloat16)
+    elif kind in ("normal_f32", "normal_bf16"):
+        t = torch.randn(n, dtype=torch.float32, device=device, generator=g)
+        if kind == "normal_bf16":
+            t = t.to(torch.bfloat16)
+    elif kind == "mask":
+        t = (torch.rand(n, device=device, generator=g) < 0.8).to(torch.uint8)
+    else:
+        t = torch.randint(0, 256, (n * bpe,), dtype=torch.uint8, device=device, generator=g)
+    out = t.contiguous().view(torch.uint8).reshape(-1)
+    assert out.numel() == n * bpe
+    return out
+
+
+def rollout_token_counts(lengths, counts):
+    """Tokens held by each rank of a GIVEN_COUNTS rollout layout (input sizing only)."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    edges = np.concatenate([[0], np.cumsum(np.asarray(counts, dtype=np.int64))])
+    return [int(lengths[edges[g]:edges[g + 1]].sum()) for g in range(len(counts))]
+
+
 def config_layouts(config: str, n_gpus: int, n_seqs: int):
     """(src, dst) layouts of BASELINE.json's configs at world size n_gpus."""
     n = int(n_gpus)
