@@ -59,6 +59,19 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def ncu_traffic(desc):
+    """DRAM bytes (read + write) of one copy_kernel launch from the committed ncu capture of the
+    same workload (profiles/copy_kernel_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "copy_kernel_traffic.json")
+    try:
+        d = json.load(open(p))
+    except Exception:
+        return None
+    if d.get("workload") != desc:
+        return None
+    return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
+
+
 def workload(config, n_ranks, fields_name):
     from paper_2510_05943_b200 import workloads as W
     if config in ("c3", "c2-lpt"):
@@ -138,22 +151,28 @@ def emit(obj):
 # CPU oracle (reference arm and cpu_baseline leg): the only places bench.py runs oracle/
 # ---------------------------------------------------------------------------------------
 
-def oracle_sample(config, fields_name, n_seq_sample, seed=0):
-    """Run the oracle's decentralized dispatch on the first
-    n_seq_sample sequences of the workload, with the workload's layout shapes (8 ranks)."""
-    import numpy as np
-
+def oracle_prepare(config, fields_name, n_seq_sample, seed=0):
+    """Inputs for the oracle on the first n_seq_sample sequences of the workload, with the
+    workload's layout shapes (8 ranks).  Payload bytes are random bits (the oracle moves
+    opaque bytes; generating multi-GB float draws on the host would dominate the run)."""
     from oracle import earl_oracle as O
     from paper_2510_05943_b200 import workloads as W
     lens, _, _, fields, _ = workload(config, 8, fields_name)
     lens = [int(x) for x in lens[:n_seq_sample]]
     src, dst = W.config_layouts(config, 8, len(lens))
-    glob = W.gen_global_fields(fields, sum(lens), seed_base=1000 + seed)
+    glob = W.gen_global_fields(fields, sum(lens), seed_base=1000 + seed, random_bits=True)
     src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+    del glob
+    return (src, dst, lens, src_arrays, fields), sum(lens) * W.bytes_per_token(fields), sum(lens)
+
+
+def oracle_run(prep):
+    """Time the oracle's decentralized dispatch once."""
+    from oracle import earl_oracle as O
+    src, dst, lens, src_arrays, fields = prep
     t0 = time.perf_counter()
     O.dispatch(src, dst, lens, src_arrays, fields, 8)
-    dt = time.perf_counter() - t0
-    return sum(lens) * W.bytes_per_token(fields), dt, len(lens), sum(lens)
+    return time.perf_counter() - t0
 
 
 def cpu_threads():
@@ -163,26 +182,28 @@ def cpu_threads():
         return os.cpu_count()
 
 
+REF_SEQS_PER_STEP = 32     # reference arm: bounded sample per step (~1 s of oracle work)
+CPU_BASELINE_SEQS = 256    # cpu_baseline leg: ~10 s of oracle work
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n_seq = 12
-    vals = []
+    prep, nbytes, ntok = oracle_prepare(args.config, args.fields, REF_SEQS_PER_STEP)
+    times = []
     for k in range(args.warmup + args.steps):
-        nbytes, dt, ns, ntok = oracle_sample(args.config, args.fields, n_seq, seed=k)
+        dt = oracle_run(prep)
         if k >= args.warmup:
-            vals.append((nbytes, dt))
-    tot_b = sum(v[0] for v in vals)
-    tot_t = sum(v[1] for v in vals)
-    value = tot_b / tot_t / 1e9
+            times.append(dt)
+    value = nbytes * len(times) / sum(times) / 1e9
     _, _, _, _, desc = workload(args.config, 8, args.fields)
-    sample = (f"first {n_seq} sequences ({ntok} tokens) of the workload per step, same layout "
-              f"shapes over 8 simulated ranks, single-threaded NumPy oracle")
+    sample = (f"first {REF_SEQS_PER_STEP} sequences ({ntok} tokens, {nbytes} B) of the workload "
+              f"per step, same layout shapes over 8 simulated ranks, single-threaded NumPy oracle")
     emit({"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-          "ms_per_step": tot_t / len(vals) * 1e3, "higher_is_better": True, "scaling": "strong",
-          "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+          "ms_per_step": sum(times) / len(times) * 1e3, "higher_is_better": True,
+          "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
           "config": {"workload": desc, "sample": sample},
           "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
                            "sample": sample},
@@ -280,7 +301,7 @@ def run_single(args):
            "roofline": {"bound": "hbm", "kernel": "copy_kernel (fused direct, all 8 ranks)",
                         "achieved": alg_exec / (t_exec_avg * 1e-3) / 1e9, "peak": peak,
                         "unit": "GB/s", "frac": alg_exec / (t_exec_avg * 1e-3) / 1e9 / peak,
-                        "traffic": None, "algorithmic_bytes": int(alg_exec),
+                        "traffic": ncu_traffic(desc), "algorithmic_bytes": int(alg_exec),
                         "peak_source": peak_src},
            "gpu_launches": int(launches),
            "plan_stats": {"records": st["records"], "segments": st["segments"],
@@ -363,13 +384,15 @@ def run_single(args):
         out["clocks"] = clocks.stop()
 
     if not (args.no_cpu_baseline or args.profile):
-        n_seq = 12
-        nbytes, dt, ns, ntok = oracle_sample(args.config, args.fields, n_seq)
+        prep, nbytes, ntok = oracle_prepare(args.config, args.fields, CPU_BASELINE_SEQS)
+        dt = oracle_run(prep)
+        del prep
         out["cpu_baseline"] = {
             "value": nbytes / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
             "host_cores": os.cpu_count(), "affinity_cores": cpu_threads(), "seconds": dt,
-            "sample": f"first {ns} sequences ({ntok} tokens, {nbytes} B) of the workload, same "
-                      f"layout shapes over 8 simulated ranks; single-threaded NumPy oracle"}
+            "sample": f"first {CPU_BASELINE_SEQS} sequences ({ntok} tokens, {nbytes} B) of the "
+                      f"workload, same layout shapes over 8 simulated ranks; single-threaded "
+                      f"NumPy oracle, random-bit payload"}
     emit(out)
 
 

@@ -89,6 +89,38 @@ class EmulatedDispatch:
         return cu, ids[:ns], ts[:ns]
 
 
+def allgather_lengths(local_lens: torch.Tensor, group=None):
+    """Step a1: every rank learns the global int32 length vector in rank
+    order -- first the per-rank counts (int64), then the lengths padded to the largest count.
+    Works on any torch.distributed backend (tensors stay on local_lens.device).
+    Returns (global int32 tensor, per-rank counts)."""
+    import torch.distributed as dist
+    dev = local_lens.device
+    world = dist.get_world_size(group)
+    n = torch.tensor([local_lens.numel()], dtype=torch.int64, device=dev)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n, group=group)
+    counts = [int(c.item()) for c in counts]
+    m = max(counts) if counts else 0
+    pad = torch.zeros(max(m, 1), dtype=torch.int32, device=dev)
+    pad[: local_lens.numel()] = local_lens.to(torch.int32)
+    allp = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(allp, pad, group=group)
+    if m == 0:
+        return torch.zeros(0, dtype=torch.int32, device=dev), counts
+    return torch.cat([allp[r][: counts[r]] for r in range(world)]), counts
+
+
+def max_over_ranks(values, group=None):
+    """Element-wise max of a list of floats over the ranks (timing: the slowest rank decides)."""
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return [float(x) for x in t.tolist()]
+
+
 class Dispatcher:
     """One process per GPU (torch.distributed initialised).  Fused P2P exchange."""
 
@@ -106,21 +138,12 @@ class Dispatcher:
             self.comm.import_peers(handles)
 
     def allgather_lens(self, local_lens: torch.Tensor):
-        """Step a1: every rank learns the global lengths (counts first, then padded lengths).
-        Returns (global int32 device tensor, per-rank counts list)."""
-        dist = self.dist
-        n = torch.tensor([local_lens.numel()], dtype=torch.int64, device=self.device)
-        counts = [torch.zeros_like(n) for _ in range(self.world)]
-        dist.all_gather(counts, n, group=self.group)
-        counts = [int(c.item()) for c in counts]
-        m = max(counts) if counts else 0
-        pad = torch.zeros(max(m, 1), dtype=torch.int32, device=self.device)
-        pad[: local_lens.numel()] = local_lens.to(torch.int32)
-        allp = [torch.zeros_like(pad) for _ in range(self.world)]
-        dist.all_gather(allp, pad, group=self.group)
-        glob = torch.cat([allp[r][: counts[r]] for r in range(self.world)]) if m else \
-            torch.zeros(0, dtype=torch.int32, device=self.device)
-        return glob, counts
+        """Step a1 (see allgather_lengths) on this dispatcher's process group; gloo groups
+        (tests) run the collective on host tensors."""
+        backend = self.dist.get_backend(self.group)
+        dev = self.device if backend == "nccl" else torch.device("cpu")
+        glob, counts = allgather_lengths(local_lens.to(dev), self.group)
+        return glob.to(self.device), counts
 
     def plan(self, src, dst, seq_lens: torch.Tensor, fields, stream=None):
         self._src = layout_for_device(src, self.device)

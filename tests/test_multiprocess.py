@@ -1,0 +1,82 @@
+"""N > 1 path with one process per rank.
+
+* CPU (gloo, world 2 and 4): host-side logic -- length all-gather (step a1), max-over-ranks
+  timing reduction, window-handle exchange plumbing.
+* GPU (marked gpu): W processes on one B200 exchange through CUDA-IPC-mapped windows with the
+  fused P2P exec and its epoch barrier; bit-exact against the oracle, several execs in a row.
+"""
+import multiprocessing as mp
+import random
+import socket
+
+import pytest
+
+from paper_2510_05943_b200 import workloads as W
+from tests import mp_worker
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def run_procs(target, world, extra=(), timeout=240):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + tuple(extra)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, msg = q.get(timeout=timeout)
+            res[r] = msg
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    bad = {r: m for r, m in res.items() if m != "ok"}
+    assert not bad, bad
+    assert len(res) == world
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_host_logic(world):
+    run_procs(mp_worker.cpu_main, world)
+
+
+def _gpu_ok():
+    import torch
+    return torch.cuda.is_available()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1_dp2_dp1", "c3_dp4_tp4", "c4_dp4_sp2", "random"])
+def test_p2p_exec_processes_share_one_gpu(name):
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    f3 = W.field_set("tiny3") + [("m", 1, 1, "mask")]
+    if name == "c1_dp2_dp1":
+        world, lens = 2, W.TINY_LENGTHS.tolist()
+        src, dst = W.rollout_layout(8, 2), W.layout(dp=1, assign="contig")
+    elif name == "c3_dp4_tp4":
+        world, lens = 4, W.c2_lengths(0)[:40].tolist()
+        src, dst = W.config_layouts("c3", 4, 40)
+    elif name == "c4_dp4_sp2":
+        world, lens = 4, W.c4_lengths(0)[:10].tolist()
+        src, dst = W.config_layouts("c4", 4, 10)
+    else:
+        from tests.helpers import random_layout
+        rng = random.Random(3)
+        world, n = 3, 30
+        lens = [rng.randint(0, 300) for _ in range(n)]
+        src = random_layout(rng, world, n, allow_lpt=True)
+        dst = random_layout(rng, world, n, allow_lpt=True)
+    run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 3),), timeout=600)
