@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c2-lpt", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c2-lpt", "c5", "c5-lt"])
+    ap.add_argument("--n-seqs", type=int, default=512, help="c5/c5-lt: sequences in the batch")
     ap.add_argument("--fields", default="scalar6-fp32+hidden2560")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -72,23 +73,26 @@ def ncu_traffic(desc):
     return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
 
 
-def workload(config, n_ranks, fields_name):
+def workload(config, n_ranks, fields_name, n_seqs=512):
     from paper_2510_05943_b200 import workloads as W
     if config in ("c3", "c2-lpt"):
         lens = W.c2_lengths(0)
     elif config == "c4":
         lens = W.c4_lengths(0)
-    else:  # c5: uniform lengths, round robin
-        lens = [4096] * 512
+    elif config == "c5":  # sweep series, uniform lengths, round-robin all-to-allv
+        lens = [4096] * n_seqs
+    else:  # c5-lt: sweep series with the C2 long-tail length distribution
+        lens = W.lognormal_lengths(n_seqs, 2048, 0.75, 64, 8192, 0)
     import numpy as np
     lens = np.asarray(lens, dtype=np.int64)
-    src, dst = W.config_layouts(config, n_ranks, len(lens))
+    src, dst = W.config_layouts("c5" if config == "c5-lt" else config, n_ranks, len(lens))
     fields = W.field_set(fields_name)
     names = {
         "c3": "C2/C3 4B-class Tic-Tac-Toe batch: 512 episodes, lognormal(2048, 0.75) clip [64,8192]",
         "c4": "C4 70B-class long context: 256 episodes, lognormal(8192, 0.6) clip [4096,32768]",
         "c2-lpt": "C2 batch, LPT rebalance",
-        "c5": "C5 uniform all-to-allv, L=4096",
+        "c5": f"C5 uniform all-to-allv, {n_seqs} x L=4096",
+        "c5-lt": f"C5 long-tail all-to-allv, {n_seqs} episodes lognormal(2048, 0.75) clip [64,8192]",
     }
     lay = lambda L: (f"DP{L['dp']}" + (f"xSP{L['sp']}" if L['sp'] > 1 else "")
                      + (f"xTP{L['tp']}" if L['tp'] > 1 else "") + f"[{L['assign']}]")
@@ -225,7 +229,7 @@ def run_single(args):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     R = 8
-    lens, src, dst, fields, desc = workload(args.config, R, args.fields)
+    lens, src, dst, fields, desc = workload(args.config, R, args.fields, args.n_seqs)
     F = len(fields)
     Bf = [b * e for (_, b, e, _) in fields]
     ed = EmulatedDispatch(R)
@@ -410,11 +414,19 @@ def run_multi(args):
     from paper_2510_05943_b200.dispatch import Dispatcher
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # EARL_SHARED_GPU=1: every rank on cuda:0 with gloo plumbing -- validates the N>1 code path
+    # on a one-GPU box (ranks time-slice the GPU, so its numbers are not performance numbers)
+    shared = os.environ.get("EARL_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     rank, world = dist.get_rank(), dist.get_world_size()
-    lens, src, dst, fields, desc = workload(args.config, world, args.fields)
+    lens, src, dst, fields, desc = workload(args.config, world, args.fields, args.n_seqs)
     F = len(fields)
     B = W.bytes_per_token(fields)
     T = int(lens.sum())
@@ -460,12 +472,10 @@ def run_multi(args):
     dist.barrier()
     t1 = time.time()
     launches = earl.kernel_launch_count() - l0
-    ms = torch.tensor([a.elapsed_time(b) / args.steps,
-                       sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps,
-                       statistics.median(e[0].elapsed_time(e[1]) for e in evs)],
-                      dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_step, t_exec, t_plan = [float(x) for x in ms.tolist()]
+    from paper_2510_05943_b200.dispatch import max_over_ranks
+    ms_step, t_exec, t_plan = max_over_ranks([a.elapsed_time(b) / args.steps,
+                                              sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps,
+                                              statistics.median(e[0].elapsed_time(e[1]) for e in evs)])
     plan = D.plan(src, dst, glens, fields)
     plan.sync()
     plan.destroy()
@@ -478,7 +488,8 @@ def run_multi(args):
                "data": "synthetic (seeded device draws)",
                "config": {"workload": desc, "global_batch": int(len(lens)), "tokens": T,
                           "bytes_per_token": B, "payload_bytes": payload,
-                          "l2": "inputs larger than L2", "parallelism": f"{world} ranks, P2P"},
+                          "l2": "inputs larger than L2", "parallelism": f"{world} ranks, P2P",
+                          "shared_gpu": shared},
                "per_gpu_GBps": payload / (ms_step * 1e-3) / 1e9 / world,
                "t_plan_ms": t_plan, "t_exec_ms": t_exec,
                "roofline": {"bound": "nvlink", "kernel": "entry barrier + copy_kernel (P2P)",

@@ -41,15 +41,19 @@ earl_status_t fail(earl_status_t st, const char* fmt, ...) {
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev && cudaSetDevice(dev) != cudaSuccess) cudaGetLastError();
   }
   ~DeviceGuard() {
     int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    if (cudaGetDevice(&cur) != cudaSuccess) cur = -1;
+    if (prev >= 0 && cur != prev && cudaSetDevice(prev) != cudaSuccess) cudaGetLastError();
   }
 };
+
+// Launch checks read cudaGetLastError(); clear any stale error left by an unrelated earlier
+// runtime call first, so a launch is never blamed for someone else's failure.
+inline void clear_stale_error() { (void)cudaGetLastError(); }
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -70,7 +74,23 @@ struct earl_comm {
   unsigned int* done_ctr = nullptr;
   int sm_count = 148;
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+  int refs = 1;          // the user's handle + one per live plan: freed when it reaches 0
 };
+
+namespace {
+void comm_release(earl_comm* c) {
+  if (--c->refs > 0) return;
+  DeviceGuard g(c->device);
+  cudaDeviceSynchronize();
+  for (int p = 0; p < kMaxWorld; ++p)
+    if (c->peer_mapped[p]) cudaIpcCloseMemHandle(c->peer[p]);
+  for (int r = 0; r < kMaxWorld; ++r)
+    if (c->win[r]) cudaFree(c->win[r]);
+  if (c->done_ctr) cudaFree(c->done_ctr);
+  cudaGetLastError();
+  delete c;
+}
+}  // namespace
 
 struct earl_plan {
   earl_comm* comm = nullptr;
@@ -225,16 +245,11 @@ extern "C" earl_status_t earl_comm_info(earl_comm_t c, int32_t* rank, int32_t* w
   return EARL_OK;
 }
 
+// Plans hold a reference: the comm's resources outlive every plan made on it, whatever order
+// the caller (or a garbage collector) destroys them in.
 extern "C" earl_status_t earl_comm_destroy(earl_comm_t c) {
   if (!c) return EARL_OK;
-  DeviceGuard g(c->device);
-  cudaDeviceSynchronize();
-  for (int p = 0; p < kMaxWorld; ++p)
-    if (c->peer_mapped[p]) cudaIpcCloseMemHandle(c->peer[p]);
-  for (int r = 0; r < kMaxWorld; ++r)
-    if (c->win[r]) cudaFree(c->win[r]);
-  if (c->done_ctr) cudaFree(c->done_ctr);
-  delete c;
+  comm_release(c);
   return EARL_OK;
 }
 
@@ -364,6 +379,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
 
   earl_plan* p = new earl_plan();
   p->comm = c;
+  c->refs += 1;
   p->N = n_seqs;
   p->n_fields = n_fields;
   p->stream = s;
@@ -395,10 +411,12 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   total += sz((int64_t)src->sp * (N + 1), 8) + sz((int64_t)dst->sp * (N + 1), 8);
   total += sz(N + 1, 8);
   total += 8 * sz(max_pieces, 4) + sz(max_pieces + 1, 8);
+  total += sz(kMaxPlanGrid, 8) + sz((int64_t)kMaxPlanGrid * kMaxKeys, 4);
   total += 4 * sz(max_records, 4) + 3 * sz(max_records, 8) + sz(max_records + 1, 8);
   p->mem_bytes = total;
   cudaError_t e = cudaMallocAsync(&p->mem, total, s);
   if (e != cudaSuccess) {
+    c->refs -= 1;
     delete p;
     return fail(EARL_ERR_CUDA, "plan cudaMallocAsync(%zu): %s", total, cudaGetErrorString(e));
   }
@@ -424,6 +442,8 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   a.ps_y = carve<int32_t>(q, max_pieces);
   a.ps_kk = carve<int32_t>(q, max_pieces);
   a.ps_scan = carve<int64_t>(q, max_pieces + 1);
+  a.cta_sums = carve<int64_t>(q, kMaxPlanGrid);
+  a.ghist = carve<int32_t>(q, (int64_t)kMaxPlanGrid * kMaxKeys);
   a.rec.seq = carve<int32_t>(q, max_records);
   a.rec.x = carve<int32_t>(q, max_records);
   a.rec.n = carve<int32_t>(q, max_records);
@@ -435,6 +455,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
 
   auto abort_plan = [&](earl_status_t code, const char* what, cudaError_t err) {
     cudaFreeAsync(p->mem, s);
+    c->refs -= 1;
     delete p;
     return fail(code, "%s: %s", what, cudaGetErrorString(err));
   };
@@ -447,7 +468,9 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
     while (n2 < N) n2 <<= 1;
     lpt_smem = (size_t)n2 * sizeof(uint64_t);
   }
-  e = launch_planner(a, lpt_smem, s);
+  const int grid = planner_grid(N, max_pieces, c->sm_count, lpt_smem);
+  clear_stale_error();
+  e = launch_planner(a, lpt_smem, grid, s);
   if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "planner launch", e);
   g_launches.fetch_add(1);
   e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming);
@@ -485,6 +508,7 @@ extern "C" earl_status_t earl_plan_local_meta(earl_plan_t p, int32_t rank, int32
   int g, k, t;
   if (!coords(p->lay[1], rank, &g, &k, &t)) return EARL_OK;  // not a destination: nothing
   DeviceGuard dg(p->comm->device);
+  clear_stale_error();
   cudaError_t e = launch_local_meta(p->args, g, k, cu, ids, tok_start, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "local_meta launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
@@ -605,9 +629,13 @@ extern "C" earl_status_t earl_plan_export(earl_plan_t p, int64_t capacity, int64
 
 extern "C" earl_status_t earl_plan_destroy(earl_plan_t p) {
   if (!p) return EARL_OK;
-  DeviceGuard g(p->comm->device);
-  if (p->mem) cudaFreeAsync(p->mem, p->stream);
-  if (p->ev) cudaEventDestroy(p->ev);
+  {
+    DeviceGuard g(p->comm->device);
+    if (p->mem) cudaFreeAsync(p->mem, p->stream);
+    if (p->ev) cudaEventDestroy(p->ev);
+    cudaGetLastError();
+  }
+  comm_release(p->comm);
   delete p;
   return EARL_OK;
 }
@@ -663,6 +691,7 @@ CopyTrace& trace_state() {
   return t;
 }
 cudaError_t traced_launch(CopyArgs& a, earl_comm* c, cudaStream_t s) {
+  clear_stale_error();
   CopyTrace& t = trace_state();
   if (!t.path) return launch_copy(a, copy_grid(c), 0, s);
   const size_t n = (size_t)c->sm_count * 64 * 4;
@@ -752,6 +781,7 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
     uint64_t* pads[kMaxWorld] = {};
     for (int q = 0; q < c->world; ++q) pads[q] = reinterpret_cast<uint64_t*>(c->peer[q]);
     for (int q = 0; q < kMaxWorld; ++q) a.peer_pad[q] = pads[q];
+    clear_stale_error();
     cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, a.epoch, c->timeout_ns,
                                          a.err, a.err_detail, s);
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));

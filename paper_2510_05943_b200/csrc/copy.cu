@@ -91,13 +91,29 @@ __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world,
 // congruent path, so the bytes in flight per SM are set by the ring, not by occupancy.
 // ---------------------------------------------------------------------------------------
 
-struct __align__(16) ChunkDesc {
+// One contiguous source range landed in a stage at stage offset `so` (a stage holds up to
+// kSubs of them: small pieces share a stage, so the bytes in flight are set by the ring and
+// not by the number of pieces).
+struct __align__(16) SubDesc {
   const uint8_t* src_al;  // 16-B aligned source address of the load
+  uint8_t* dst0;          // destination of the first byte for replica 0
+  uint32_t so;            // stage offset of the load (multiple of 16)
   uint32_t load_bytes;    // multiple of 16
-  uint32_t off;           // first chunk byte inside the stage (src & 15)
-  uint32_t len;           // chunk bytes
-  uint32_t R;             // destination replicas
-  uint8_t* dst[kMaxWorld];
+  uint32_t len;           // bytes
+  uint8_t off;            // src & 15
+  uint8_t R;              // destination replicas
+  uint8_t f;              // field (replica base lookup)
+  uint8_t d0;             // destination rank of replica 0 (direct / unpack)
+};
+static_assert(sizeof(SubDesc) == 32, "SubDesc layout");
+
+constexpr int kSubs = 32;        // sub-ranges per stage
+constexpr uint32_t kMinSpace = 256;  // close a stage when less than this is left
+
+struct __align__(16) StageDesc {
+  uint32_t n;
+  uint32_t pad_[3];
+  SubDesc sub[kSubs];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -146,42 +162,75 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Lane-0-only walker over a warp's slice of the launch's work.  Work is measured in a cost
-// space, not in bytes: piece (record j, field f) costs its n_j * B_f bytes plus c0, the
-// byte-equivalent of one chunk round trip, so a warp whose slice holds thousands of small
-// scalar pieces gets proportionally fewer bytes (equal-byte slices made those warps the
-// stragglers: profiles/r01_trace.txt).  Cost offsets [0, n_j*B_f) of a piece map 1:1 to its
-// bytes; the trailing c0 maps to no bytes, so slices partition the bytes exactly.
+// Lane-0-only walker over a warp's share of the launch's work.
+//
+// Work is measured in a record-major cost space: record j (all fields) occupies
+// [cost(j), cost(j+1)) with cost(j) = (tok_prefix[j] - tbeg) * B + (j - rbeg) * F * c0, and
+// field f of record j is the sub-interval starting at n_j * Bpre[f] + f * c0 whose first
+// n_j * B_f cost units map 1:1 to its bytes, followed by c0 units that map to no bytes (the
+// fixed cost of a piece).  Equal-byte slices made the warps holding thousands of small scalar
+// pieces the stragglers (profiles/r01_trace.txt); the c0 term balances them.  Record-major
+// order loads a record's metadata once for all of its fields.
 struct Walker {
   const CopyArgs* a;
   const PlanHeader* h;
   int64_t rbeg, rend, tbeg;
-  uint64_t ntok, nrec, c0, x1, xpos;
+  uint64_t c0, x1, xpos, unit, n_units, first_dyn;
+  unsigned int* work_ctr;
+  int F;
+  // current record
   int64_t j;
   int f;
+  uint64_t n, cj, fo;          // tokens, cost start, cost offset of field f inside the record
+  int s, ds, ts, d0;
+  int64_t src_tok, dst_tok, msg_tok, kt, msg_base, fb;
+  // current piece (its own field and replica-0 rank: the walker may already have advanced)
   const uint8_t* psrc;
-  uint8_t* pdst[kMaxWorld];
+  uint8_t* pdst;
   uint32_t R;
   uint64_t prem;
+  int pf, pd0;
 
-  __device__ uint64_t field_cost(int ff) const {
-    return ntok * a->Bpre[ff] + (uint64_t)ff * nrec * c0;
+  __device__ uint64_t cost(int64_t jj) const {
+    return (uint64_t)(a->rec.tok_prefix[jj] - tbeg) * a->Bpre[F] + (uint64_t)(jj - rbeg) * F * c0;
   }
-  __device__ uint64_t rec_cost(int64_t jj, int ff) const {
-    return field_cost(ff) + (uint64_t)(a->rec.tok_prefix[jj] - tbeg) * a->Bf[ff] +
-           (uint64_t)(jj - rbeg) * c0;
-  }
-
-  // dynamic scheduling: further units of `unit` cost come from a plan-owned counter
-  uint64_t unit, n_units, first_dyn;
-  unsigned int* work_ctr;
+  __device__ uint64_t total() const { return cost(rend); }
 
   __device__ void setup(const CopyArgs* a_, int64_t rbeg_, int64_t rend_, int64_t tbeg_,
-                        uint64_t ntok_, uint64_t c0_, uint64_t unit_, uint64_t n_units_,
-                        uint64_t first_dyn_) {
-    a = a_; h = a_->hdr; rbeg = rbeg_; rend = rend_; tbeg = tbeg_; ntok = ntok_;
-    nrec = (uint64_t)(rend_ - rbeg_); c0 = c0_; unit = unit_; n_units = n_units_;
-    first_dyn = first_dyn_; work_ctr = a_->work_ctr; prem = 0; R = 0; xpos = x1 = 0;
+                        uint64_t c0_, uint64_t unit_, uint64_t n_units_, uint64_t first_dyn_) {
+    a = a_; h = a_->hdr; rbeg = rbeg_; rend = rend_; tbeg = tbeg_; c0 = c0_; unit = unit_;
+    n_units = n_units_; first_dyn = first_dyn_; work_ctr = a_->work_ctr; F = a_->n_fields;
+    prem = 0; R = 0; xpos = x1 = 0; j = rbeg; f = 0;
+  }
+
+  __device__ void load_record(int64_t jj) {
+    j = jj;
+    const int64_t t0 = a->rec.tok_prefix[jj], t1 = a->rec.tok_prefix[jj + 1];
+    const uint32_t code = a->rec.code[jj];
+    src_tok = a->rec.src_tok[jj];
+    dst_tok = a->rec.dst_tok[jj];
+    n = (uint64_t)(t1 - t0);
+    cj = (uint64_t)(t0 - tbeg) * a->Bpre[F] + (uint64_t)(jj - rbeg) * F * c0;
+    s = code & 0xff;
+    const int ss = (code >> 8) & 0xff;
+    ds = (code >> 16) & 0xff;
+    ts = code >> 24;
+    d0 = a->rank0_d + ds * a->tp_d + ts;
+    if (a->mode != kDirect) {
+      const int key = ss * a->n_dst_shards + ds;
+      msg_tok = a->rec.msg_tok[jj];
+      kt = h->key_tokens[key];
+      msg_base = h->msg_off[key];
+    }
+    f = 0;
+    fo = 0;
+    fb = 0;
+  }
+
+  __device__ void next_field() {
+    if (a->mode != kDirect) fb += (kt * a->Bf[f] + 15) & ~15LL;
+    fo += n * a->Bf[f] + c0;
+    ++f;
   }
 
   // Claim the next unit: returns false when the launch's work is exhausted.
@@ -193,64 +242,60 @@ struct Walker {
   }
 
   __device__ void start(uint64_t x0, uint64_t x1_) {
-    const uint64_t total = field_cost(a->n_fields);
-    x1 = x1_ < total ? x1_ : total;
+    const uint64_t tot = total();
+    x1 = x1_ < tot ? x1_ : tot;
     xpos = x0;
     prem = 0;
-    f = 0;
-    j = rbeg;
     if (xpos >= x1) return;
-    while (xpos >= field_cost(f + 1)) ++f;
     int64_t lo = rbeg, hi = rend - 1;  // last record whose cost interval starts <= xpos
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
-      if (rec_cost(mid, f) <= xpos) lo = mid; else hi = mid - 1;
+      if (cost(mid) <= xpos) lo = mid; else hi = mid - 1;
     }
-    j = lo;
+    load_record(lo);
+    while (f + 1 < F && cj + fo + n * a->Bf[f] + c0 <= xpos) next_field();
   }
 
   __device__ bool next_piece() {
-    const int Sd = a->n_dst_shards;
     while (xpos < x1) {
       const uint64_t Bf = a->Bf[f];
-      const uint64_t cj = rec_cost(j, f);
-      const uint64_t nb = (uint64_t)(a->rec.tok_prefix[j + 1] - a->rec.tok_prefix[j]) * Bf;
-      const uint64_t cend = cj + nb + c0;
-      const uint64_t lo = xpos - cj;
-      const uint64_t hi = (x1 < cend ? x1 : cend) - cj;
+      const uint64_t nb = n * Bf;
+      const uint64_t fstart = cj + fo, fend = fstart + nb + c0;
+      const uint64_t lo = xpos - fstart;
+      const uint64_t hi = (x1 < fend ? x1 : fend) - fstart;
       const uint64_t u0 = lo < nb ? lo : nb;
       const uint64_t u1 = hi < nb ? hi : nb;
       bool found = false;
       if (u1 > u0) {
-        const uint32_t code = a->rec.code[j];
-        const int s = code & 0xff, ss = (code >> 8) & 0xff, ds = (code >> 16) & 0xff, ts = code >> 24;
         int64_t msg_field = 0;
-        if (a->mode != kDirect) {
-          const int key = ss * Sd + ds;
-          const int64_t kt = h->key_tokens[key];
-          int64_t fb = 0;
-          for (int ff = 0; ff < f; ++ff) fb += (kt * a->Bf[ff] + 15) & ~15LL;
-          msg_field = h->msg_off[key] + fb + a->rec.msg_tok[j] * (int64_t)Bf + (int64_t)u0;
-        }
+        if (a->mode != kDirect) msg_field = msg_base + fb + msg_tok * (int64_t)Bf + (int64_t)u0;
         psrc = (a->mode == kUnpack) ? a->stage[s] + msg_field
-                                    : a->src[s][f] + a->rec.src_tok[j] * (int64_t)Bf + (int64_t)u0;
-        R = 0;
+                                    : a->src[s][f] + src_tok * (int64_t)Bf + (int64_t)u0;
         if (a->mode == kPack) {
-          pdst[R++] = a->stage[s] + msg_field;
+          pdst = a->stage[s] + msg_field;
+          R = 1;
         } else {
-          const int64_t doff = a->rec.dst_tok[j] * (int64_t)Bf + (int64_t)u0;
-          for (int td = ts; td < a->tp_d; td += a->tp_s) {
-            uint8_t* base = a->dst[a->rank0_d + ds * a->tp_d + td][f];
-            if (base != nullptr) pdst[R++] = base + doff;
-          }
+          R = 0;
+          uint8_t* base0 = a->dst[d0][f];
+          for (int td = ts; td < a->tp_d; td += a->tp_s)
+            if (a->dst[d0 + (td - ts)][f] != nullptr) ++R;
+          pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
+          if (base0 == nullptr) R = 0;
         }
         prem = u1 - u0;
+        pf = f;
+        pd0 = d0;
         found = R > 0;
       }
-      if (x1 >= cend) {
-        xpos = cend;
-        ++j;
-        if (j == rend) { j = rbeg; ++f; }
+      if (x1 >= fend) {
+        xpos = fend;
+        if (f + 1 < F) {
+          next_field();
+        } else if (j + 1 < rend) {
+          load_record(j + 1);
+        } else {
+          xpos = x1;
+        }
       } else {
         xpos = x1;
       }
@@ -259,64 +304,120 @@ struct Walker {
     return false;
   }
 
-  template <int CHUNK>
-  __device__ bool next_chunk(ChunkDesc& d) {
+  // Next source range of at most `space` stage bytes (space >= kMinSpace): false when the
+  // launch's work is exhausted.
+  __device__ bool next_sub(SubDesc& d, uint32_t space) {
     while (prem == 0 && !next_piece())
       if (!claim()) return false;
     const uint32_t off = (uint32_t)((uintptr_t)psrc & 15);
-    const uint64_t room = CHUNK - off;
+    const uint64_t room = space - off;
     const uint32_t len = (uint32_t)(prem < room ? prem : room);
     d.src_al = psrc - off;
-    d.off = off;
+    d.dst0 = pdst;
+    d.off = (uint8_t)off;
     d.len = len;
     d.load_bytes = (off + len + 15) & ~15u;
-    d.R = R;
-    for (uint32_t r = 0; r < R; ++r) { d.dst[r] = pdst[r]; pdst[r] += len; }
+    d.R = (uint8_t)R;
+    d.f = (uint8_t)pf;
+    d.d0 = (uint8_t)pd0;
     psrc += len;
+    pdst += len;
     prem -= len;
     return true;
   }
 };
 
-// Store one landed chunk (whole warp).
-__device__ __forceinline__ void store_chunk(const ChunkDesc& D, uint8_t* stage, int lane) {
-  const uint32_t len = D.len, R = D.R, off = D.off;
-  const uint8_t* sm = stage + off;
-  uint8_t* d0 = D.dst[0];
-  uint32_t head = (16 - (uint32_t)((uintptr_t)d0 & 15)) & 15;
+// Fill stage `st` (lane 0): pack source ranges until the stage is full, then one expect_tx for
+// the total and one TMA load per range, all completing on the stage's mbarrier.
+template <int CHUNK>
+__device__ __forceinline__ bool fill_stage(Walker& wk, StageDesc& sd, uint8_t* stage, uint64_t* bar) {
+  uint32_t used = 0, n = 0;
+  while (n < (uint32_t)kSubs && CHUNK - used >= kMinSpace) {
+    if (!wk.next_sub(sd.sub[n], CHUNK - used)) break;
+    sd.sub[n].so = used;
+    used += sd.sub[n].load_bytes;
+    ++n;
+  }
+  sd.n = n;
+  if (n == 0) return false;
+  mbar_expect_tx(bar, used);
+  for (uint32_t k = 0; k < n; ++k)
+    tma_load(stage + sd.sub[k].so, sd.sub[k].src_al, sd.sub[k].load_bytes, bar);
+  return true;
+}
+
+// Store one landed source range to its R destination replicas (whole warp); R is a
+// compile-time constant so the replica pointers stay in registers and the realign loop is
+// ~12 instructions per 512 B (a runtime-R loop cost ~100: profiles/r01_c5lt_note.txt).
+template <int R>
+__device__ __forceinline__ void store_sub_r(const CopyArgs& a, const SubDesc& S, uint8_t* stage,
+                                            int lane) {
+  const uint32_t len = S.len;
+  const uint8_t* sm = stage + S.so + S.off;
+  uint8_t* dp[R];
+  dp[0] = S.dst0;
+#pragma unroll
+  for (int r = 1; r < R; ++r)
+    dp[r] = S.dst0 + (a.dst[S.d0 + r * a.tp_s][S.f] - a.dst[S.d0][S.f]);
+  uint32_t head = (16 - (uint32_t)((uintptr_t)S.dst0 & 15)) & 15;
   if (head > len) head = len;
   if (lane < (int)head) {
     const uint8_t v = sm[lane];
-    for (uint32_t r = 0; r < R; ++r) D.dst[r][lane] = v;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r][lane] = v;
   }
   const uint32_t rest = len - head;
   const uint32_t nvec = rest >> 4;
   if (nvec > 0) {
-    const uint32_t smo = off + head;
+    const uint32_t smo = S.so + S.off + head;
     if ((smo & 15) == 0) {
-      if (lane == 0)
-        for (uint32_t r = 0; r < R; ++r) tma_store(D.dst[r] + head, stage + smo, nvec * 16);
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) tma_store(dp[r] + head, stage + smo, nvec * 16);
+      }
     } else {
-      const uint32_t base16 = smo & ~15u, sh = smo & 15;
+      const uint32_t sh = smo & 15;
       const int s4 = (int)(sh >> 2), bits = (int)(sh & 3) * 8;
+      const uint8_t* sp = stage + (smo & ~15u) + 16 * lane;
+      uint8_t* q[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) q[r] = dp[r] + head + 16 * lane;
+#pragma unroll 2
       for (uint32_t k = lane; k < nvec; k += 32) {
-        const uint4 w0 = *reinterpret_cast<const uint4*>(stage + base16 + 16 * k);
-        const uint4 w1 = *reinterpret_cast<const uint4*>(stage + base16 + 16 * k + 16);
+        const uint4 w0 = *reinterpret_cast<const uint4*>(sp);
+        const uint4 w1 = *reinterpret_cast<const uint4*>(sp + 16);
         const uint4 o = realign(w0, w1, s4, bits);
-        for (uint32_t r = 0; r < R; ++r) st_v4(D.dst[r] + head + 16 * k, o);
+#pragma unroll
+        for (int r = 0; r < R; ++r) { st_v4(q[r], o); q[r] += 512; }
+        sp += 512;
       }
     }
   }
   const uint32_t t0 = head + nvec * 16;
   if (lane < (int)(len - t0)) {
     const uint8_t v = sm[t0 + lane];
-    for (uint32_t r = 0; r < R; ++r) D.dst[r][t0 + lane] = v;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r][t0 + lane] = v;
+  }
+}
+
+__device__ __forceinline__ void store_sub(const CopyArgs& a, const SubDesc& S, uint8_t* stage,
+                                          int lane) {
+  switch (S.R) {
+    case 1: store_sub_r<1>(a, S, stage, lane); break;
+    case 2: store_sub_r<2>(a, S, stage, lane); break;
+    case 3: store_sub_r<3>(a, S, stage, lane); break;
+    case 4: store_sub_r<4>(a, S, stage, lane); break;
+    case 5: store_sub_r<5>(a, S, stage, lane); break;
+    case 6: store_sub_r<6>(a, S, stage, lane); break;
+    case 7: store_sub_r<7>(a, S, stage, lane); break;
+    default: store_sub_r<8>(a, S, stage, lane); break;
   }
 }
 
 template <int WARPS, int STAGES, int CHUNK>
 constexpr size_t copy_smem_bytes() {
-  return (size_t)WARPS * STAGES * CHUNK + (size_t)WARPS * STAGES * (sizeof(ChunkDesc) + 8);
+  return (size_t)WARPS * STAGES * CHUNK + (size_t)WARPS * STAGES * (sizeof(StageDesc) + 8);
 }
 
 template <int WARPS, int STAGES, int CHUNK>
@@ -325,9 +426,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
   __shared__ unsigned s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint8_t* data = smem + (size_t)w * STAGES * CHUNK;
-  ChunkDesc* desc = reinterpret_cast<ChunkDesc*>(smem + (size_t)WARPS * STAGES * CHUNK) + w * STAGES;
+  StageDesc* desc = reinterpret_cast<StageDesc*>(smem + (size_t)WARPS * STAGES * CHUNK) + w * STAGES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CHUNK +
-                                              (size_t)WARPS * STAGES * sizeof(ChunkDesc)) + w * STAGES;
+                                              (size_t)WARPS * STAGES * sizeof(StageDesc)) + w * STAGES;
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
@@ -335,38 +436,33 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
   __syncwarp();
   const PlanHeader* h = a.hdr;
   if (h->err == 0) {
-    int64_t rbeg, rend, tbeg, tend;
+    int64_t rbeg, rend, tbeg;
     if (a.view_rank < 0) {
-      rbeg = 0; rend = h->n_records; tbeg = 0; tend = h->rec_tokens;
+      rbeg = 0; rend = h->n_records; tbeg = 0;
     } else {
       rbeg = h->rec_begin[a.view_rank]; rend = h->rec_begin[a.view_rank + 1];
-      tbeg = h->rec_tok_begin[a.view_rank]; tend = h->rec_tok_begin[a.view_rank + 1];
+      tbeg = h->rec_tok_begin[a.view_rank];
     }
-    const uint64_t ntok = (uint64_t)(tend - tbeg);
-    const uint64_t c0 = CHUNK;
-    const uint64_t total = ntok * a.Bpre[a.n_fields] + (uint64_t)a.n_fields * (rend - rbeg) * c0;
+    const uint64_t c0 = CHUNK / 4;
     const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
     const uint64_t wid = (uint64_t)blockIdx.x * WARPS + w;
-    // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
-    uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
-    if (unit < 4 * (uint64_t)CHUNK) unit = 4 * (uint64_t)CHUNK;
-    const uint64_t n_units = (total + unit - 1) / unit;
-    const uint64_t b0 = wid * unit, b1 = b0 + unit;
     Walker wk;
     uint64_t t_start = 0;
+    int nprod = 0;
     if (lane == 0) {
       if (a.trace) t_start = globaltimer();
-      wk.setup(&a, rbeg, rend, tbeg, ntok, c0, unit, n_units, nwarps);
-      if (wid < n_units) wk.start(b0, b1);
+      wk.setup(&a, rbeg, rend, tbeg, c0, 0, 0, nwarps);
+      const uint64_t total = rend > rbeg ? wk.total() : 0;
+      // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
+      uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
+      if (unit < 4 * (uint64_t)CHUNK) unit = 4 * (uint64_t)CHUNK;
+      wk.unit = unit;
+      wk.n_units = (total + unit - 1) / unit;
+      if (wid < wk.n_units) wk.start(wid * unit, (wid + 1) * unit);
     }
-    int nprod = 0;
     for (int s = 0; s < STAGES - 1; ++s) {
       int ok = 0;
-      if (lane == 0 && wk.next_chunk<CHUNK>(desc[s])) {
-        mbar_expect_tx(&bar[s], desc[s].load_bytes);
-        tma_load(data + (size_t)s * CHUNK, desc[s].src_al, desc[s].load_bytes, &bar[s]);
-        ok = 1;
-      }
+      if (lane == 0) ok = fill_stage<CHUNK>(wk, desc[s], data + (size_t)s * CHUNK, &bar[s]);
       ok = __shfl_sync(kFull, ok, 0);
       if (!ok) break;
       ++nprod;
@@ -374,18 +470,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     for (int c = 0; c < nprod; ++c) {
       const int st = c % STAGES;
       mbar_wait(&bar[st], (uint32_t)((c / STAGES) & 1));
-      store_chunk(desc[st], data + (size_t)st * CHUNK, lane);
+      uint8_t* stage = data + (size_t)st * CHUNK;
+      const uint32_t nsub = desc[st].n;
+      for (uint32_t k = 0; k < nsub; ++k) store_sub(a, desc[st].sub[k], stage, lane);
       if (lane == 0) { bulk_commit(); bulk_wait_read1(); }
       __syncwarp();
       int ok = 0;
       if (lane == 0) {
         const int ns = (c + STAGES - 1) % STAGES;
         fence_proxy_async_smem();
-        if (wk.next_chunk<CHUNK>(desc[ns])) {
-          mbar_expect_tx(&bar[ns], desc[ns].load_bytes);
-          tma_load(data + (size_t)ns * CHUNK, desc[ns].src_al, desc[ns].load_bytes, &bar[ns]);
-          ok = 1;
-        }
+        ok = fill_stage<CHUNK>(wk, desc[ns], data + (size_t)ns * CHUNK, &bar[ns]);
       }
       ok = __shfl_sync(kFull, ok, 0);
       if (ok) ++nprod;
@@ -393,7 +487,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     if (lane == 0) bulk_wait_all();
     if (lane == 0 && a.trace) {
       uint64_t* t = a.trace + 4 * wid;
-      t[0] = t_start; t[1] = globaltimer(); t[2] = b1 - b0; t[3] = (uint64_t)nprod;
+      t[0] = t_start; t[1] = globaltimer(); t[2] = wk.unit; t[3] = (uint64_t)nprod;
     }
     __syncwarp();
   }
@@ -458,11 +552,10 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int /*unused*/, cudaStr
   }
   switch (cfg) {
     case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
-    case 2: return launch_cfg<4, 6, 8192>(a, sm_count, s);
-    case 3: return launch_cfg<8, 3, 8192>(a, sm_count, s);
+    case 2: return launch_cfg<4, 4, 8192>(a, sm_count, s);
     case 4: return launch_cfg<2, 8, 8192>(a, sm_count, s);
     case 5: return launch_cfg<16, 2, 4096>(a, sm_count, s);
-    default: return launch_cfg<4, 4, 8192>(a, sm_count, s);
+    default: return launch_cfg<8, 3, 8192>(a, sm_count, s);
   }
 }
 

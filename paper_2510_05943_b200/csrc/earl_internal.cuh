@@ -14,6 +14,7 @@ constexpr int kMaxShards = 8;               // dp*sp <= world <= 8 per layout
 constexpr int kMaxKeys = kMaxShards * kMaxShards;  // (src shard, dst shard) message keys
 constexpr int kPlanThreads = 1024;          // the planner is one CTA
 constexpr int kPadBytes = 4096;             // signal pad at the start of every window
+constexpr int kMaxPlanGrid = 256;           // planner CTAs (cooperative grid) at most
 
 // Layout as the device sees it.  shard = g*sp + k ; rank = rank0 + shard*tp + t.
 struct LayoutDesc {
@@ -81,6 +82,8 @@ struct PlanArgs {
   int32_t* pc_i; int32_t* pc_x; int32_t* pc_y; int32_t* pc_kk;  // kk = ks | kd<<8 | key<<16
   int32_t* ps_i; int32_t* ps_x; int32_t* ps_y; int32_t* ps_kk;
   int64_t* ps_scan;          // [max_pieces+1]
+  int64_t* cta_sums;         // [kMaxPlanGrid] grid-scan partials
+  int32_t* ghist;            // [kMaxPlanGrid][kMaxKeys] grid-partition histograms
   int64_t max_pieces;
   int64_t max_records;
   Records rec;
@@ -125,7 +128,8 @@ constexpr int kReadySlot = 0;
 constexpr int kDoneSlot = 8;
 
 // launchers (defined in the .cu files)
-cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, cudaStream_t s);
+int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
+cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int unused, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
                                  uint64_t epoch, uint64_t timeout_ns, int32_t* err,

@@ -1,13 +1,14 @@
 // planner.cu -- device-side dispatch planner.
 //
-// One CTA of 1024 threads computes the whole plan in phases separated by __syncthreads, so the
-// plan needs no host synchronisation, no inter-CTA protocol and is bit-for-bit deterministic
-// (every rank computes the identical plan from the identical lengths; integer arithmetic only).
-// The planner is latency-bound integer work (a few µs at the configs' N <= 512); every scan
-// walks tiles of 4096 items with a block-wide warp-shuffle scan and carries the running total.
+// One cooperative grid of G CTAs x 1024 threads computes the whole plan in phases separated by
+// grid-wide barriers.  G scales with the batch (G = ceil(N / 4096), at most one CTA per SM), so
+// the configs' N <= 512 run as a single CTA (barriers degenerate to __syncthreads) while the
+// bandwidth sweep's 4e5 sequences spread over ~100 SMs.  There is no host synchronisation, and
+// the plan is bit-for-bit deterministic for any G (integer arithmetic only; every scan and
+// partition is order-defined), so every rank computes the identical plan from identical lengths.
 //
 // Phases ("adaptive to the current data distribution layout and parallelism
-// configuration"; the steps follow SURVEY.md §8(c) and the readings in DESIGN.md):
+// configuration"; the steps follow SURVEY.md §8(c) and the readings in DESIGN.md §2):
 //   0  P = exclusive scan of L (int64), T = sum L; latch L_i < 0 (reading c20)
 //   1  g(i) for src and dst: GIVEN_COUNTS / CONTIG midpoint / LPT / EXPLICIT (reading c4)
 //   2  per layout: stable partition of sequences by group (ascending i inside a group, c5);
@@ -16,7 +17,15 @@
 //   4  stable partition of pieces by message key (src shard, dst shard); message token offsets
 //   5  per-(rank, shard) record / token bases, message byte offsets (16-B aligned field blocks)
 //   6  records: piece x sending replica ts < min(TP_src, TP_dst) (reading c9), in (s, ds, i, x)
+//
+// Grid-wide primitives: grid_scan (per-CTA reduce -> barrier -> per-CTA carry from the CTA
+// sums -> block scans with carry) and grid_partition (per-CTA key histograms -> barrier ->
+// per-(key, CTA) bases -> stable in-CTA ranks via __match_any_sync).
+#include <cooperative_groups.h>
+
 #include "earl_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace earl {
 
@@ -29,6 +38,14 @@ constexpr int kItems = 4;
 __device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
   if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
 }
+
+__device__ __forceinline__ void gsync() {
+  if (gridDim.x == 1) __syncthreads();
+  else cg::this_grid().sync();
+}
+
+__device__ __forceinline__ int64_t range_lo(int64_t n) { return n * blockIdx.x / gridDim.x; }
+__device__ __forceinline__ int64_t range_hi(int64_t n) { return n * (blockIdx.x + 1) / gridDim.x; }
 
 // BLOCK rule: q = L / sp, r = L % sp, chunk k = [k*q + min(k,r), (k+1)*q + min(k+1,r)).
 __device__ __forceinline__ int64_t chunk_lo(int64_t L, int sp, int k) {
@@ -68,29 +85,66 @@ __device__ int64_t block_excl_scan(int64_t v, int64_t& total, int64_t* sm) {
   return res;
 }
 
-// Exclusive scan over [0, n): put(i, sum_{j<i} get(j)); returns the total.
+// Exclusive scan over [lo, hi) starting from `carry`: put(i, carry + sum_{lo<=j<i} get(j)).
+// Returns the range's sum.
 template <class Get, class Put>
-__device__ int64_t tile_scan(int64_t n, Get get, Put put, int64_t* sm) {
-  int64_t carry = 0;
-  for (int64_t base = 0; base < n; base += (int64_t)NT * kItems) {
+__device__ int64_t tile_scan_range(int64_t lo, int64_t hi, int64_t carry, Get get, Put put,
+                                   int64_t* sm) {
+  int64_t sum = 0;
+  for (int64_t base = lo; base < hi; base += (int64_t)NT * kItems) {
     int64_t v[kItems];
     int64_t tsum = 0;
     const int64_t i0 = base + (int64_t)threadIdx.x * kItems;
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      v[it] = (i0 + it < n) ? get(i0 + it) : 0;
+      v[it] = (i0 + it < hi) ? get(i0 + it) : 0;
       tsum += v[it];
     }
     int64_t total;
-    int64_t run = carry + block_excl_scan(tsum, total, sm);
+    int64_t run = carry + sum + block_excl_scan(tsum, total, sm);
 #pragma unroll
     for (int it = 0; it < kItems; ++it) {
-      if (i0 + it < n) put(i0 + it, run);
+      if (i0 + it < hi) put(i0 + it, run);
       run += v[it];
     }
-    carry += total;
+    sum += total;
   }
-  return carry;
+  return sum;
+}
+
+// Grid-wide exclusive scan over [0, n).  `get` must be pure (it runs twice when G > 1) and
+// read only data published before the call; outputs of `put` are visible to other CTAs after
+// the caller's next gsync().  Returns the total (in every CTA).
+template <class Get, class Put>
+__device__ int64_t grid_scan(int64_t n, Get get, Put put, int64_t* cta_sums, int64_t* sm) {
+  const int64_t lo = range_lo(n), hi = range_hi(n);
+  if (gridDim.x == 1) return tile_scan_range(lo, hi, 0, get, put, sm);
+  int64_t part = 0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += NT) part += get(i);
+  int64_t total;
+  block_excl_scan(part, total, sm);
+  if (threadIdx.x == 0) cta_sums[blockIdx.x] = total;
+  gsync();
+  // carry = sum of the CTAs before this one; grand total (warp 0)
+  __shared__ int64_t s_carry, s_total;
+  if (threadIdx.x < 32) {
+    int64_t before = 0, all = 0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) {
+      const int64_t v = cta_sums[b];
+      all += v;
+      if (b < (int)blockIdx.x) before += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(kFull, before, o);
+      all += __shfl_xor_sync(kFull, all, o);
+    }
+    if (threadIdx.x == 0) { s_carry = before; s_total = all; }
+  }
+  __syncthreads();
+  const int64_t carry = s_carry, grand = s_total;
+  tile_scan_range(lo, hi, carry, get, put, sm);
+  return grand;
 }
 
 struct PartitionSmem {
@@ -98,28 +152,51 @@ struct PartitionSmem {
   int64_t running[kMaxKeys];
   int64_t tile_tot[kMaxKeys];
   int64_t bstart[kMaxKeys + 1];
+  int64_t before[kMaxKeys];
+  int64_t tot[kMaxKeys];
   unsigned hist[kMaxKeys];
 };
 
-// Stable counting sort of [0, n) by key(i) in [0, K), K <= 64: emit(i, sorted position).
-// On return ps.bstart[0..K] holds the bucket starts (bstart[K] = n).
+// Grid-wide stable counting sort of [0, n) by key(i) in [0, K), K <= 64: emit(i, position).
+// On return ps.bstart[0..K] holds the global bucket starts (same in every CTA).  Positions are
+// visible to other CTAs after the caller's next gsync().
 template <class KeyF, class Emit>
-__device__ void stable_partition(int64_t n, int K, KeyF key, Emit emit, PartitionSmem& ps) {
+__device__ void grid_partition(int64_t n, int K, KeyF key, Emit emit, int32_t* ghist,
+                               PartitionSmem& ps) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid < kMaxKeys) { ps.hist[tid] = 0; ps.running[tid] = 0; }
+  const int64_t lo = range_lo(n), hi = range_hi(n);
+  if (tid < kMaxKeys) ps.hist[tid] = 0;
   __syncthreads();
-  for (int64_t i = tid; i < n; i += NT) atomicAdd(&ps.hist[key(i)], 1u);
+  for (int64_t i = lo + tid; i < hi; i += NT) atomicAdd(&ps.hist[key(i)], 1u);
+  __syncthreads();
+  if (gridDim.x == 1) {
+    if (tid < K) { ps.tot[tid] = ps.hist[tid]; ps.before[tid] = 0; }
+  } else {
+    if (tid < K) ghist[(int64_t)blockIdx.x * kMaxKeys + tid] = (int32_t)ps.hist[tid];
+    gsync();
+    if (tid < K) {
+      int64_t before = 0, all = 0;
+      for (int b = 0; b < (int)gridDim.x; ++b) {
+        const int64_t v = ghist[(int64_t)b * kMaxKeys + tid];
+        all += v;
+        if (b < (int)blockIdx.x) before += v;
+      }
+      ps.tot[tid] = all;
+      ps.before[tid] = before;
+    }
+  }
   __syncthreads();
   if (tid == 0) {
     int64_t acc = 0;
-    for (int k = 0; k < K; ++k) { ps.bstart[k] = acc; acc += ps.hist[k]; }
+    for (int k = 0; k < K; ++k) { ps.bstart[k] = acc; acc += ps.tot[k]; }
     ps.bstart[K] = acc;
   }
+  if (tid < K) ps.running[tid] = ps.before[tid];
   __syncthreads();
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t base = 0; base < n; base += NT) {
+  for (int64_t base = lo; base < hi; base += NT) {
     const int64_t i = base + tid;
-    const int k = (i < n) ? key(i) : -1;
+    const int k = (i < hi) ? key(i) : -1;
     ps.whist[w][lane] = 0;
     ps.whist[w][lane + 32] = 0;
     __syncwarp();
@@ -161,13 +238,14 @@ __device__ __forceinline__ int for_each_piece(int64_t L, int sps, int spd, F f) 
   return cnt;
 }
 
+// LPT (one CTA; N <= 8192): bitonic sort of (INT32_MAX - L, i) keys in shared memory, then
+// Graham's greedy in one thread with the D <= 8 loads in registers.
 __device__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
   const int tid = threadIdx.x;
   const int64_t N = a.N;
   const int D = a.lay[l].dp;
   int64_t n2 = 1;
   while (n2 < N) n2 <<= 1;
-  // key: (L desc, i asc) == ascending (INT32_MAX - L, i)
   for (int64_t i = tid; i < n2; i += NT)
     keys[i] = (i < N) ? ((uint64_t)(0x7fffffffu - (uint32_t)a.lens[i]) << 32) | (uint64_t)i
                       : ~0ull;
@@ -185,8 +263,6 @@ __device__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
       __syncthreads();
     }
   }
-  // Graham's greedy: least-loaded group, ties to the lowest index.  One thread; the D <= 8
-  // loads live in registers and L is recovered from the sort key (no dependent global load).
   if (tid == 0) {
     int64_t ld[kMaxShards];
 #pragma unroll
@@ -209,36 +285,38 @@ __device__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
+__global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ PlanArgs a) {
   extern __shared__ uint64_t lpt_keys[];
   __shared__ int64_t sm_scan[NT / 32 + 1];
   __shared__ PartitionSmem ps;
   PlanHeader* h = a.hdr;
   const int tid = threadIdx.x;
+  const bool lead = blockIdx.x == 0;
   const int64_t N = a.N;
+  const int64_t gtid = (int64_t)blockIdx.x * NT + tid, gstride = (int64_t)gridDim.x * NT;
 
   // ---- phase 0: lengths, P, T -------------------------------------------------------
-  const int64_t T = tile_scan(
-      N,
-      [&](int64_t i) {
-        int32_t L = a.seq_lens[i];
-        if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
-        a.lens[i] = L;
-        return (int64_t)L;
-      },
-      [&](int64_t i, int64_t ex) { a.P[i] = ex; }, sm_scan);
-  if (tid == 0) { a.P[N] = T; h->T = T; }
-  __syncthreads();
+  for (int64_t i = gtid; i < N; i += gstride) {
+    int32_t L = a.seq_lens[i];
+    if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
+    a.lens[i] = L;
+  }
+  gsync();
+  const int64_t T = grid_scan(
+      N, [&](int64_t i) { return (int64_t)a.lens[i]; },
+      [&](int64_t i, int64_t ex) { a.P[i] = ex; }, a.cta_sums, sm_scan);
+  if (lead && tid == 0) { a.P[N] = T; h->T = T; }
+  gsync();
 
   // ---- phase 1: assignment -----------------------------------------------------------
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp;
     if (L.assign == EARL_ASSIGN_LPT) {
-      lpt_assign(a, l, lpt_keys);
+      if (lead) lpt_assign(a, l, lpt_keys);
       continue;
     }
-    for (int64_t i = tid; i < N; i += NT) {
+    for (int64_t i = gtid; i < N; i += gstride) {
       int g = 0;
       if (L.assign == EARL_ASSIGN_GIVEN_COUNTS) {
         while (g < D - 1 && i >= L.count_start[g + 1]) ++g;
@@ -257,54 +335,60 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
       a.grp[l][i] = g;
     }
   }
-  __syncthreads();
+  gsync();
 
   // ---- phase 2: per-layout group order and local token offsets ------------------------
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp, SP = L.sp;
-    int32_t* grp = a.grp[l];
+    const int32_t* grp = a.grp[l];
     int32_t* perm = a.perm[l];
-    stable_partition(
+    grid_partition(
         N, D, [&](int64_t i) { return grp[i]; },
-        [&](int64_t i, int64_t pos) { perm[pos] = (int32_t)i; }, ps);
-    if (tid <= D) h->group_start[l][tid] = ps.bstart[tid];
-    if (tid < D) h->group_count[l][tid] = ps.bstart[tid + 1] - ps.bstart[tid];
-    __syncthreads();
+        [&](int64_t i, int64_t pos) { perm[pos] = (int32_t)i; }, a.ghist, ps);
+    if (lead) {
+      if (tid <= D) h->group_start[l][tid] = ps.bstart[tid];
+      if (tid < D) h->group_count[l][tid] = ps.bstart[tid + 1] - ps.bstart[tid];
+    }
+    __shared__ int64_t s_gstart[kMaxShards + 1];
+    if (tid <= D) s_gstart[tid] = ps.bstart[tid];
+    gsync();
     for (int k = 0; k < SP; ++k) {
       int64_t* cum = a.cum[l] + (int64_t)k * (N + 1);
       int64_t* off = a.off[l] + (int64_t)k * N;
-      const int64_t tot = tile_scan(
+      const int64_t tot = grid_scan(
           N, [&](int64_t j) { return chunk_len(a.lens[perm[j]], SP, k); },
-          [&](int64_t j, int64_t ex) { cum[j] = ex; }, sm_scan);
-      if (tid == 0) cum[N] = tot;
-      __syncthreads();
-      for (int64_t j = tid; j < N; j += NT) {
+          [&](int64_t j, int64_t ex) { cum[j] = ex; }, a.cta_sums, sm_scan);
+      if (lead && tid == 0) cum[N] = tot;
+      gsync();
+      for (int64_t j = gtid; j < N; j += gstride) {
         const int i = perm[j];
-        off[i] = cum[j] - cum[h->group_start[l][grp[i]]];
+        off[i] = cum[j] - cum[s_gstart[grp[i]]];
       }
-      if (tid < D) {
-        const int64_t st = cum[h->group_start[l][tid + 1]] - cum[h->group_start[l][tid]];
+      if (lead && tid < D) {
+        const int64_t st = cum[s_gstart[tid + 1]] - cum[s_gstart[tid]];
         h->shard_tokens[l][tid * SP + k] = st;
         if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid * SP + k);
       }
-      __syncthreads();
+      // the next grid_scan / phase begins with a barrier-free read of lens/perm only; off and
+      // shard_tokens are consumed after later barriers
     }
+    gsync();
   }
 
   // ---- phase 3: pieces ----------------------------------------------------------------
   const LayoutDesc& S = a.lay[0];
   const LayoutDesc& Dl = a.lay[1];
   const int Sd = Dl.dp * Dl.sp;
-  const int64_t M = tile_scan(
+  const int64_t M = grid_scan(
       N,
       [&](int64_t i) {
         return (int64_t)for_each_piece(a.lens[i], S.sp, Dl.sp, [](int, int, int64_t, int64_t) {});
       },
-      [&](int64_t i, int64_t ex) { a.pbase[i] = ex; }, sm_scan);
-  if (tid == 0) { a.pbase[N] = M; h->n_pieces = M; }
-  __syncthreads();
-  for (int64_t i = tid; i < N; i += NT) {
+      [&](int64_t i, int64_t ex) { a.pbase[i] = ex; }, a.cta_sums, sm_scan);
+  if (lead && tid == 0) { a.pbase[N] = M; h->n_pieces = M; }
+  gsync();
+  for (int64_t i = gtid; i < N; i += gstride) {
     int64_t p = a.pbase[i];
     const int ss0 = a.grp[0][i] * S.sp, ds0 = a.grp[1][i] * Dl.sp;
     for_each_piece(a.lens[i], S.sp, Dl.sp, [&](int ks, int kd, int64_t x, int64_t y) {
@@ -315,11 +399,11 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
       ++p;
     });
   }
-  __syncthreads();
+  gsync();
 
   // ---- phase 4: pieces by message key, message token offsets -------------------------
   const int K = S.dp * S.sp * Sd;
-  stable_partition(
+  grid_partition(
       M, K, [&](int64_t q) { return a.pc_kk[q] >> 16; },
       [&](int64_t q, int64_t pos) {
         a.ps_i[pos] = a.pc_i[q];
@@ -327,22 +411,23 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
         a.ps_y[pos] = a.pc_y[q];
         a.ps_kk[pos] = a.pc_kk[q];
       },
-      ps);
-  if (tid <= K) h->key_piece_start[tid] = ps.bstart[tid];
-  if (tid < K) h->key_pieces[tid] = ps.bstart[tid + 1] - ps.bstart[tid];
-  __syncthreads();
-  const int64_t Mtok = tile_scan(
+      a.ghist, ps);
+  if (lead) {
+    if (tid <= K) h->key_piece_start[tid] = ps.bstart[tid];
+    if (tid < K) h->key_pieces[tid] = ps.bstart[tid + 1] - ps.bstart[tid];
+  }
+  gsync();
+  const int64_t Mtok = grid_scan(
       M, [&](int64_t q) { return (int64_t)(a.ps_y[q] - a.ps_x[q]); },
-      [&](int64_t q, int64_t ex) { a.ps_scan[q] = ex; }, sm_scan);
-  if (tid == 0) a.ps_scan[M] = Mtok;
-  __syncthreads();
-  if (tid < K)
-    h->key_tokens[tid] = a.ps_scan[h->key_piece_start[tid + 1]] - a.ps_scan[h->key_piece_start[tid]];
-  __syncthreads();
+      [&](int64_t q, int64_t ex) { a.ps_scan[q] = ex; }, a.cta_sums, sm_scan);
+  if (lead && tid == 0) a.ps_scan[M] = Mtok;
+  gsync();
 
   // ---- phase 5: bases and message offsets (one thread; <= 8 x 8 entries) --------------
   const int nts = S.tp < Dl.tp ? S.tp : Dl.tp;
-  if (tid == 0) {
+  if (lead && tid == 0) {
+    for (int key = 0; key < K; ++key)
+      h->key_tokens[key] = a.ps_scan[h->key_piece_start[key + 1]] - a.ps_scan[h->key_piece_start[key]];
     int64_t rec = 0, tok = 0;
     for (int r = 0; r < a.world; ++r) {
       h->rec_begin[r] = rec;
@@ -374,11 +459,11 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
     }
     a.rec.tok_prefix[rec] = tok;
   }
-  __syncthreads();
+  gsync();
 
   // ---- phase 6: records ---------------------------------------------------------------
   const int64_t nrec = M * nts;
-  for (int64_t idx = tid; idx < nrec; idx += NT) {
+  for (int64_t idx = gtid; idx < nrec; idx += gstride) {
     const int64_t q = idx / nts;
     const int ts = (int)(idx - q * nts);
     const int kk = a.ps_kk[q];
@@ -403,8 +488,8 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const PlanArgs a) {
 }
 
 // Destination metadata of dst shard (g, k): cu_seqlens (int32), seq_ids (int64), tok_start.
-__global__ void local_meta_kernel(const PlanArgs a, int g, int k, int32_t* cu, int64_t* ids,
-                                  int32_t* tok_start) {
+__global__ void local_meta_kernel(const __grid_constant__ PlanArgs a, int g, int k, int32_t* cu,
+                                  int64_t* ids, int32_t* tok_start) {
   const PlanHeader* h = a.hdr;
   const int64_t N = a.N;
   const int64_t n = h->group_count[1][g];
@@ -424,14 +509,37 @@ __global__ void local_meta_kernel(const PlanArgs a, int g, int k, int32_t* cu, i
 
 }  // namespace
 
-cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, cudaStream_t s) {
-  if (lpt_smem > 0) {
-    cudaError_t e = cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)lpt_smem);
-    if (e != cudaSuccess) return e;
+int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, planner_kernel, NT, 64 * 1024);
+    if (per_sm < 1) per_sm = 1;
   }
-  planner_kernel<<<1, NT, lpt_smem, s>>>(a);
-  return cudaGetLastError();
+  const int64_t work = n_seqs > max_pieces ? n_seqs : max_pieces;
+  int64_t g = (work + 4095) / 4096;
+  const int64_t cap = (int64_t)sm_count * per_sm;
+  if (g > cap) g = cap;
+  if (g > kMaxPlanGrid) g = kMaxPlanGrid;
+  if (g < 1) g = 1;
+  (void)lpt_smem;
+  return (int)g;
+}
+
+cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         64 * 1024);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  if (grid == 1) {
+    planner_kernel<<<1, NT, lpt_smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  void* args[] = {const_cast<PlanArgs*>(&a)};
+  return cudaLaunchCooperativeKernel((const void*)planner_kernel, dim3(grid), dim3(NT), args,
+                                     lpt_smem, s);
 }
 
 cudaError_t launch_local_meta(const PlanArgs& a, int g, int k, int32_t* cu, int64_t* ids,

@@ -202,3 +202,41 @@ def test_lpt_capacity_and_misaligned_buffers():
     with pytest.raises(EarlError) as e:
         p.exec([buf[4:], None], [buf[16:], buf[32:]])
     assert e.value.name == "EARL_ERR_INVALID_ARGUMENT"
+
+
+@pytest.mark.parametrize("n,dst", [
+    (60000, dict(dp=2, sp=2, tp=2, assign="contig")),
+    (100000, dict(dp=8, assign="explicit", group_of_seq=None)),
+    (45000, dict(rank0=1, dp=3, sp=2, assign="given_counts")),
+])
+def test_large_n_cooperative_planner(n, dst):
+    """N large enough for a multi-CTA cooperative planner grid (G = ceil(N/4096) > 1): plan,
+    bytes and metadata equal the oracle's."""
+    rng = np.random.default_rng(n)
+    lens = rng.integers(0, 48, size=n).tolist()
+    dst = dict(dst)
+    if dst["assign"] == "explicit":
+        dst["group_of_seq"] = rng.integers(0, dst["dp"], size=n).astype(np.int32)
+    if dst["assign"] == "given_counts":
+        dst["counts"] = W.near_equal_counts(n, dst["dp"])
+    run_gpu_case(W.rollout_layout(n, 8), W.layout(**dst), lens, [("m", 1, 1, "x"), ("a", 4, 1, "x")],
+                 8, seed=9)
+
+
+def test_plan_outlives_comm_handle():
+    """Plans hold a reference on their comm: destroying the comm handle first (as a garbage
+    collector may) leaves the plan usable and the device error state clean."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    ed = EmulatedDispatch(2)
+    f = [("a", 4, 1, "x")]
+    p = ed.plan(W.layout(dp=1), W.layout(dp=2), [4, 4], f)
+    recv = ed.alloc_recv(p, f)
+    ed.comm.destroy()
+    src = torch.arange(8, dtype=torch.int32, device="cuda").view(torch.uint8)
+    p.exec([src, None], ed.flat(recv))
+    torch.cuda.synchronize()
+    p.sync()
+    assert recv[0][0].view(torch.int32).tolist() == [0, 1, 2, 3]
+    assert recv[1][0].view(torch.int32).tolist() == [4, 5, 6, 7]
+    p.destroy()
