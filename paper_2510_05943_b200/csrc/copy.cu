@@ -1,17 +1,18 @@
 // copy.cu -- the byte-moving kernels of the dispatcher (SURVEY.md §8(a) a3 pack, a5 unpack,
 // a6 fused direct/P2P, a7 completion).
 //
-// All three modes run the same persistent kernel over the plan's copy records.  The work of a
-// launch is the field-major byte space  sum_f Ntok * B_f  (Ntok = tokens of the records in
-// the launch's view); every warp takes one contiguous, equal slice of it, so a 32K-token
-// sequence next to hundreds of 100-token ones is split by bytes, not by sequence.  A warp
-// finds its first record by binary search over the records' token prefix and then walks
-// records in order.  Each (record, field) piece is copied by warp_copy: 16-B vector stores on
-// the destination, 16-B vector loads on the source realigned in registers (warp shuffle +
-// funnel shift) when source and destination differ mod 16 -- the 4-B id/fp32 fields and 1-B
-// masks start at arbitrary token offsets.  Replicated destinations (TP, reading c2) are
-// written from the same registers: each source byte is read once.  No tensor cores: the path
-// is pure data movement (HBM roofline).
+// All three modes run the same persistent kernel (one CTA per SM, 8 warps) over the plan's
+// copy records.  The work of a launch is a record-major cost space (bytes + a fixed cost per
+// (record, field) piece); warps take units of it -- first a static one, then further units
+// from a plan-owned atomic counter -- so a 32K-token sequence next to hundreds of 100-token
+// ones is split by cost, not by sequence, and stragglers are absorbed.  Bytes move through a
+// per-warp TMA ring (cp.async.bulk global->shared, mbarrier complete_tx) and leave either by
+// cp.async.bulk shared->global (source and destination congruent mod 16, local destination)
+// or by 16-B warp stores (realigned in registers with funnel shifts when they are not
+// congruent -- the 4-B id/fp32 fields and 1-B masks start at arbitrary token offsets -- and for
+// destinations on a peer GPU).  Replicated destinations (TP, reading c2) are written from the
+// same shared-memory stage: each source byte is read once.  No tensor cores: the path is pure
+// data movement (HBM roofline).
 #include "earl_internal.cuh"
 
 namespace earl {
@@ -371,9 +372,27 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, const SubDesc& S,
   if (nvec > 0) {
     const uint32_t smo = S.so + S.off + head;
     if ((smo & 15) == 0) {
+      // local replicas: one bulk TMA store each; replicas on a peer GPU (multi-process comm)
+      // are written by the warp with 16-B stores over NVLink
+      bool remote[R];
+      bool any_remote = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        remote[r] = a.mode != kPack && a.me >= 0 && (S.d0 + r * a.tp_s) != a.me;
+        any_remote |= remote[r];
+      }
       if (lane == 0) {
 #pragma unroll
-        for (int r = 0; r < R; ++r) tma_store(dp[r] + head, stage + smo, nvec * 16);
+        for (int r = 0; r < R; ++r)
+          if (!remote[r]) tma_store(dp[r] + head, stage + smo, nvec * 16);
+      }
+      if (any_remote) {
+        for (uint32_t k = lane; k < nvec; k += 32) {
+          const uint4 v = *reinterpret_cast<const uint4*>(stage + smo + 16 * k);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (remote[r]) st_v4(dp[r] + head + 16 * k, v);
+        }
       }
     } else {
       const uint32_t sh = smo & 15;
