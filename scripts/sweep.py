@@ -1,0 +1,132 @@
+"""C5 bandwidth sweep (BASELINE.json configs[4]) on one B200, 8-rank emulation.
+
+For payload P per rank in 1 MiB .. 4 GiB, uniform (L = 4096) and long-tail (C2 distribution)
+lengths, scalar6-fp32 fields (series A) and +hidden2560 (series B, P >= 64 MiB):
+  * a2a  : earl_dispatch_plan + earl_dispatch_exec, DP8 -> DP8 EXPLICIT round-robin
+           (uniform all-to-allv), i.e. the decentralized dispatch;
+  * cent : the centralized gather-and-dispatch baseline (reading c13): DP8 ->
+           DP1 on rank 0, then DP1 -> DP8, two plans + two execs.
+Times are CUDA-event medians with an L2 flush before every timed repetition.  Beside the
+measured (HBM-bound, one GPU) times it reports the NVLink model of SURVEY.md §8(d):
+t_a2a = max_r max(egress_r, ingress_r) / 770 GB/s, t_cent = (ingress_0 + egress_0) / 770 GB/s
+(the controller's link serialises both phases).  Writes profiles/<tag>_sweep.json.
+"""
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2510_05943_b200 import workloads as W  # noqa: E402
+from paper_2510_05943_b200.dispatch import EmulatedDispatch  # noqa: E402
+
+NVL = 770e9
+HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
+    if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6.65e12
+R = 8
+MiB = 1 << 20
+
+
+def lengths(kind, n):
+    if kind == "uniform":
+        return np.full(n, 4096, dtype=np.int64)
+    return W.lognormal_lengths(n, 2048, 0.75, 64, 8192, 0)
+
+
+def n_for(kind, fields, per_rank):
+    B = W.bytes_per_token(fields)
+    mean = 4096 if kind == "uniform" else float(W.lognormal_lengths(100000, 2048, 0.75, 64, 8192, 0).mean())
+    return max(R, int(round(per_rank * R / (B * mean))))
+
+
+def timed(fn, reps, flush):
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(512 * MiB, dtype=torch.uint8, device=dev)
+    ed = EmulatedDispatch(R)
+    rows = []
+    for series, fname in (("A", "scalar6-fp32"), ("B", "scalar6-fp32+hidden2560")):
+        fields = W.field_set(fname)
+        F = len(fields)
+        for kind in ("uniform", "longtail"):
+            for p_mib in (1, 4, 16, 64, 256, 1024, 4096):
+                if series == "B" and p_mib < 64:
+                    continue
+                n = n_for(kind, fields, p_mib * MiB)
+                lens = lengths(kind, n)
+                src = W.rollout_layout(n, R)
+                dst = W.layout(dp=R, assign="explicit", group_of_seq=np.arange(n, dtype=np.int32) % R)
+                mid = W.layout(dp=1, assign="given_counts", counts=[n])
+                tok = W.rollout_token_counts(lens, src["counts"])
+                send = [W.gen_field_device(fields[f], tok[r], 1000 + 16 * r + f, dev)
+                        for r in range(R) for f in range(F)]
+                lens_dev = torch.as_tensor(lens.astype(np.int32)).to(dev)
+                p_a = ed.plan(src, dst, lens_dev, fields)
+                p_1 = ed.plan(src, mid, lens_dev, fields)
+                p_2 = ed.plan(mid, dst, lens_dev, fields)
+                st_a, st_1, st_2 = p_a.stats(), p_1.stats(), p_2.stats()
+                recv = ed.flat(ed.alloc_recv(p_a, fields))
+                midb = ed.flat(ed.alloc_recv(p_1, fields))
+                recv2 = ed.flat(ed.alloc_recv(p_2, fields))
+
+                def a2a():
+                    q = ed.plan(src, dst, lens_dev, fields)
+                    q.exec(send, recv)
+                    q.destroy()
+
+                def cent():
+                    q1 = ed.plan(src, mid, lens_dev, fields)
+                    q1.exec(send, midb)
+                    q2 = ed.plan(mid, dst, lens_dev, fields)
+                    q2.exec(midb, recv2)
+                    q1.destroy()
+                    q2.destroy()
+
+                for _ in range(2):
+                    a2a(); cent()
+                torch.cuda.synchronize()
+                reps = 10 if p_mib <= 1024 else 4
+                t_a = timed(a2a, reps, flush)
+                t_c = timed(cent, reps, flush)
+                payload = st_a["total_tokens"] * st_a["bytes_per_token"]
+                hbm_a = sum(st_a["read_bytes"]) + st_a["total"]
+                nvl_a = max(max(st_a["egress"]), max(st_a["ingress"])) / NVL * 1e3
+                nvl_c = (st_1["ingress"][0] + st_2["egress"][0]) / NVL * 1e3
+                row = {"series": series, "fields": fname, "lengths": kind, "per_rank_MiB": p_mib,
+                       "n_seqs": int(n), "payload_bytes": int(payload),
+                       "a2a_ms": t_a, "cent_ms": t_c, "measured_ratio": t_c / t_a,
+                       "a2a_GBps": payload / t_a / 1e6, "a2a_hbm_frac": hbm_a / (t_a * 1e-3) / HBM,
+                       "nvlink_model_a2a_ms": nvl_a, "nvlink_model_cent_ms": nvl_c,
+                       "nvlink_model_ratio": nvl_c / nvl_a if nvl_a else None,
+                       "moved_a2a": st_a["moved"], "moved_cent": st_1["moved"] + st_2["moved"]}
+                rows.append(row)
+                print(json.dumps(row), flush=True)
+                for q in (p_a, p_1, p_2):
+                    q.destroy()
+                del send, recv, midb, recv2
+                torch.cuda.empty_cache()
+    out = os.path.join(ROOT, "gpurun_out", f"{tag}_sweep.json")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump({"about": __doc__, "hbm_peak_Bps": HBM, "nvlink_Bps": NVL, "rows": rows}, open(out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
