@@ -208,10 +208,25 @@ EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* s
  * ([1] or emulated [world]; size earl_plan_stats().stage_bytes[rank]). */
 EARL_API earl_status_t earl_dispatch_pack(earl_plan_t plan, const void* const* send_bufs,
                                  void* const* stage_bufs, void* stream);
-/* Staged path, step a5 (emulated comm): scatter every packed message into every
- * destination replica's final field arrays (read once, written once per replica). */
+/* Staged path, step a5: scatter packed messages into the final field arrays.
+ * Emulated comm: stage_bufs [world] are the senders' stage buffers (as packed) and every
+ *   destination replica's arrays are written (each message byte read once, written once per
+ *   replica); recv_bufs is [world][n_fields].
+ * Multi-process comm: stage_bufs[0] is this rank's receive buffer holding the messages it
+ *   received, concatenated in source-rank order at the offsets earl_plan_messages reports;
+ *   recv_bufs [n_fields] are this rank's field arrays. */
 EARL_API earl_status_t earl_dispatch_unpack(earl_plan_t plan, const void* const* stage_bufs,
                                    void* const* recv_bufs, void* stream);
+
+/* Staged path, step a4 bookkeeping for a multi-process exchange (e.g. grouped NCCL
+ * send/recv): for rank `rank`, the byte range of its stage buffer to send to each peer d
+ * (send_off[d], send_bytes[d]; message to d's shard, sent to every replica fed by this rank)
+ * and where each source s's message lands in its receive buffer (recv_off[s], recv_bytes[s];
+ * concatenated in source-rank order).  All arrays are HOST [world]; synchronises on the plan.
+ * A rank's message to itself appears in both tables (copy it locally). */
+EARL_API earl_status_t earl_plan_messages(earl_plan_t plan, int32_t rank, int64_t* send_off,
+                                          int64_t* send_bytes, int64_t* recv_off,
+                                          int64_t* recv_bytes);
 
 /* ---- misc -------------------------------------------------------------------------- */
 EARL_API const char* earl_status_string(earl_status_t status);

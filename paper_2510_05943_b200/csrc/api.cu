@@ -657,6 +657,8 @@ earl_status_t fill_copy_args(earl_plan_t p, CopyArgs& a, int mode) {
   a.nts = S.tp < D.tp ? S.tp : D.tp;
   a.rank0_s = S.rank0; a.tp_s = S.tp;
   a.rank0_d = D.rank0; a.tp_d = D.tp; a.sp_d = D.sp; a.n_dst_shards = D.dp * D.sp;
+  a.n_src_shards = S.dp * S.sp;
+  a.protocol = 0;
   a.Bpre[0] = 0;
   for (int f = 0; f < p->n_fields; ++f) {
     a.Bf[f] = p->args.Bf[f];
@@ -775,6 +777,7 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
       for (int f = 0; f < F; ++f) a.dst[0][f] = static_cast<uint8_t*>(recv_bufs[f]);
   }
   if (!c->emulated && c->world > 1) {
+    a.protocol = 1;
     c->epoch += 1;
     a.epoch = c->epoch;
     a.my_pad = reinterpret_cast<uint64_t*>(c->win[c->rank]);
@@ -810,7 +813,6 @@ extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* se
       return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", rr);
     a.stage[rr] = static_cast<uint8_t*>(stage_bufs[r]);
   }
-  a.world = 1;  // no completion protocol: pack is rank-local
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
@@ -821,26 +823,85 @@ extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* 
                                               void* const* recv_bufs, void* stream) {
   if (!p || !stage_bufs || !recv_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   earl_comm* c = p->comm;
-  if (!c->emulated)
-    return fail(EARL_ERR_UNSUPPORTED, "unpack of received messages needs an emulated comm");
   DeviceGuard g(c->device);
   CopyArgs a;
   fill_copy_args(p, a, kUnpack);
   const int F = p->n_fields;
-  for (int r = 0; r < c->world; ++r) {
-    if (stage_bufs[r] && !aligned16(stage_bufs[r]))
-      return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", r);
-    a.stage[r] = const_cast<uint8_t*>(static_cast<const uint8_t*>(stage_bufs[r]));
+  if (c->emulated) {
+    for (int r = 0; r < c->world; ++r) {
+      if (stage_bufs[r] && !aligned16(stage_bufs[r]))
+        return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", r);
+      a.stage[r] = const_cast<uint8_t*>(static_cast<const uint8_t*>(stage_bufs[r]));
+      for (int f = 0; f < F; ++f) {
+        void* ptr = recv_bufs[r * F + f];
+        if (ptr && !aligned16(ptr))
+          return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer rank %d field %d not 16-B aligned", r, f);
+        a.dst[r][f] = static_cast<uint8_t*>(ptr);
+      }
+    }
+  } else {
+    // a real rank: stage_bufs[0] holds the messages it received, concatenated in source-rank
+    // order (earl_plan_messages gives each one's offset); recv_bufs[F] are its field arrays
+    if (stage_bufs[0] && !aligned16(stage_bufs[0]))
+      return fail(EARL_ERR_INVALID_ARGUMENT, "receive stage buffer not 16-B aligned");
+    a.recv_stage = static_cast<const uint8_t*>(stage_bufs[0]);
     for (int f = 0; f < F; ++f) {
-      void* ptr = recv_bufs[r * F + f];
+      void* ptr = recv_bufs[f];
       if (ptr && !aligned16(ptr))
-        return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer rank %d field %d not 16-B aligned", r, f);
-      a.dst[r][f] = static_cast<uint8_t*>(ptr);
+        return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer field %d not 16-B aligned", f);
+      a.dst[c->rank][f] = static_cast<uint8_t*>(ptr);
     }
   }
-  a.world = 1;
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "unpack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_messages(earl_plan_t p, int32_t rank, int64_t* send_off,
+                                            int64_t* send_bytes, int64_t* recv_off,
+                                            int64_t* recv_bytes) {
+  if (!p || !send_off || !send_bytes || !recv_off || !recv_bytes)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  const int W = p->comm->world;
+  if (rank < 0 || rank >= W) return fail(EARL_ERR_INVALID_ARGUMENT, "rank %d outside the comm", rank);
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  const PlanHeader& h = p->host_hdr;
+  const earl_layout_t& S = p->lay[0];
+  const earl_layout_t& D = p->lay[1];
+  const int Sd = D.dp * D.sp;
+  const int nts = S.tp < D.tp ? S.tp : D.tp;
+  auto msg_bytes = [&](int key) {
+    int64_t b = 0;
+    for (int f = 0; f < p->n_fields; ++f) b += ((int64_t)h.key_tokens[key] * p->args.Bf[f] + 15) & ~15LL;
+    return b;
+  };
+  for (int q = 0; q < W; ++q) { send_off[q] = send_bytes[q] = recv_off[q] = recv_bytes[q] = 0; }
+  int g, k, t;
+  // sends: this rank's message to dst shard ds goes to every replica td == ts (mod tp_src)
+  if (coords(S, rank, &g, &k, &t) && t < nts) {
+    const int ss = g * S.sp + k;
+    for (int d = 0; d < W; ++d) {
+      int gd, kd, td;
+      if (!coords(D, d, &gd, &kd, &td) || td % S.tp != t) continue;
+      const int ds = gd * D.sp + kd;
+      send_off[d] = h.msg_off[ss * Sd + ds];
+      send_bytes[d] = msg_bytes(ss * Sd + ds);
+    }
+  }
+  // receives: concatenated in source-rank order
+  if (coords(D, rank, &g, &k, &t)) {
+    const int ds = g * D.sp + k;
+    int64_t off = 0;
+    for (int s = 0; s < W; ++s) {
+      int gs, ks, ts;
+      if (!coords(S, s, &gs, &ks, &ts) || ts >= nts || t % S.tp != ts) continue;
+      const int key = (gs * S.sp + ks) * Sd + ds;
+      recv_off[s] = off;
+      recv_bytes[s] = msg_bytes(key);
+      off += recv_bytes[s];
+    }
+  }
   return EARL_OK;
 }

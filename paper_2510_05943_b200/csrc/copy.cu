@@ -172,10 +172,68 @@ __device__ __forceinline__ void fence_mbar_init() {
 // fixed cost of a piece).  Equal-byte slices made the warps holding thousands of small scalar
 // pieces the stragglers (profiles/r01_trace.txt); the c0 term balances them.  Record-major
 // order loads a record's metadata once for all of its fields.
+// The records a launch moves, as up to 8 contiguous blocks of the (s, ds, i, x)-ordered record
+// table: everything (emulated comm), this rank's own records (fused exec / pack), or, for the
+// unpack of a real rank, one block per source rank that sends to it -- each with the start of
+// that source's message in this rank's receive buffer (messages concatenated in rank order).
+struct View {
+  int n;
+  int64_t rbeg[kMaxWorld], rend[kMaxWorld], tbeg[kMaxWorld];
+  uint64_t cbase[kMaxWorld + 1];
+  const uint8_t* msg[kMaxWorld];
+};
+
+__device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
+  const PlanHeader* h = a.hdr;
+  const int F = a.n_fields;
+  const uint64_t B = a.Bpre[F];
+  v.n = 0;
+  v.cbase[0] = 0;
+  auto add = [&](int64_t rb, int64_t re, const uint8_t* msg) {
+    if (re <= rb) return;
+    const int64_t t0 = a.rec.tok_prefix[rb], t1 = a.rec.tok_prefix[re];
+    v.rbeg[v.n] = rb; v.rend[v.n] = re; v.tbeg[v.n] = t0; v.msg[v.n] = msg;
+    v.cbase[v.n + 1] = v.cbase[v.n] + (uint64_t)(t1 - t0) * B + (uint64_t)(re - rb) * F * c0;
+    ++v.n;
+  };
+  if (a.view_rank < 0) {
+    add(0, h->n_records, nullptr);
+  } else if (a.mode != kUnpack) {
+    add(h->rec_begin[a.view_rank], h->rec_begin[a.view_rank + 1], nullptr);
+  } else {
+    const int Sd = a.n_dst_shards;
+    const int rr = a.me - a.rank0_d;
+    if (rr < 0 || rr >= Sd * a.tp_d) return;
+    const int td = rr % a.tp_d, ds = rr / a.tp_d;
+    const uint8_t* m = a.recv_stage;
+    for (int s = 0; s < a.world; ++s) {
+      const int q = s - a.rank0_s;
+      if (q < 0 || q >= a.n_src_shards * a.tp_s) continue;
+      const int ts = q % a.tp_s, ss = q / a.tp_s;
+      if (ts >= a.nts || td % a.tp_s != ts) continue;
+      const int key = ss * Sd + ds;
+      const int64_t rb = h->rec_base[s][ds];
+      const int64_t re = (ds + 1 < Sd) ? h->rec_base[s][ds + 1] : h->rec_begin[s + 1];
+      add(rb, re, m);
+      for (int f = 0; f < F; ++f) m += (h->key_tokens[key] * a.Bf[f] + 15) & ~15LL;
+    }
+  }
+}
+
+// Lane-0-only walker over a warp's share of the launch's work.
+//
+// Work is measured in a record-major cost space: record j (all fields) of view block b
+// occupies [cost(j), cost(j+1)) with cost(j) = cbase[b] + (tok_prefix[j] - tbeg[b]) * B +
+// (j - rbeg[b]) * F * c0, and field f of record j is the sub-interval starting at
+// n_j * Bpre[f] + f * c0 whose first n_j * B_f cost units map 1:1 to its bytes, followed by c0
+// units that map to no bytes (the fixed cost of a piece).  Equal-byte slices made the warps
+// holding thousands of small scalar pieces the stragglers; the c0 term balances them.
+// Record-major order loads a record's metadata once for all of its fields.
 struct Walker {
   const CopyArgs* a;
   const PlanHeader* h;
-  int64_t rbeg, rend, tbeg;
+  View v;
+  int b;  // current view block
   uint64_t c0, x1, xpos, unit, n_units, first_dyn;
   unsigned int* work_ctr;
   int F;
@@ -192,16 +250,18 @@ struct Walker {
   uint64_t prem;
   int pf, pd0;
 
-  __device__ uint64_t cost(int64_t jj) const {
-    return (uint64_t)(a->rec.tok_prefix[jj] - tbeg) * a->Bpre[F] + (uint64_t)(jj - rbeg) * F * c0;
+  __device__ uint64_t cost(int bb, int64_t jj) const {
+    return v.cbase[bb] + (uint64_t)(a->rec.tok_prefix[jj] - v.tbeg[bb]) * a->Bpre[F] +
+           (uint64_t)(jj - v.rbeg[bb]) * F * c0;
   }
-  __device__ uint64_t total() const { return cost(rend); }
+  __device__ uint64_t total() const { return v.cbase[v.n]; }
 
-  __device__ void setup(const CopyArgs* a_, int64_t rbeg_, int64_t rend_, int64_t tbeg_,
-                        uint64_t c0_, uint64_t unit_, uint64_t n_units_, uint64_t first_dyn_) {
-    a = a_; h = a_->hdr; rbeg = rbeg_; rend = rend_; tbeg = tbeg_; c0 = c0_; unit = unit_;
-    n_units = n_units_; first_dyn = first_dyn_; work_ctr = a_->work_ctr; F = a_->n_fields;
-    prem = 0; R = 0; xpos = x1 = 0; j = rbeg; f = 0;
+  __device__ void setup(const CopyArgs* a_, uint64_t c0_, uint64_t first_dyn_) {
+    a = a_; h = a_->hdr; c0 = c0_; unit = 0; n_units = 0; first_dyn = first_dyn_;
+    work_ctr = a_->work_ctr; F = a_->n_fields;
+    prem = 0; R = 0; xpos = x1 = 0; f = 0; b = 0;
+    build_view(*a_, c0_, v);
+    j = v.n ? v.rbeg[0] : 0;
   }
 
   __device__ void load_record(int64_t jj) {
@@ -211,7 +271,7 @@ struct Walker {
     src_tok = a->rec.src_tok[jj];
     dst_tok = a->rec.dst_tok[jj];
     n = (uint64_t)(t1 - t0);
-    cj = (uint64_t)(t0 - tbeg) * a->Bpre[F] + (uint64_t)(jj - rbeg) * F * c0;
+    cj = v.cbase[b] + (uint64_t)(t0 - v.tbeg[b]) * a->Bpre[F] + (uint64_t)(jj - v.rbeg[b]) * F * c0;
     s = code & 0xff;
     const int ss = (code >> 8) & 0xff;
     ds = (code >> 16) & 0xff;
@@ -248,16 +308,19 @@ struct Walker {
     xpos = x0;
     prem = 0;
     if (xpos >= x1) return;
-    int64_t lo = rbeg, hi = rend - 1;  // last record whose cost interval starts <= xpos
+    b = 0;
+    while (b + 1 < v.n && v.cbase[b + 1] <= xpos) ++b;
+    int64_t lo = v.rbeg[b], hi = v.rend[b] - 1;  // last record whose cost starts <= xpos
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
-      if (cost(mid) <= xpos) lo = mid; else hi = mid - 1;
+      if (cost(b, mid) <= xpos) lo = mid; else hi = mid - 1;
     }
     load_record(lo);
     while (f + 1 < F && cj + fo + n * a->Bf[f] + c0 <= xpos) next_field();
   }
 
   __device__ bool next_piece() {
+    const bool unpack_rank = a->mode == kUnpack && a->view_rank >= 0;
     while (xpos < x1) {
       const uint64_t Bf = a->Bf[f];
       const uint64_t nb = n * Bf;
@@ -270,11 +333,21 @@ struct Walker {
       if (u1 > u0) {
         int64_t msg_field = 0;
         if (a->mode != kDirect) msg_field = msg_base + fb + msg_tok * (int64_t)Bf + (int64_t)u0;
-        psrc = (a->mode == kUnpack) ? a->stage[s] + msg_field
-                                    : a->src[s][f] + src_tok * (int64_t)Bf + (int64_t)u0;
+        if (a->mode == kUnpack) {
+          psrc = unpack_rank ? v.msg[b] + fb + msg_tok * (int64_t)Bf + (int64_t)u0
+                             : a->stage[s] + msg_field;
+        } else {
+          psrc = a->src[s][f] + src_tok * (int64_t)Bf + (int64_t)u0;
+        }
         if (a->mode == kPack) {
           pdst = a->stage[s] + msg_field;
           R = 1;
+          pd0 = d0;
+        } else if (unpack_rank) {
+          uint8_t* base = a->dst[a->me][f];
+          pdst = base + dst_tok * (int64_t)Bf + (int64_t)u0;
+          R = base != nullptr ? 1 : 0;
+          pd0 = a->me;
         } else {
           R = 0;
           uint8_t* base0 = a->dst[d0][f];
@@ -282,18 +355,21 @@ struct Walker {
             if (a->dst[d0 + (td - ts)][f] != nullptr) ++R;
           pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
           if (base0 == nullptr) R = 0;
+          pd0 = d0;
         }
         prem = u1 - u0;
         pf = f;
-        pd0 = d0;
         found = R > 0;
       }
       if (x1 >= fend) {
         xpos = fend;
         if (f + 1 < F) {
           next_field();
-        } else if (j + 1 < rend) {
+        } else if (j + 1 < v.rend[b]) {
           load_record(j + 1);
+        } else if (b + 1 < v.n) {
+          ++b;
+          load_record(v.rbeg[b]);
         } else {
           xpos = x1;
         }
@@ -455,13 +531,6 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
   __syncwarp();
   const PlanHeader* h = a.hdr;
   if (h->err == 0) {
-    int64_t rbeg, rend, tbeg;
-    if (a.view_rank < 0) {
-      rbeg = 0; rend = h->n_records; tbeg = 0;
-    } else {
-      rbeg = h->rec_begin[a.view_rank]; rend = h->rec_begin[a.view_rank + 1];
-      tbeg = h->rec_tok_begin[a.view_rank];
-    }
     const uint64_t c0 = CHUNK / 4;
     const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
     const uint64_t wid = (uint64_t)blockIdx.x * WARPS + w;
@@ -470,8 +539,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     int nprod = 0;
     if (lane == 0) {
       if (a.trace) t_start = globaltimer();
-      wk.setup(&a, rbeg, rend, tbeg, c0, 0, 0, nwarps);
-      const uint64_t total = rend > rbeg ? wk.total() : 0;
+      wk.setup(&a, c0, nwarps);
+      const uint64_t total = wk.total();
       // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
       uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
       if (unit < 4 * (uint64_t)CHUNK) unit = 4 * (uint64_t)CHUNK;
@@ -521,7 +590,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     }
   }
   // completion (multi-process comm): last CTA releases this epoch to every peer and waits
-  if (a.world > 1 && a.view_rank >= 0) {
+  if (a.protocol) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __threadfence_system();
     __syncthreads();

@@ -100,7 +100,9 @@ struct CopyArgs {
   int32_t n_fields;
   int32_t view_rank;       // -1: every record (emulated); else records of source rank view_rank
   int32_t nts;             // min(tp_src, tp_dst)
-  int32_t rank0_s, tp_s, rank0_d, tp_d, sp_d, n_dst_shards;
+  int32_t rank0_s, tp_s, rank0_d, tp_d, sp_d, n_dst_shards, n_src_shards;
+  int32_t protocol;        // 1: multi-process fused exec (epoch release / acquire at the end)
+  const uint8_t* recv_stage;                  // unpack on a real rank: received messages
   uint32_t Bf[kMaxFields];
   uint64_t Bpre[kMaxFields + 1];  // prefix of Bf
   const PlanHeader* hdr;

@@ -164,3 +164,52 @@ class Dispatcher:
             views.append(window_tensor(ptr, max(16, n_max * b), self.device)[: mine * b])
         # exec takes the raw window pointers (valid even when this rank receives 0 bytes)
         return full, views
+
+    # -- staged path (pack -> grouped send/recv -> unpack): the exchange comparator ----------
+
+    def alloc_stage(self, plan):
+        """Send stage (this rank's packed messages) and receive stage (the messages it gets,
+        concatenated in source-rank order), plus the per-peer byte table of earl_plan_messages."""
+        st = plan.stats()
+        msgs = plan.messages(self.rank)
+        send_stage = torch.empty(max(16, int(st["stage_bytes"][self.rank])), dtype=torch.uint8,
+                                 device=self.device)
+        recv_stage = torch.empty(max(16, int(sum(msgs[3]))), dtype=torch.uint8, device=self.device)
+        return send_stage, recv_stage, msgs
+
+    def exchange(self, send_stage, recv_stage, msgs):
+        """Step a4 of the staged path: every per-peer message as one grouped send/recv
+        (torch.distributed.batch_isend_irecv == ncclGroupStart / ncclSend / ncclRecv /
+        ncclGroupEnd on an NCCL group; host-staged on a gloo group, for tests).  The message to
+        itself is a device-local copy."""
+        dist = self.dist
+        so, sb, ro, rb = msgs
+        me = self.rank
+        if sb[me]:
+            recv_stage[ro[me]:ro[me] + rb[me]].copy_(send_stage[so[me]:so[me] + sb[me]])
+        gloo = dist.get_backend(self.group) != "nccl"
+        host_recv = {}
+        ops = []
+        for p in range(self.world):
+            if p == me:
+                continue
+            if sb[p]:
+                buf = send_stage[so[p]:so[p] + sb[p]]
+                ops.append(dist.P2POp(dist.isend, buf.cpu() if gloo else buf, p, self.group))
+            if rb[p]:
+                buf = recv_stage[ro[p]:ro[p] + rb[p]]
+                if gloo:
+                    host_recv[p] = torch.empty(rb[p], dtype=torch.uint8)
+                    buf = host_recv[p]
+                ops.append(dist.P2POp(dist.irecv, buf, p, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for p, hbuf in host_recv.items():
+            recv_stage[ro[p]:ro[p] + rb[p]].copy_(hbuf)
+
+    def exec_staged(self, plan, send_bufs, recv_bufs, send_stage, recv_stage, msgs, stream=None):
+        """pack (this rank's records) -> grouped send/recv -> unpack (this rank's arrays)."""
+        plan.pack(send_bufs, [send_stage], stream)
+        self.exchange(send_stage, recv_stage, msgs)
+        plan.unpack([recv_stage], recv_bufs, stream)

@@ -36,8 +36,8 @@ EXPORTED = [
     "earl_comm_reset_alloc", "earl_comm_info", "earl_comm_destroy", "earl_dispatch_plan",
     "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
     "earl_plan_export", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
-    "earl_dispatch_unpack", "earl_status_string", "earl_last_error", "earl_abi_version",
-    "earl_kernel_launch_count",
+    "earl_dispatch_unpack", "earl_plan_messages", "earl_status_string", "earl_last_error",
+    "earl_abi_version", "earl_kernel_launch_count",
 ]
 
 
@@ -122,6 +122,7 @@ def lib():
         "earl_dispatch_exec": [vp, pvp, pvp, vp],
         "earl_dispatch_pack": [vp, pvp, pvp, vp],
         "earl_dispatch_unpack": [vp, pvp, pvp, vp],
+        "earl_plan_messages": [vp, i32, vp, vp, vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -292,6 +293,13 @@ class Plan:
         ptrs = [c.ctypes.data_as(C.c_void_p) for c in cols]
         check(lib().earl_plan_export(self.h, m, C.byref(n), *ptrs))
         return [tuple(int(c[j]) for c in cols) for j in range(m)]
+
+    def messages(self, rank: int):
+        """Per-peer (send_off, send_bytes, recv_off, recv_bytes) of `rank` (host-synchronising)."""
+        W = self.comm.world
+        arrs = [np.zeros(W, dtype=np.int64) for _ in range(4)]
+        check(lib().earl_plan_messages(self.h, int(rank), *[x.ctypes.data_as(C.c_void_p) for x in arrs]))
+        return [x.tolist() for x in arrs]
 
     # -- execution (stream-ordered, asynchronous) --
     def exec(self, send_bufs, recv_bufs, stream=None):

@@ -59,7 +59,8 @@ def gpu_main(rank, world, port, q, case):
         from paper_2510_05943_b200.dispatch import Dispatcher
         torch.cuda.set_device(0)
         init(rank, world, port, "gloo")
-        lens, src, dst, fields, n_exec = case
+        lens, src, dst, fields, n_exec = case[:5]
+        staged = len(case) > 5 and case[5] == "staged"
         T = sum(lens)
         glob = W.gen_global_fields(fields, T, seed_base=77, random_bits=True)
         src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
@@ -73,7 +74,11 @@ def gpu_main(rank, world, port, q, case):
             ptrs, views = D.alloc_recv(plan, fields)
             for v in views:
                 v.fill_(0xA5)
-            plan.exec(mine, ptrs)
+            if staged:  # pack -> grouped send/recv -> unpack
+                send_stage, recv_stage, msgs = D.alloc_stage(plan)
+                D.exec_staged(plan, mine, ptrs, send_stage, recv_stage, msgs)
+            else:
+                plan.exec(mine, ptrs)
             torch.cuda.synchronize()
             plan.sync()
             if rank in want:

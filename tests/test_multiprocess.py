@@ -56,8 +56,9 @@ def _gpu_ok():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fused", "staged"])
 @pytest.mark.parametrize("name", ["c1_dp2_dp1", "c3_dp4_tp4", "c4_dp4_sp2", "random"])
-def test_p2p_exec_processes_share_one_gpu(name):
+def test_p2p_exec_processes_share_one_gpu(name, mode):
     if not _gpu_ok():
         pytest.skip("needs a GPU")
     from paper_2510_05943_b200 import build
@@ -79,4 +80,4 @@ def test_p2p_exec_processes_share_one_gpu(name):
         lens = [rng.randint(0, 300) for _ in range(n)]
         src = random_layout(rng, world, n, allow_lpt=True)
         dst = random_layout(rng, world, n, allow_lpt=True)
-    run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 3),), timeout=600)
+    run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 3, mode),), timeout=600)
