@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-staged", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
+    ap.add_argument("--exchange", choices=["p2p", "staged"], default="p2p",
+                    help="N>1: fused P2P stores (default) or pack + grouped NCCL send/recv + unpack")
     return ap.parse_args()
 
 
@@ -441,6 +443,9 @@ def run_multi(args):
     plan = D.plan(src, dst, glens, fields)
     st = plan.stats()
     recv_ptrs, _views = D.alloc_recv(plan, fields)
+    staged = args.exchange == "staged"
+    if staged:
+        send_stage, recv_stage, msgs = D.alloc_stage(plan)
     plan.destroy()
 
     def step(ev=None):
@@ -450,7 +455,10 @@ def run_multi(args):
         p = D.plan(src, dst, gl, fields, stream)
         if ev is not None:
             ev[1].record(stream)
-        p.exec(send, recv_ptrs, stream)
+        if staged:  # pack -> grouped NCCL send/recv -> unpack (the exchange comparator)
+            D.exec_staged(p, send, recv_ptrs, send_stage, recv_stage, msgs, stream)
+        else:       # fused P2P: one pass, stores straight into the peers' windows
+            p.exec(send, recv_ptrs, stream)
         if ev is not None:
             ev[2].record(stream)
         p.destroy()
@@ -479,6 +487,47 @@ def run_multi(args):
     plan = D.plan(src, dst, glens, fields)
     plan.sync()
     plan.destroy()
+
+    # end to end through the public API with host buffers: H2D of this rank's payload (pinned),
+    # length all-gather, plan, exchange, D2H of this rank's cu_seqlens -- every step
+    e2e = None
+    if not (args.no_e2e or args.profile):
+        host_send = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in send]
+        for hs, d in zip(host_send, send):
+            hs.copy_(d)
+        ns_mine = int(st["n_local_seqs"][rank])
+        cu_dev = torch.empty(ns_mine + 1, dtype=torch.int32, device=dev)
+        cu_host = torch.empty(ns_mine + 1, dtype=torch.int32, pin_memory=True)
+        h2d = sum(hs.numel() for hs in host_send)
+
+        def e2e_step():
+            for hs, d in zip(host_send, send):
+                d.copy_(hs, non_blocking=True)
+            gl, _ = D.allgather_lens(my_lens)
+            p = D.plan(src, dst, gl, fields, stream)
+            if staged:
+                D.exec_staged(p, send, recv_ptrs, send_stage, recv_stage, msgs, stream)
+            else:
+                p.exec(send, recv_ptrs, stream)
+            p.local_meta(rank, cu_dev, None, None, stream)
+            cu_host.copy_(cu_dev, non_blocking=True)
+            p.destroy()
+
+        n_e2e = max(3, min(args.steps, 10))
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks([ea.elapsed_time(eb) / n_e2e])[0]
+        e2e = {"value": T * B / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int((ns_mine + 1) * 4),
+               "steps": n_e2e, "per_rank": True}
     if rank == 0:
         payload = T * B
         nvl = max(max(st["egress"]), max(st["ingress"]))
@@ -492,7 +541,9 @@ def run_multi(args):
                           "shared_gpu": shared},
                "per_gpu_GBps": payload / (ms_step * 1e-3) / 1e9 / world,
                "t_plan_ms": t_plan, "t_exec_ms": t_exec,
-               "roofline": {"bound": "nvlink", "kernel": "entry barrier + copy_kernel (P2P)",
+               "exchange": args.exchange,
+               "roofline": {"bound": "nvlink", "kernel": ("pack + NCCL send/recv + unpack" if staged
+                                                          else "entry barrier + copy_kernel (P2P)"),
                             "achieved": nvl / (t_exec * 1e-3) / 1e9, "peak": NVLINK_PEER_GBPS,
                             "unit": "GB/s", "frac": nvl / (t_exec * 1e-3) / 1e9 / NVLINK_PEER_GBPS,
                             "traffic": None, "algorithmic_bytes": int(nvl),
@@ -500,6 +551,8 @@ def run_multi(args):
                "gpu_launches": int(launches) * world,
                "plan_stats": {"max_egress": st["max_egress"], "max_ingress": st["max_ingress"],
                               "moved": st["moved"], "records": st["records"]}}
+        if e2e:
+            out["e2e"] = e2e
         if clocks:
             clocks.mark(t0, t1)
             out["clocks"] = clocks.stop()

@@ -692,15 +692,23 @@ CopyTrace& trace_state() {
   if (!init) { t.path = getenv("EARL_COPY_TRACE"); init = true; }
   return t;
 }
+// >= 90% of the bytes per token in fields whose width is a multiple of 16 B (always congruent)
+int congruent_heavy(const CopyArgs& a) {
+  uint64_t cong = 0;
+  for (int f = 0; f < a.n_fields; ++f)
+    if (a.Bf[f] % 16 == 0) cong += a.Bf[f];
+  return cong * 10 >= a.Bpre[a.n_fields] * 9 ? 1 : 0;
+}
+
 cudaError_t traced_launch(CopyArgs& a, earl_comm* c, cudaStream_t s) {
   clear_stale_error();
   CopyTrace& t = trace_state();
-  if (!t.path) return launch_copy(a, copy_grid(c), 0, s);
+  if (!t.path) return launch_copy(a, copy_grid(c), congruent_heavy(a), s);
   const size_t n = (size_t)c->sm_count * 64 * 4;
   if (!t.dev) { cudaMalloc(&t.dev, n * 8); t.n = n; }
   cudaMemsetAsync(t.dev, 0, n * 8, s);
   a.trace = t.dev;
-  cudaError_t e = launch_copy(a, copy_grid(c), 0, s);
+  cudaError_t e = launch_copy(a, copy_grid(c), congruent_heavy(a), s);
   if (e != cudaSuccess) return e;
   std::vector<uint64_t> h(n);
   cudaMemcpyAsync(h.data(), t.dev, n * 8, cudaMemcpyDeviceToHost, s);

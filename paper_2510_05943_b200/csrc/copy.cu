@@ -108,7 +108,7 @@ struct __align__(16) SubDesc {
 };
 static_assert(sizeof(SubDesc) == 32, "SubDesc layout");
 
-constexpr int kSubs = 32;        // sub-ranges per stage
+constexpr int kSubs = 16;        // sub-ranges per stage
 constexpr uint32_t kMinSpace = 256;  // close a stage when less than this is left
 
 struct __align__(16) StageDesc {
@@ -163,15 +163,6 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-// Lane-0-only walker over a warp's share of the launch's work.
-//
-// Work is measured in a record-major cost space: record j (all fields) occupies
-// [cost(j), cost(j+1)) with cost(j) = (tok_prefix[j] - tbeg) * B + (j - rbeg) * F * c0, and
-// field f of record j is the sub-interval starting at n_j * Bpre[f] + f * c0 whose first
-// n_j * B_f cost units map 1:1 to its bytes, followed by c0 units that map to no bytes (the
-// fixed cost of a piece).  Equal-byte slices made the warps holding thousands of small scalar
-// pieces the stragglers (profiles/r01_trace.txt); the c0 term balances them.  Record-major
-// order loads a record's metadata once for all of its fields.
 // The records a launch moves, as up to 8 contiguous blocks of the (s, ds, i, x)-ordered record
 // table: everything (emulated comm), this rank's own records (fused exec / pack), or, for the
 // unpack of a real rank, one block per source rank that sends to it -- each with the start of
@@ -229,14 +220,16 @@ __device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
 // units that map to no bytes (the fixed cost of a piece).  Equal-byte slices made the warps
 // holding thousands of small scalar pieces the stragglers; the c0 term balances them.
 // Record-major order loads a record's metadata once for all of its fields.
+//
+// The walker holds scalars only (so it lives in registers); the launch's View (dynamically
+// indexed, local memory) is consulted only when a warp changes block, and the kernel parameter
+// is passed by reference into every (inlined) method so its fields are constant-bank loads.
 struct Walker {
-  const CopyArgs* a;
-  const PlanHeader* h;
-  View v;
-  int b;  // current view block
-  uint64_t c0, x1, xpos, unit, n_units, first_dyn;
-  unsigned int* work_ctr;
-  int F;
+  int b;  // current view block and its fields
+  int64_t b_rbeg, b_rend, b_tbeg;
+  uint64_t b_cbase;
+  const uint8_t* b_msg;
+  uint64_t c0, x1, xpos, unit, n_units, first_dyn, total;
   // current record
   int64_t j;
   int f;
@@ -250,79 +243,91 @@ struct Walker {
   uint64_t prem;
   int pf, pd0;
 
-  __device__ uint64_t cost(int bb, int64_t jj) const {
-    return v.cbase[bb] + (uint64_t)(a->rec.tok_prefix[jj] - v.tbeg[bb]) * a->Bpre[F] +
-           (uint64_t)(jj - v.rbeg[bb]) * F * c0;
-  }
-  __device__ uint64_t total() const { return v.cbase[v.n]; }
-
-  __device__ void setup(const CopyArgs* a_, uint64_t c0_, uint64_t first_dyn_) {
-    a = a_; h = a_->hdr; c0 = c0_; unit = 0; n_units = 0; first_dyn = first_dyn_;
-    work_ctr = a_->work_ctr; F = a_->n_fields;
-    prem = 0; R = 0; xpos = x1 = 0; f = 0; b = 0;
-    build_view(*a_, c0_, v);
-    j = v.n ? v.rbeg[0] : 0;
+  __device__ __forceinline__ void set_block(const View& v, int bb) {
+    b = bb;
+    if (bb < v.n) {
+      b_rbeg = v.rbeg[bb]; b_rend = v.rend[bb]; b_tbeg = v.tbeg[bb]; b_cbase = v.cbase[bb];
+      b_msg = v.msg[bb];
+    } else {
+      b_rbeg = b_rend = b_tbeg = 0; b_cbase = 0; b_msg = nullptr;
+    }
   }
 
-  __device__ void load_record(int64_t jj) {
+  __device__ __forceinline__ void setup(const CopyArgs& a, const View& v, uint64_t c0_,
+                                        uint64_t first_dyn_) {
+    c0 = c0_; unit = 0; n_units = 0; first_dyn = first_dyn_; total = v.cbase[v.n];
+    prem = 0; R = 0; xpos = x1 = 0; f = 0;
+    set_block(v, 0);
+    j = b_rbeg;
+  }
+
+  __device__ __forceinline__ uint64_t cost(const CopyArgs& a, int64_t jj) const {
+    const int F = a.n_fields;
+    return b_cbase + (uint64_t)(a.rec.tok_prefix[jj] - b_tbeg) * a.Bpre[F] +
+           (uint64_t)(jj - b_rbeg) * F * c0;
+  }
+
+  __device__ __forceinline__ void load_record(const CopyArgs& a, int64_t jj) {
+    const int F = a.n_fields;
     j = jj;
-    const int64_t t0 = a->rec.tok_prefix[jj], t1 = a->rec.tok_prefix[jj + 1];
-    const uint32_t code = a->rec.code[jj];
-    src_tok = a->rec.src_tok[jj];
-    dst_tok = a->rec.dst_tok[jj];
+    const int64_t t0 = a.rec.tok_prefix[jj], t1 = a.rec.tok_prefix[jj + 1];
+    const uint32_t code = a.rec.code[jj];
+    src_tok = a.rec.src_tok[jj];
+    dst_tok = a.rec.dst_tok[jj];
     n = (uint64_t)(t1 - t0);
-    cj = v.cbase[b] + (uint64_t)(t0 - v.tbeg[b]) * a->Bpre[F] + (uint64_t)(jj - v.rbeg[b]) * F * c0;
+    cj = b_cbase + (uint64_t)(t0 - b_tbeg) * a.Bpre[F] + (uint64_t)(jj - b_rbeg) * F * c0;
     s = code & 0xff;
     const int ss = (code >> 8) & 0xff;
     ds = (code >> 16) & 0xff;
     ts = code >> 24;
-    d0 = a->rank0_d + ds * a->tp_d + ts;
-    if (a->mode != kDirect) {
-      const int key = ss * a->n_dst_shards + ds;
-      msg_tok = a->rec.msg_tok[jj];
-      kt = h->key_tokens[key];
-      msg_base = h->msg_off[key];
+    d0 = a.rank0_d + ds * a.tp_d + ts;
+    if (a.mode != kDirect) {
+      const int key = ss * a.n_dst_shards + ds;
+      msg_tok = a.rec.msg_tok[jj];
+      kt = a.hdr->key_tokens[key];
+      msg_base = a.hdr->msg_off[key];
     }
     f = 0;
     fo = 0;
     fb = 0;
   }
 
-  __device__ void next_field() {
-    if (a->mode != kDirect) fb += (kt * a->Bf[f] + 15) & ~15LL;
-    fo += n * a->Bf[f] + c0;
+  __device__ __forceinline__ void next_field(const CopyArgs& a) {
+    if (a.mode != kDirect) fb += (kt * a.Bf[f] + 15) & ~15LL;
+    fo += n * a.Bf[f] + c0;
     ++f;
   }
 
-  // Claim the next unit: returns false when the launch's work is exhausted.
-  __device__ bool claim() {
-    const uint64_t u = first_dyn + atomicAdd(work_ctr, 1u);
-    if (u >= n_units) return false;
-    start(u * unit, (u + 1) * unit);
-    return true;
-  }
-
-  __device__ void start(uint64_t x0, uint64_t x1_) {
-    const uint64_t tot = total();
-    x1 = x1_ < tot ? x1_ : tot;
+  __device__ __forceinline__ void start(const CopyArgs& a, const View& v, uint64_t x0,
+                                        uint64_t x1_) {
+    x1 = x1_ < total ? x1_ : total;
     xpos = x0;
     prem = 0;
     if (xpos >= x1) return;
-    b = 0;
-    while (b + 1 < v.n && v.cbase[b + 1] <= xpos) ++b;
-    int64_t lo = v.rbeg[b], hi = v.rend[b] - 1;  // last record whose cost starts <= xpos
+    int bb = 0;
+    while (bb + 1 < v.n && v.cbase[bb + 1] <= xpos) ++bb;
+    set_block(v, bb);
+    int64_t lo = b_rbeg, hi = b_rend - 1;  // last record whose cost starts <= xpos
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
-      if (cost(b, mid) <= xpos) lo = mid; else hi = mid - 1;
+      if (cost(a, mid) <= xpos) lo = mid; else hi = mid - 1;
     }
-    load_record(lo);
-    while (f + 1 < F && cj + fo + n * a->Bf[f] + c0 <= xpos) next_field();
+    load_record(a, lo);
+    while (f + 1 < a.n_fields && cj + fo + n * a.Bf[f] + c0 <= xpos) next_field(a);
   }
 
-  __device__ bool next_piece() {
-    const bool unpack_rank = a->mode == kUnpack && a->view_rank >= 0;
+  // Claim the next unit: returns false when the launch's work is exhausted.
+  __device__ __forceinline__ bool claim(const CopyArgs& a, const View& v) {
+    const uint64_t u = first_dyn + atomicAdd(a.work_ctr, 1u);
+    if (u >= n_units) return false;
+    start(a, v, u * unit, (u + 1) * unit);
+    return true;
+  }
+
+  __device__ __forceinline__ bool next_piece(const CopyArgs& a, const View& v) {
+    const bool unpack_rank = a.mode == kUnpack && a.view_rank >= 0;
     while (xpos < x1) {
-      const uint64_t Bf = a->Bf[f];
+      const uint64_t Bf = a.Bf[f];
       const uint64_t nb = n * Bf;
       const uint64_t fstart = cj + fo, fend = fstart + nb + c0;
       const uint64_t lo = xpos - fstart;
@@ -332,27 +337,27 @@ struct Walker {
       bool found = false;
       if (u1 > u0) {
         int64_t msg_field = 0;
-        if (a->mode != kDirect) msg_field = msg_base + fb + msg_tok * (int64_t)Bf + (int64_t)u0;
-        if (a->mode == kUnpack) {
-          psrc = unpack_rank ? v.msg[b] + fb + msg_tok * (int64_t)Bf + (int64_t)u0
-                             : a->stage[s] + msg_field;
+        if (a.mode != kDirect) msg_field = msg_base + fb + msg_tok * (int64_t)Bf + (int64_t)u0;
+        if (a.mode == kUnpack) {
+          psrc = unpack_rank ? b_msg + fb + msg_tok * (int64_t)Bf + (int64_t)u0
+                             : a.stage[s] + msg_field;
         } else {
-          psrc = a->src[s][f] + src_tok * (int64_t)Bf + (int64_t)u0;
+          psrc = a.src[s][f] + src_tok * (int64_t)Bf + (int64_t)u0;
         }
-        if (a->mode == kPack) {
-          pdst = a->stage[s] + msg_field;
+        if (a.mode == kPack) {
+          pdst = a.stage[s] + msg_field;
           R = 1;
           pd0 = d0;
         } else if (unpack_rank) {
-          uint8_t* base = a->dst[a->me][f];
+          uint8_t* base = a.dst[a.me][f];
           pdst = base + dst_tok * (int64_t)Bf + (int64_t)u0;
           R = base != nullptr ? 1 : 0;
-          pd0 = a->me;
+          pd0 = a.me;
         } else {
           R = 0;
-          uint8_t* base0 = a->dst[d0][f];
-          for (int td = ts; td < a->tp_d; td += a->tp_s)
-            if (a->dst[d0 + (td - ts)][f] != nullptr) ++R;
+          uint8_t* base0 = a.dst[d0][f];
+          for (int td = ts; td < a.tp_d; td += a.tp_s)
+            if (a.dst[d0 + (td - ts)][f] != nullptr) ++R;
           pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
           if (base0 == nullptr) R = 0;
           pd0 = d0;
@@ -363,13 +368,13 @@ struct Walker {
       }
       if (x1 >= fend) {
         xpos = fend;
-        if (f + 1 < F) {
-          next_field();
-        } else if (j + 1 < v.rend[b]) {
-          load_record(j + 1);
+        if (f + 1 < a.n_fields) {
+          next_field(a);
+        } else if (j + 1 < b_rend) {
+          load_record(a, j + 1);
         } else if (b + 1 < v.n) {
-          ++b;
-          load_record(v.rbeg[b]);
+          set_block(v, b + 1);
+          load_record(a, b_rbeg);
         } else {
           xpos = x1;
         }
@@ -383,9 +388,10 @@ struct Walker {
 
   // Next source range of at most `space` stage bytes (space >= kMinSpace): false when the
   // launch's work is exhausted.
-  __device__ bool next_sub(SubDesc& d, uint32_t space) {
-    while (prem == 0 && !next_piece())
-      if (!claim()) return false;
+  __device__ __forceinline__ bool next_sub(const CopyArgs& a, const View& v, SubDesc& d,
+                                           uint32_t space) {
+    while (prem == 0 && !next_piece(a, v))
+      if (!claim(a, v)) return false;
     const uint32_t off = (uint32_t)((uintptr_t)psrc & 15);
     const uint64_t room = space - off;
     const uint32_t len = (uint32_t)(prem < room ? prem : room);
@@ -407,10 +413,11 @@ struct Walker {
 // Fill stage `st` (lane 0): pack source ranges until the stage is full, then one expect_tx for
 // the total and one TMA load per range, all completing on the stage's mbarrier.
 template <int CHUNK>
-__device__ __forceinline__ bool fill_stage(Walker& wk, StageDesc& sd, uint8_t* stage, uint64_t* bar) {
+__device__ __forceinline__ bool fill_stage(const CopyArgs& a, const View& v, Walker& wk,
+                                           StageDesc& sd, uint8_t* stage, uint64_t* bar) {
   uint32_t used = 0, n = 0;
   while (n < (uint32_t)kSubs && CHUNK - used >= kMinSpace) {
-    if (!wk.next_sub(sd.sub[n], CHUNK - used)) break;
+    if (!wk.next_sub(a, v, sd.sub[n], CHUNK - used)) break;
     sd.sub[n].so = used;
     used += sd.sub[n].load_bytes;
     ++n;
@@ -535,22 +542,24 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     const uint64_t nwarps = (uint64_t)gridDim.x * WARPS;
     const uint64_t wid = (uint64_t)blockIdx.x * WARPS + w;
     Walker wk;
+    View v;
     uint64_t t_start = 0;
     int nprod = 0;
     if (lane == 0) {
       if (a.trace) t_start = globaltimer();
-      wk.setup(&a, c0, nwarps);
-      const uint64_t total = wk.total();
+      build_view(a, c0, v);
+      wk.setup(a, v, c0, nwarps);
+      const uint64_t total = wk.total;
       // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
       uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
       if (unit < 4 * (uint64_t)CHUNK) unit = 4 * (uint64_t)CHUNK;
       wk.unit = unit;
       wk.n_units = (total + unit - 1) / unit;
-      if (wid < wk.n_units) wk.start(wid * unit, (wid + 1) * unit);
+      if (wid < wk.n_units) wk.start(a, v, wid * unit, (wid + 1) * unit);
     }
     for (int s = 0; s < STAGES - 1; ++s) {
       int ok = 0;
-      if (lane == 0) ok = fill_stage<CHUNK>(wk, desc[s], data + (size_t)s * CHUNK, &bar[s]);
+      if (lane == 0) ok = fill_stage<CHUNK>(a, v, wk, desc[s], data + (size_t)s * CHUNK, &bar[s]);
       ok = __shfl_sync(kFull, ok, 0);
       if (!ok) break;
       ++nprod;
@@ -567,7 +576,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       if (lane == 0) {
         const int ns = (c + STAGES - 1) % STAGES;
         fence_proxy_async_smem();
-        ok = fill_stage<CHUNK>(wk, desc[ns], data + (size_t)ns * CHUNK, &bar[ns]);
+        ok = fill_stage<CHUNK>(a, v, wk, desc[ns], data + (size_t)ns * CHUNK, &bar[ns]);
       }
       ok = __shfl_sync(kFull, ok, 0);
       if (ok) ++nprod;
@@ -630,19 +639,25 @@ cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
 
 }  // namespace
 
-// Copy-engine shape (warps per CTA, ring stages, chunk bytes).  The default was chosen by
-// measurement (profiles/); EARL_COPY_CFG selects another compiled shape for tuning.
-cudaError_t launch_copy(const CopyArgs& a, int sm_count, int /*unused*/, cudaStream_t s) {
-  static int cfg = -1;
-  if (cfg < 0) {
+// Copy-engine shape (warps per CTA, ring stages, chunk bytes), chosen per launch from the field
+// widths (measured): when nearly all bytes sit in fields whose width is a
+// multiple of 16 B (hidden vectors: source and destination always congruent, bytes leave by TMA
+// bulk stores) 4 warps x 4 stages write fewer concurrent streams and win on TP-replicated
+// stores (0.934 vs 0.915 of peak on c3); otherwise the realign path needs the issue slots of 8
+// warps (0.93 vs 0.63 on the long-tail scalar sweep).  EARL_COPY_CFG forces a shape for tuning.
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s) {
+  static int forced = -2;
+  if (forced == -2) {
     const char* e = getenv("EARL_COPY_CFG");
-    cfg = e ? atoi(e) : 0;
+    forced = e ? atoi(e) : -1;
   }
+  const int cfg = forced >= 0 ? forced : (congruent_heavy ? 2 : 3);
   switch (cfg) {
     case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
     case 2: return launch_cfg<4, 4, 8192>(a, sm_count, s);
     case 4: return launch_cfg<2, 8, 8192>(a, sm_count, s);
     case 5: return launch_cfg<16, 2, 4096>(a, sm_count, s);
+    case 6: return launch_cfg<8, 4, 6144>(a, sm_count, s);
     default: return launch_cfg<8, 3, 8192>(a, sm_count, s);
   }
 }

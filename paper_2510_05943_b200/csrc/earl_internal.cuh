@@ -132,7 +132,7 @@ constexpr int kDoneSlot = 8;
 // launchers (defined in the .cu files)
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
-cudaError_t launch_copy(const CopyArgs& a, int sm_count, int unused, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
                                  uint64_t epoch, uint64_t timeout_ns, int32_t* err,
                                  int32_t* err_detail, cudaStream_t s);

@@ -412,10 +412,9 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
         a.ps_kk[pos] = a.pc_kk[q];
       },
       a.ghist, ps);
-  if (lead) {
-    if (tid <= K) h->key_piece_start[tid] = ps.bstart[tid];
-    if (tid < K) h->key_pieces[tid] = ps.bstart[tid + 1] - ps.bstart[tid];
-  }
+  __shared__ int64_t s_kstart[kMaxKeys + 1], s_ktok[kMaxKeys], s_kscan0[kMaxKeys];
+  __shared__ int64_t s_rbase[kMaxWorld][kMaxShards], s_tbase[kMaxWorld][kMaxShards];
+  if (tid <= K) s_kstart[tid] = ps.bstart[tid];
   gsync();
   const int64_t Mtok = grid_scan(
       M, [&](int64_t q) { return (int64_t)(a.ps_y[q] - a.ps_x[q]); },
@@ -423,43 +422,69 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   if (lead && tid == 0) a.ps_scan[M] = Mtok;
   gsync();
 
-  // ---- phase 5: bases and message offsets (one thread; <= 8 x 8 entries) --------------
+  // ---- phase 5: bases and message offsets ---------------------------------------------
+  // Every CTA derives the <= 64-entry tables itself in shared memory (parallel loads of the
+  // published scan, then one thread walks <= 8 x 8 entries in shared memory); CTA 0 also
+  // publishes them in the header for the copy kernels and the host.
   const int nts = S.tp < Dl.tp ? S.tp : Dl.tp;
-  if (lead && tid == 0) {
-    for (int key = 0; key < K; ++key)
-      h->key_tokens[key] = a.ps_scan[h->key_piece_start[key + 1]] - a.ps_scan[h->key_piece_start[key]];
+  if (tid < K) {
+    s_kscan0[tid] = a.ps_scan[s_kstart[tid]];
+    s_ktok[tid] = a.ps_scan[s_kstart[tid + 1]] - s_kscan0[tid];
+  }
+  __syncthreads();
+  __shared__ int64_t s_rec_begin[kMaxWorld + 1], s_tok_begin[kMaxWorld + 1];
+  __shared__ int64_t s_msg_off[kMaxKeys], s_stage[kMaxShards];
+  if (tid == 0) {
     int64_t rec = 0, tok = 0;
     for (int r = 0; r < a.world; ++r) {
-      h->rec_begin[r] = rec;
-      h->rec_tok_begin[r] = tok;
+      s_rec_begin[r] = rec;
+      s_tok_begin[r] = tok;
       const int rr = r - S.rank0;
       const bool in_src = rr >= 0 && rr < S.dp * S.sp * S.tp;
       const int ss = in_src ? rr / S.tp : 0, ts = in_src ? rr % S.tp : 0;
       for (int ds = 0; ds < Sd; ++ds) {
-        h->rec_base[r][ds] = rec;
-        h->rec_tok_base[r][ds] = tok;
+        s_rbase[r][ds] = rec;
+        s_tbase[r][ds] = tok;
         if (in_src && ts < nts) {
-          rec += h->key_pieces[ss * Sd + ds];
-          tok += h->key_tokens[ss * Sd + ds];
+          rec += s_kstart[ss * Sd + ds + 1] - s_kstart[ss * Sd + ds];
+          tok += s_ktok[ss * Sd + ds];
         }
       }
     }
-    h->rec_begin[a.world] = rec;
-    h->rec_tok_begin[a.world] = tok;
-    h->n_records = rec;
-    h->rec_tokens = tok;
+    s_rec_begin[a.world] = rec;
+    s_tok_begin[a.world] = tok;
     for (int ss = 0; ss < S.dp * S.sp; ++ss) {
       int64_t off = 0;
       for (int ds = 0; ds < Sd; ++ds) {
-        h->msg_off[ss * Sd + ds] = off;
-        for (int f = 0; f < a.n_fields; ++f)
-          off += (h->key_tokens[ss * Sd + ds] * a.Bf[f] + 15) & ~15LL;
+        s_msg_off[ss * Sd + ds] = off;
+        for (int f = 0; f < a.n_fields; ++f) off += (s_ktok[ss * Sd + ds] * a.Bf[f] + 15) & ~15LL;
       }
-      h->stage_bytes_shard[ss] = off;
+      s_stage[ss] = off;
     }
-    a.rec.tok_prefix[rec] = tok;
   }
-  gsync();
+  __syncthreads();
+  if (lead) {
+    if (tid <= K) h->key_piece_start[tid] = s_kstart[tid];
+    if (tid < K) {
+      h->key_pieces[tid] = s_kstart[tid + 1] - s_kstart[tid];
+      h->key_tokens[tid] = s_ktok[tid];
+      h->msg_off[tid] = s_msg_off[tid];
+    }
+    if (tid < S.dp * S.sp) h->stage_bytes_shard[tid] = s_stage[tid];
+    if (tid <= a.world) {
+      h->rec_begin[tid] = s_rec_begin[tid];
+      h->rec_tok_begin[tid] = s_tok_begin[tid];
+    }
+    if (tid < a.world * Sd) {
+      h->rec_base[tid / Sd][tid % Sd] = s_rbase[tid / Sd][tid % Sd];
+      h->rec_tok_base[tid / Sd][tid % Sd] = s_tbase[tid / Sd][tid % Sd];
+    }
+    if (tid == 0) {
+      h->n_records = s_rec_begin[a.world];
+      h->rec_tokens = s_tok_begin[a.world];
+      a.rec.tok_prefix[s_rec_begin[a.world]] = s_tok_begin[a.world];
+    }
+  }
 
   // ---- phase 6: records ---------------------------------------------------------------
   const int64_t nrec = M * nts;
@@ -470,12 +495,12 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     const int ks = kk & 0xff, kd = (kk >> 8) & 0xff, key = kk >> 16;
     const int ss = key / Sd, ds = key - ss * Sd;
     const int s = S.rank0 + ss * S.tp + ts;
-    const int64_t rho = q - h->key_piece_start[key];
-    const int64_t j = h->rec_base[s][ds] + rho;
+    const int64_t rho = q - s_kstart[key];
+    const int64_t j = s_rbase[s][ds] + rho;
     const int i = a.ps_i[q];
     const int64_t x = a.ps_x[q], y = a.ps_y[q];
     const int64_t L = a.lens[i];
-    const int64_t msg_tok = a.ps_scan[q] - a.ps_scan[h->key_piece_start[key]];
+    const int64_t msg_tok = a.ps_scan[q] - s_kscan0[key];
     a.rec.seq[j] = i;
     a.rec.x[j] = (int32_t)x;
     a.rec.n[j] = (int32_t)(y - x);
@@ -483,7 +508,7 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     a.rec.src_tok[j] = a.off[0][(int64_t)ks * N + i] + (x - chunk_lo(L, S.sp, ks));
     a.rec.dst_tok[j] = a.off[1][(int64_t)kd * N + i] + (x - chunk_lo(L, Dl.sp, kd));
     a.rec.msg_tok[j] = msg_tok;
-    a.rec.tok_prefix[j] = h->rec_tok_base[s][ds] + msg_tok;
+    a.rec.tok_prefix[j] = s_tbase[s][ds] + msg_tok;
   }
 }
 
