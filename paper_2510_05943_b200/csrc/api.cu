@@ -412,6 +412,8 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   total += sz(N + 1, 8);
   total += 8 * sz(max_pieces, 4) + sz(max_pieces + 1, 8);
   total += sz(kMaxPlanGrid, 8) + sz((int64_t)kMaxPlanGrid * kMaxKeys, 4);
+  const int64_t nscr = (N > max_pieces ? N : max_pieces) + 1;
+  total += sz(nscr, 8) + 2 * sz(nscr, 4);
   total += 4 * sz(max_records, 4) + 3 * sz(max_records, 8) + sz(max_records + 1, 8);
   p->mem_bytes = total;
   cudaError_t e = cudaMallocAsync(&p->mem, total, s);
@@ -444,6 +446,9 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   a.ps_scan = carve<int64_t>(q, max_pieces + 1);
   a.cta_sums = carve<int64_t>(q, kMaxPlanGrid);
   a.ghist = carve<int32_t>(q, (int64_t)kMaxPlanGrid * kMaxKeys);
+  a.vtmp = carve<int64_t>(q, nscr);
+  a.ktmp = carve<int32_t>(q, nscr);
+  a.ptmp = carve<int32_t>(q, nscr);
   a.rec.seq = carve<int32_t>(q, max_records);
   a.rec.x = carve<int32_t>(q, max_records);
   a.rec.n = carve<int32_t>(q, max_records);
@@ -469,8 +474,21 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
     lpt_smem = (size_t)n2 * sizeof(uint64_t);
   }
   const int grid = planner_grid(N, max_pieces, c->sm_count, lpt_smem);
+  static const char* plan_trace = getenv("EARL_PLAN_TRACE");
+  if (plan_trace) cudaMallocAsync((void**)&a.phase_ts, 16 * sizeof(uint64_t), s);
   clear_stale_error();
   e = launch_planner(a, lpt_smem, grid, s);
+  if (plan_trace && e == cudaSuccess) {  // debug only: synchronous read-back of phase times
+    uint64_t ts[16];
+    cudaMemcpyAsync(ts, a.phase_ts, sizeof(ts), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "earl plan trace N=%lld G=%d us:", (long long)N, grid);
+    for (int k = 1; k < 8; ++k) fprintf(stderr, " p%d=%.1f", k - 1, (ts[k] - ts[k - 1]) / 1e3);
+    fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]\n", (ts[7] - ts[0]) / 1e3,
+            (ts[8] - ts[5]) / 1e3, (ts[9] - ts[8]) / 1e3, (ts[6] - ts[9]) / 1e3);
+    cudaFreeAsync(a.phase_ts, s);
+    a.phase_ts = nullptr;
+  }
   if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "planner launch", e);
   g_launches.fetch_add(1);
   e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming);

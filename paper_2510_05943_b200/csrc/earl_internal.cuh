@@ -84,6 +84,10 @@ struct PlanArgs {
   int64_t* ps_scan;          // [max_pieces+1]
   int64_t* cta_sums;         // [kMaxPlanGrid] grid-scan partials
   int32_t* ghist;            // [kMaxPlanGrid][kMaxKeys] grid-partition histograms
+  int64_t* vtmp;             // [max(N, max_pieces) + 1] scan inputs
+  int32_t* ktmp;             // [max(N, max_pieces)] partition keys
+  int32_t* ptmp;             // [max(N, max_pieces)] partition output (position -> index)
+  uint64_t* phase_ts;        // debug (EARL_PLAN_TRACE): %globaltimer at phase boundaries
   int64_t max_pieces;
   int64_t max_records;
   Records rec;

@@ -39,6 +39,14 @@ __device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
   if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
 }
 
+__device__ __forceinline__ void stamp(const PlanArgs& a, int k) {
+  if (a.phase_ts != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.phase_ts[k] = t;
+  }
+}
+
 __device__ __forceinline__ void gsync() {
   if (gridDim.x == 1) __syncthreads();
   else cg::this_grid().sync();
@@ -48,12 +56,14 @@ __device__ __forceinline__ int64_t range_lo(int64_t n) { return n * blockIdx.x /
 __device__ __forceinline__ int64_t range_hi(int64_t n) { return n * (blockIdx.x + 1) / gridDim.x; }
 
 // BLOCK rule: q = L / sp, r = L % sp, chunk k = [k*q + min(k,r), (k+1)*q + min(k+1,r)).
+// Sequence lengths are int32 (the C ABI's seq_lens), so the division is 32-bit.
 __device__ __forceinline__ int64_t chunk_lo(int64_t L, int sp, int k) {
-  const int64_t q = L / sp, r = L % sp;
-  return k * q + (k < r ? (int64_t)k : r);
+  const uint32_t q = (uint32_t)L / (uint32_t)sp, r = (uint32_t)L - q * (uint32_t)sp;
+  return (int64_t)k * q + ((uint32_t)k < r ? (uint32_t)k : r);
 }
 __device__ __forceinline__ int64_t chunk_len(int64_t L, int sp, int k) {
-  return L / sp + ((int64_t)k < L % sp ? 1 : 0);
+  const uint32_t q = (uint32_t)L / (uint32_t)sp, r = (uint32_t)L - q * (uint32_t)sp;
+  return (int64_t)q + ((uint32_t)k < r ? 1 : 0);
 }
 
 // Block-wide exclusive scan of one int64 per thread.  sm: [NT/32 + 1].
@@ -221,6 +231,25 @@ __device__ void grid_partition(int64_t n, int K, KeyF key, Emit emit, int32_t* g
   }
 }
 
+// The planner's code runs once per plan in a single CTA for the configs' N, so its latency is
+// dominated by instruction fetch: every scan and partition therefore goes through ONE
+// non-inlined copy of these two routines over plain arrays (values / keys precomputed by
+// small elementwise passes), instead of one inlined instantiation per call site.
+__device__ __noinline__ int64_t scan_array(const int64_t* vals, int64_t* out, int64_t n,
+                                           int64_t* cta_sums, int64_t* sm) {
+  return grid_scan(
+      n, [&](int64_t i) { return vals[i]; }, [&](int64_t i, int64_t ex) { out[i] = ex; }, cta_sums,
+      sm);
+}
+
+__device__ __noinline__ void partition_array(const int32_t* keys, int64_t n, int K,
+                                             int32_t* perm_out, int32_t* ghist,
+                                             PartitionSmem& ps) {
+  grid_partition(
+      n, K, [&](int64_t i) { return keys[i]; },
+      [&](int64_t i, int64_t pos) { perm_out[pos] = (int32_t)i; }, ghist, ps);
+}
+
 // Two-pointer intersection of the BLOCK partitions of [0, L) into sps and spd chunks:
 // calls f(ks, kd, x, y) for every non-empty overlap in increasing x.
 template <class F>
@@ -240,7 +269,7 @@ __device__ __forceinline__ int for_each_piece(int64_t L, int sps, int spd, F f) 
 
 // LPT (one CTA; N <= 8192): bitonic sort of (INT32_MAX - L, i) keys in shared memory, then
 // Graham's greedy in one thread with the D <= 8 loads in registers.
-__device__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
+__device__ __noinline__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
   const int tid = threadIdx.x;
   const int64_t N = a.N;
   const int D = a.lay[l].dp;
@@ -263,24 +292,62 @@ __device__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys) {
       __syncthreads();
     }
   }
-  if (tid == 0) {
+  if (a.P[N] < (1LL << 28)) {
+    // Graham's greedy on warp 0: lane g holds group g's load; the least-loaded group (ties to
+    // the lowest index) is one __reduce_min_sync over (load << 3 | g) -- loads stay < 2^28
+    if (tid < 32) {
+      const int lane = tid;
+      uint32_t load = 0;
+      for (int64_t q = 0; q < N; ++q) {
+        const uint64_t key = keys[q];
+        const uint32_t L = 0x7fffffffu - (uint32_t)(key >> 32);
+        const uint32_t packed = lane < D ? ((load << 3) | (uint32_t)lane) : 0xffffffffu;
+        const uint32_t m = __reduce_min_sync(kFull, packed);
+        const int best = (int)(m & 7u);
+        if (lane == best) load += L;
+        __syncwarp();
+        if (lane == 0) keys[q] = (key & 0xffffffffull) | ((uint64_t)best << 32);
+      }
+    }
+  } else if (tid == 0) {
+    // Graham's greedy: the least-loaded group (ties to the lowest index) by a depth-3
+    // tournament over the <= 8 register-resident loads (groups >= D never win)
     int64_t ld[kMaxShards];
 #pragma unroll
-    for (int g = 0; g < kMaxShards; ++g) ld[g] = 0;
-    for (int64_t q = 0; q < N; ++q) {
-      const uint64_t key = keys[q];
-      const int i = (int)(key & 0xffffffffu);
-      const int64_t L = (int64_t)(0x7fffffffu - (uint32_t)(key >> 32));
-      int best = 0;
-      int64_t bl = ld[0];
+    for (int g = 0; g < kMaxShards; ++g) ld[g] = g < D ? 0 : INT64_MAX;
+    constexpr int kB = 8;  // keys are read 8 at a time (independent loads off the chain)
+    for (int64_t q0 = 0; q0 < N; q0 += kB) {
+      uint64_t kb[kB];
 #pragma unroll
-      for (int g = 1; g < kMaxShards; ++g)
-        if (g < D && ld[g] < bl) { bl = ld[g]; best = g; }
+      for (int u = 0; u < kB; ++u) kb[u] = (q0 + u < N) ? keys[q0 + u] : 0;
 #pragma unroll
-      for (int g = 0; g < kMaxShards; ++g)
-        if (g == best) ld[g] += L;
-      a.grp[l][i] = best;
+      for (int u = 0; u < kB; ++u) {
+        if (q0 + u >= N) break;
+        const int64_t L = (int64_t)(0x7fffffffu - (uint32_t)(kb[u] >> 32));
+        int w1[4];
+        int64_t v1[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const bool right = ld[2 * p + 1] < ld[2 * p];
+          w1[p] = right ? 2 * p + 1 : 2 * p;
+          v1[p] = right ? ld[2 * p + 1] : ld[2 * p];
+        }
+        const bool r2a = v1[1] < v1[0], r2b = v1[3] < v1[2];
+        const int wa = r2a ? w1[1] : w1[0], wb = r2b ? w1[3] : w1[2];
+        const int64_t va = r2a ? v1[1] : v1[0], vb = r2b ? v1[3] : v1[2];
+        const int best = vb < va ? wb : wa;
+#pragma unroll
+        for (int g = 0; g < kMaxShards; ++g)
+          if (g == best) ld[g] += L;
+        // the key is consumed: keep (i, group) in its slot for the parallel write-out
+        keys[q0 + u] = (kb[u] & 0xffffffffull) | ((uint64_t)best << 32);
+      }
     }
+  }
+  __syncthreads();
+  for (int64_t q = tid; q < N; q += NT) {
+    const uint64_t v = keys[q];
+    a.grp[l][(int)(v & 0xffffffffu)] = (int32_t)(v >> 32);
   }
   __syncthreads();
 }
@@ -296,19 +363,20 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   const int64_t gtid = (int64_t)blockIdx.x * NT + tid, gstride = (int64_t)gridDim.x * NT;
 
   // ---- phase 0: lengths, P, T -------------------------------------------------------
+  stamp(a, 0);
   for (int64_t i = gtid; i < N; i += gstride) {
     int32_t L = a.seq_lens[i];
     if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
     a.lens[i] = L;
+    a.vtmp[i] = L;
   }
   gsync();
-  const int64_t T = grid_scan(
-      N, [&](int64_t i) { return (int64_t)a.lens[i]; },
-      [&](int64_t i, int64_t ex) { a.P[i] = ex; }, a.cta_sums, sm_scan);
+  const int64_t T = scan_array(a.vtmp, a.P, N, a.cta_sums, sm_scan);
   if (lead && tid == 0) { a.P[N] = T; h->T = T; }
   gsync();
 
   // ---- phase 1: assignment -----------------------------------------------------------
+  stamp(a, 1);
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp;
@@ -338,14 +406,13 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   gsync();
 
   // ---- phase 2: per-layout group order and local token offsets ------------------------
+  stamp(a, 2);
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp, SP = L.sp;
     const int32_t* grp = a.grp[l];
     int32_t* perm = a.perm[l];
-    grid_partition(
-        N, D, [&](int64_t i) { return grp[i]; },
-        [&](int64_t i, int64_t pos) { perm[pos] = (int32_t)i; }, a.ghist, ps);
+    partition_array(grp, N, D, perm, a.ghist, ps);
     if (lead) {
       if (tid <= D) h->group_start[l][tid] = ps.bstart[tid];
       if (tid < D) h->group_count[l][tid] = ps.bstart[tid + 1] - ps.bstart[tid];
@@ -356,9 +423,9 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     for (int k = 0; k < SP; ++k) {
       int64_t* cum = a.cum[l] + (int64_t)k * (N + 1);
       int64_t* off = a.off[l] + (int64_t)k * N;
-      const int64_t tot = grid_scan(
-          N, [&](int64_t j) { return chunk_len(a.lens[perm[j]], SP, k); },
-          [&](int64_t j, int64_t ex) { cum[j] = ex; }, a.cta_sums, sm_scan);
+      for (int64_t j = gtid; j < N; j += gstride) a.vtmp[j] = chunk_len(a.lens[perm[j]], SP, k);
+      gsync();
+      const int64_t tot = scan_array(a.vtmp, cum, N, a.cta_sums, sm_scan);
       if (lead && tid == 0) cum[N] = tot;
       gsync();
       for (int64_t j = gtid; j < N; j += gstride) {
@@ -377,15 +444,14 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   }
 
   // ---- phase 3: pieces ----------------------------------------------------------------
+  stamp(a, 3);
   const LayoutDesc& S = a.lay[0];
   const LayoutDesc& Dl = a.lay[1];
   const int Sd = Dl.dp * Dl.sp;
-  const int64_t M = grid_scan(
-      N,
-      [&](int64_t i) {
-        return (int64_t)for_each_piece(a.lens[i], S.sp, Dl.sp, [](int, int, int64_t, int64_t) {});
-      },
-      [&](int64_t i, int64_t ex) { a.pbase[i] = ex; }, a.cta_sums, sm_scan);
+  for (int64_t i = gtid; i < N; i += gstride)
+    a.vtmp[i] = for_each_piece(a.lens[i], S.sp, Dl.sp, [](int, int, int64_t, int64_t) {});
+  gsync();
+  const int64_t M = scan_array(a.vtmp, a.pbase, N, a.cta_sums, sm_scan);
   if (lead && tid == 0) { a.pbase[N] = M; h->n_pieces = M; }
   gsync();
   for (int64_t i = gtid; i < N; i += gstride) {
@@ -396,33 +462,35 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
       a.pc_x[p] = (int32_t)x;
       a.pc_y[p] = (int32_t)y;
       a.pc_kk[p] = ks | (kd << 8) | (((ss0 + ks) * Sd + ds0 + kd) << 16);
+      a.ktmp[p] = (ss0 + ks) * Sd + ds0 + kd;
       ++p;
     });
   }
   gsync();
 
   // ---- phase 4: pieces by message key, message token offsets -------------------------
+  stamp(a, 4);
   const int K = S.dp * S.sp * Sd;
-  grid_partition(
-      M, K, [&](int64_t q) { return a.pc_kk[q] >> 16; },
-      [&](int64_t q, int64_t pos) {
-        a.ps_i[pos] = a.pc_i[q];
-        a.ps_x[pos] = a.pc_x[q];
-        a.ps_y[pos] = a.pc_y[q];
-        a.ps_kk[pos] = a.pc_kk[q];
-      },
-      a.ghist, ps);
+  partition_array(a.ktmp, M, K, a.ptmp, a.ghist, ps);
   __shared__ int64_t s_kstart[kMaxKeys + 1], s_ktok[kMaxKeys], s_kscan0[kMaxKeys];
   __shared__ int64_t s_rbase[kMaxWorld][kMaxShards], s_tbase[kMaxWorld][kMaxShards];
   if (tid <= K) s_kstart[tid] = ps.bstart[tid];
   gsync();
-  const int64_t Mtok = grid_scan(
-      M, [&](int64_t q) { return (int64_t)(a.ps_y[q] - a.ps_x[q]); },
-      [&](int64_t q, int64_t ex) { a.ps_scan[q] = ex; }, a.cta_sums, sm_scan);
+  for (int64_t pos = gtid; pos < M; pos += gstride) {
+    const int32_t q = a.ptmp[pos];
+    a.ps_i[pos] = a.pc_i[q];
+    a.ps_x[pos] = a.pc_x[q];
+    a.ps_y[pos] = a.pc_y[q];
+    a.ps_kk[pos] = a.pc_kk[q];
+    a.vtmp[pos] = a.pc_y[q] - a.pc_x[q];
+  }
+  gsync();
+  const int64_t Mtok = scan_array(a.vtmp, a.ps_scan, M, a.cta_sums, sm_scan);
   if (lead && tid == 0) a.ps_scan[M] = Mtok;
   gsync();
 
   // ---- phase 5: bases and message offsets ---------------------------------------------
+  stamp(a, 5);
   // Every CTA derives the <= 64-entry tables itself in shared memory (parallel loads of the
   // published scan, then one thread walks <= 8 x 8 entries in shared memory); CTA 0 also
   // publishes them in the header for the copy kernels and the host.
@@ -432,37 +500,69 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     s_ktok[tid] = a.ps_scan[s_kstart[tid + 1]] - s_kscan0[tid];
   }
   __syncthreads();
+  stamp(a, 8);
   __shared__ int64_t s_rec_begin[kMaxWorld + 1], s_tok_begin[kMaxWorld + 1];
   __shared__ int64_t s_msg_off[kMaxKeys], s_stage[kMaxShards];
-  if (tid == 0) {
-    int64_t rec = 0, tok = 0;
-    for (int r = 0; r < a.world; ++r) {
-      s_rec_begin[r] = rec;
-      s_tok_begin[r] = tok;
-      const int rr = r - S.rank0;
-      const bool in_src = rr >= 0 && rr < S.dp * S.sp * S.tp;
-      const int ss = in_src ? rr / S.tp : 0, ts = in_src ? rr % S.tp : 0;
-      for (int ds = 0; ds < Sd; ++ds) {
-        s_rbase[r][ds] = rec;
-        s_tbase[r][ds] = tok;
-        if (in_src && ts < nts) {
-          rec += s_kstart[ss * Sd + ds + 1] - s_kstart[ss * Sd + ds];
-          tok += s_ktok[ss * Sd + ds];
+  // warp 0, in parallel: record/token bases over the (rank r, dst shard ds) entries in rank
+  // order (two entries per lane, warp scans), and message byte offsets inside each source
+  // shard's stage buffer (one key per lane, prefix within the row)
+  __shared__ int64_t s_msgb[kMaxKeys];
+  if (tid < 32) {
+    const int lane = tid;
+    const int E = a.world * Sd;
+    int64_t cnt[2], tk[2];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int e = lane + 32 * hf;
+      cnt[hf] = 0;
+      tk[hf] = 0;
+      if (e < E) {
+        const int r = e / Sd, ds = e - (e / Sd) * Sd;
+        const int rr = r - S.rank0;
+        if (rr >= 0 && rr < S.dp * S.sp * S.tp && rr % S.tp < nts) {
+          const int key = (rr / S.tp) * Sd + ds;
+          cnt[hf] = s_kstart[key + 1] - s_kstart[key];
+          tk[hf] = s_ktok[key];
         }
       }
     }
-    s_rec_begin[a.world] = rec;
-    s_tok_begin[a.world] = tok;
-    for (int ss = 0; ss < S.dp * S.sp; ++ss) {
-      int64_t off = 0;
-      for (int ds = 0; ds < Sd; ++ds) {
-        s_msg_off[ss * Sd + ds] = off;
-        for (int f = 0; f < a.n_fields; ++f) off += (s_ktok[ss * Sd + ds] * a.Bf[f] + 15) & ~15LL;
+    int64_t carry_c = 0, carry_t = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      int64_t ic = cnt[hf], it = tk[hf];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t yc = __shfl_up_sync(kFull, ic, o), yt = __shfl_up_sync(kFull, it, o);
+        if (lane >= o) { ic += yc; it += yt; }
       }
-      s_stage[ss] = off;
+      const int e = lane + 32 * hf;
+      if (e < E) {
+        const int r = e / Sd, ds = e - (e / Sd) * Sd;
+        s_rbase[r][ds] = carry_c + ic - cnt[hf];
+        s_tbase[r][ds] = carry_t + it - tk[hf];
+        if (ds == 0) { s_rec_begin[r] = s_rbase[r][0]; s_tok_begin[r] = s_tbase[r][0]; }
+      }
+      carry_c += __shfl_sync(kFull, ic, 31);
+      carry_t += __shfl_sync(kFull, it, 31);
+    }
+    if (lane == 0) { s_rec_begin[a.world] = carry_c; s_tok_begin[a.world] = carry_t; }
+    // message bytes per key, then the offset of each message inside its source shard's buffer
+    for (int key = lane; key < K; key += 32) {
+      int64_t mb = 0;
+      for (int f = 0; f < a.n_fields; ++f) mb += (s_ktok[key] * a.Bf[f] + 15) & ~15LL;
+      s_msgb[key] = mb;
+    }
+    __syncwarp();
+    for (int key = lane; key < K; key += 32) {
+      const int ss = key / Sd, ds = key - ss * Sd;
+      int64_t off = 0;
+      for (int q = 0; q < ds; ++q) off += s_msgb[ss * Sd + q];
+      s_msg_off[key] = off;
+      if (ds == Sd - 1) s_stage[ss] = off + s_msgb[key];
     }
   }
   __syncthreads();
+  stamp(a, 9);
   if (lead) {
     if (tid <= K) h->key_piece_start[tid] = s_kstart[tid];
     if (tid < K) {
@@ -487,6 +587,7 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   }
 
   // ---- phase 6: records ---------------------------------------------------------------
+  stamp(a, 6);
   const int64_t nrec = M * nts;
   for (int64_t idx = gtid; idx < nrec; idx += gstride) {
     const int64_t q = idx / nts;
@@ -510,6 +611,7 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     a.rec.msg_tok[j] = msg_tok;
     a.rec.tok_prefix[j] = s_tbase[s][ds] + msg_tok;
   }
+  stamp(a, 7);
 }
 
 // Destination metadata of dst shard (g, k): cu_seqlens (int32), seq_ids (int64), tok_start.
@@ -534,14 +636,23 @@ __global__ void local_meta_kernel(const __grid_constant__ PlanArgs a, int g, int
 
 }  // namespace
 
+// Grid size: one CTA per 4096 items (sequences or pieces), at most what can be co-resident.
+// EARL_PLAN_GRID=<g> forces g (tests use it to check that the plan does not depend on G).
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem) {
   static int per_sm = -1;
+  static int forced = -2;
   if (per_sm < 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, planner_kernel, NT, 64 * 1024);
+    cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, planner_kernel, NT, 64 * 1024) !=
+        cudaSuccess)
+      per_sm = 1;
+    (void)cudaGetLastError();
     if (per_sm < 1) per_sm = 1;
+    const char* e = getenv("EARL_PLAN_GRID");
+    forced = e ? atoi(e) : -1;
   }
   const int64_t work = n_seqs > max_pieces ? n_seqs : max_pieces;
-  int64_t g = (work + 4095) / 4096;
+  int64_t g = forced > 0 ? forced : (work + 4095) / 4096;
   const int64_t cap = (int64_t)sm_count * per_sm;
   if (g > cap) g = cap;
   if (g > kMaxPlanGrid) g = kMaxPlanGrid;

@@ -62,3 +62,38 @@ def test_argument_validation_needs_no_gpu():
     assert L.earl_comm_create(0, 9, 0, 0, C.byref(C.c_void_p())) == 8  # UNSUPPORTED
     assert b"world 9" in L.earl_last_error()
     assert L.earl_comm_create(3, 2, 0, 0, C.byref(C.c_void_p())) == 1
+
+
+def _build_c_smoke(tmp_path):
+    build.build()
+    exe = str(tmp_path / "abi_smoke")
+    libdir = os.path.dirname(earl.LIB_PATH)
+    cmd = ["gcc", "-O1", "-o", exe, os.path.join(ROOT, "tests", "c", "abi_smoke.c"),
+           "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           "-L", libdir, "-learl_dispatch", "-Wl,-rpath," + libdir,
+           "-L", "/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_program_links_and_validates_without_gpu(tmp_path):
+    """A plain C program compiles against include/earl_dispatch.h, links libearl_dispatch.so
+    and gets the documented status codes for invalid arguments (no GPU involved)."""
+    exe = _build_c_smoke(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "no-GPU checks passed" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_program_dispatches_on_gpu(tmp_path):
+    """The same C program plans and executes BASELINE configs[0] through the C ABI alone and
+    checks bytes, cu_seqlens, stats and the exported plan against tests/golden/c1_tiny.json."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    exe = _build_c_smoke(tmp_path)
+    r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "GPU dispatch checks passed" in r.stdout

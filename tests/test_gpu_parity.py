@@ -240,3 +240,50 @@ def test_plan_outlives_comm_handle():
     assert recv[0][0].view(torch.int32).tolist() == [0, 1, 2, 3]
     assert recv[1][0].view(torch.int32).tolist() == [4, 5, 6, 7]
     p.destroy()
+
+
+_GRID_SCRIPT = r"""
+import hashlib, sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from oracle import earl_oracle as O
+from paper_2510_05943_b200 import workloads as W
+from paper_2510_05943_b200.dispatch import EmulatedDispatch
+rng = np.random.default_rng(21)
+n = 20000
+lens = rng.integers(0, 60, size=n).tolist()
+out = []
+for dst in (W.layout(dp=2, sp=2, tp=2, assign="contig"),
+            W.layout(dp=4, assign="lpt") if False else W.layout(dp=4, sp=2, assign="explicit",
+                     group_of_seq=rng.integers(0, 4, size=n).astype(np.int32))):
+    ed = EmulatedDispatch(8)
+    fields = [("m", 1, 1, "x"), ("a", 4, 1, "x")]
+    p = ed.plan(W.rollout_layout(n, 8), dst, lens, fields)
+    segs = p.export()
+    h = hashlib.blake2b(np.asarray(segs, dtype=np.int64).tobytes(), digest_size=16).hexdigest()
+    st = p.stats()
+    out.append(h + ":" + str(st["records"]) + ":" + str(st["total"]))
+print("|".join(out))
+"""
+
+
+def test_plan_independent_of_planner_grid():
+    """The cooperative planner's result does not depend on its grid size: G = 1, 3, 7 and the
+    automatic choice give byte-identical canonical plans (subprocesses: EARL_PLAN_GRID is read
+    once per process)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = _GRID_SCRIPT.format(root=root)
+    outs = {}
+    for g in ("1", "3", "7", ""):
+        env = dict(os.environ)
+        if g:
+            env["EARL_PLAN_GRID"] = g
+        else:
+            env.pop("EARL_PLAN_GRID", None)
+        r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, env=env,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[g] = r.stdout.strip().splitlines()[-1]
+    assert len(set(outs.values())) == 1, outs
