@@ -50,6 +50,7 @@ ERR_CAPACITY = "CAPACITY"
 ERR_UNSUPPORTED = "UNSUPPORTED"
 
 LPT_MAX_SEQS = 8192       # reading c4 / §8(b): LPT limited to N <= 8192
+SP_SPLITS = ("block", "zigzag", "flat", "threshold")  # readings c7, n1-n3
 MAX_WORLD = 8             # reading c21: one box, W <= 8
 INT32_MAX = 2**31 - 1
 
@@ -94,6 +95,11 @@ def validate_layout(lay, n_seqs, world):
             raise OracleError(ERR_LAYOUT, f"{key} < 1")
     if lay["rank0"] < 0 or lay["rank0"] + n_ranks(lay) > world:
         raise OracleError(ERR_LAYOUT, "layout ranks outside the comm")
+    split = lay.get("sp_split", "block")
+    if split not in SP_SPLITS:
+        raise OracleError(ERR_INVALID_ARGUMENT, f"unknown sp_split {split!r}")
+    if split == "threshold" and int(lay.get("sp_min_len", 0)) < 0:
+        raise OracleError(ERR_INVALID_ARGUMENT, "sp_min_len < 0")
     a = lay["assign"]
     if a == "given_counts":
         c = lay["counts"]
@@ -199,36 +205,94 @@ def sp_chunk(L, SP, k):
     return k * q + min(k, r), (k + 1) * q + min(k + 1, r)
 
 
+def group_members(seq_lens, g_of, D):
+    """Sequences of every group in ascending global index (reading c5)."""
+    members = {g: [] for g in range(D)}
+    for i in range(len(seq_lens)):
+        members[g_of[i]].append(i)
+    return members
+
+
+def seq_chunks(lay, seq_lens, g_of):
+    """Step 4, generalised SP split.  For every sequence i, the ordered list of its virtual
+    chunks (c, lo, hi, k): token range [lo, hi) of sequence i, held by SP rank k of its group.
+    The chunks of a sequence are consecutive and cover [0, L_i).
+
+      block     (reading c7)  c = k = 0..SP-1, chunk k = sp_chunk(L, SP, k)
+      zigzag    (reading n1)  c = 0..2SP-1, chunk c = sp_chunk(L, 2SP, c), held by
+                              k = c if c < SP else 2SP-1-c  (rank k holds chunks k and 2SP-1-k)
+      flat      (reading n2)  the group's sequences concatenated in ascending i form a stream of
+                              S_g tokens; SP rank k holds stream block sp_chunk(S_g, SP, k);
+                              chunk k of sequence i is that block's intersection with i
+      threshold (reading n3)  L >= sp_min_len: block; otherwise the whole sequence goes to SP
+                              rank (position of i in its group) mod SP: chunk c = [0,0) before
+                              that rank, [0,L) at it, [L,L) after it
+    """
+    SP = lay["sp"]
+    split = lay.get("sp_split", "block")
+    thresh = int(lay.get("sp_min_len", 0))
+    out = {}
+    for g, members in group_members(seq_lens, g_of, lay["dp"]).items():
+        if split == "flat":
+            S = sum(int(seq_lens[i]) for i in members)
+            blocks = [sp_chunk(S, SP, k) for k in range(SP)]
+            pos = 0
+            for i in members:
+                L = int(seq_lens[i])
+                out[i] = [(k, min(max(a - pos, 0), L), min(max(b - pos, 0), L), k)
+                          for k, (a, b) in enumerate(blocks)]
+                pos += L
+            continue
+        for p, i in enumerate(members):
+            L = int(seq_lens[i])
+            if split == "zigzag":
+                out[i] = [(c,) + sp_chunk(L, 2 * SP, c) + (c if c < SP else 2 * SP - 1 - c,)
+                          for c in range(2 * SP)]
+            elif split == "threshold" and L < thresh:
+                owner = p % SP
+                out[i] = [(c, 0 if c <= owner else L, 0 if c < owner else L, c) for c in range(SP)]
+            else:
+                out[i] = [(k,) + sp_chunk(L, SP, k) + (k,) for k in range(SP)]
+    return out
+
+
 # ---------------------------------------------------------------------------
 # step 5: holdings
 # ---------------------------------------------------------------------------
 
 def holdings(lay, seq_lens, g_of):
-    """Step 5: for every rank of the layout, its ordered list of (i, a, b) chunks (ascending i,
-    reading c5) plus cu_seqlens / seq_ids / tok_start and each chunk's local token offset.
+    """Step 5: every rank (g, k, t) of the layout holds, for each sequence of group g in
+    ascending i (reading c5), the chunks of that sequence SP rank k holds, in chunk order --
+    i.e. its tokens in ascending position.  Also cu_seqlens (tokens held per sequence, scanned),
+    seq_ids, tok_start (first token of the first held chunk) and each chunk's local offset.
 
-    Returns dict rank -> {"chunks": [(i, a, b)], "local_off": {i: offset}, "cu_seqlens": [...],
-    "seq_ids": [...], "tok_start": [...], "n_tokens": int}.
+    Returns dict rank -> {"chunks": [(i, c, lo, hi)], "local_off": {(i, c): offset},
+    "cu_seqlens": [...], "seq_ids": [...], "tok_start": [...], "n_tokens": int}.
     """
+    chunks_of = seq_chunks(lay, seq_lens, g_of)
     out = {}
-    for g in range(lay["dp"]):
-        members = [i for i in range(len(seq_lens)) if g_of[i] == g]
+    for g, members in group_members(seq_lens, g_of, lay["dp"]).items():
         for k in range(lay["sp"]):
-            chunks = []
+            held = []
             local_off = {}
             cu = [0]
+            tok_start = []
             for i in members:
-                a, b = sp_chunk(seq_lens[i], lay["sp"], k)
-                local_off[i] = cu[-1]
-                chunks.append((i, a, b))
-                cu.append(cu[-1] + (b - a))
+                mine = [(c, lo, hi) for (c, lo, hi, kk) in chunks_of[i] if kk == k]
+                tok_start.append(mine[0][1])
+                total = cu[-1]
+                for (c, lo, hi) in mine:
+                    local_off[(i, c)] = total
+                    held.append((i, c, lo, hi))
+                    total += hi - lo
+                cu.append(total)
             for t in range(lay["tp"]):
                 out[rank_of(lay, g, k, t)] = {
-                    "chunks": chunks,
+                    "chunks": held,
                     "local_off": local_off,
                     "cu_seqlens": list(cu),
                     "seq_ids": list(members),
-                    "tok_start": [a for (_, a, _) in chunks],
+                    "tok_start": list(tok_start),
                     "n_tokens": cu[-1],
                 }
     return out
@@ -252,7 +316,7 @@ def rank_arrays_from_global(lay, seq_lens, g_of, global_fields, fields):
     for r, h in hold.items():
         per_field = []
         for f, arr in enumerate(global_fields):
-            parts = [arr[(P[i] + a) * Bf[f]:(P[i] + b) * Bf[f]] for (i, a, b) in h["chunks"]]
+            parts = [arr[(P[i] + a) * Bf[f]:(P[i] + b) * Bf[f]] for (i, _, a, b) in h["chunks"]]
             per_field.append(np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8))
         out[r] = per_field
     return out
@@ -278,12 +342,12 @@ def route(src, dst, seq_lens, world):
     gd = assign_groups(dst, seq_lens)
     hs = holdings(src, seq_lens, gs)
     hd = holdings(dst, seq_lens, gd)
+    cs_of = seq_chunks(src, seq_lens, gs)
+    cd_of = seq_chunks(dst, seq_lens, gd)
     segs = []
     for i in range(N):
-        for kd in range(dst["sp"]):
-            a_d, b_d = sp_chunk(seq_lens[i], dst["sp"], kd)
-            for ks in range(src["sp"]):
-                a_s, b_s = sp_chunk(seq_lens[i], src["sp"], ks)
+        for (cd, a_d, b_d, kd) in cd_of[i]:
+            for (cs, a_s, b_s, ks) in cs_of[i]:
                 x, y = max(a_s, a_d), min(b_s, b_d)
                 if x >= y:
                     continue
@@ -291,8 +355,8 @@ def route(src, dst, seq_lens, world):
                     ts = td % src["tp"]
                     s = rank_of(src, gs[i], ks, ts)
                     d = rank_of(dst, gd[i], kd, td)
-                    src_off = hs[s]["local_off"][i] + (x - a_s)
-                    dst_off = hd[d]["local_off"][i] + (x - a_d)
+                    src_off = hs[s]["local_off"][(i, cs)] + (x - a_s)
+                    dst_off = hd[d]["local_off"][(i, cd)] + (x - a_d)
                     segs.append((s, d, i, x, y, src_off, dst_off))
     segs.sort(key=lambda r: (r[0], r[1], r[2], r[3]))
     return segs
@@ -381,20 +445,20 @@ def dispatch(src, dst, seq_lens, src_arrays, fields, world):
 
 def brute_force(src, dst, seq_lens, src_arrays, fields, world):
     """Step 9: rebuild the global per-field arrays from the src ranks (replica ts = 0, chunks in
-    k order), then cut every dst rank's arrays straight out of them."""
+    position order), then cut every dst rank's arrays straight out of them."""
     seq_lens = [int(x) for x in seq_lens]
     Bf = field_bytes(fields)
     gs = assign_groups(src, seq_lens)
     gd = assign_groups(dst, seq_lens)
     hs = holdings(src, seq_lens, gs)
+    cs_of = seq_chunks(src, seq_lens, gs)
     glob = []
     for f in range(len(fields)):
         parts = []
         for i in range(len(seq_lens)):
-            for k in range(src["sp"]):
+            for (c, a, b, k) in cs_of[i]:
                 r = rank_of(src, gs[i], k, 0)
-                a, b = sp_chunk(seq_lens[i], src["sp"], k)
-                o = hs[r]["local_off"][i]
+                o = hs[r]["local_off"][(i, c)]
                 parts.append(src_arrays[r][f][o * Bf[f]:(o + b - a) * Bf[f]])
         glob.append(np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8))
     return rank_arrays_from_global(dst, seq_lens, gd, glob, fields), glob

@@ -140,10 +140,11 @@ def c4_lengths(seed: int = 0) -> np.ndarray:
 # include/earl_dispatch.h and implemented separately by each side)
 # ---------------------------------------------------------------------------
 
-def layout(rank0=0, dp=1, sp=1, tp=1, assign="contig", counts=None, group_of_seq=None):
+def layout(rank0=0, dp=1, sp=1, tp=1, assign="contig", counts=None, group_of_seq=None,
+           sp_split="block", sp_min_len=0):
     return {
         "rank0": int(rank0), "dp": int(dp), "sp": int(sp), "tp": int(tp),
-        "assign": assign,
+        "assign": assign, "sp_split": sp_split, "sp_min_len": int(sp_min_len),
         "counts": None if counts is None else [int(c) for c in counts],
         "group_of_seq": None if group_of_seq is None else np.asarray(group_of_seq, dtype=np.int32),
     }
