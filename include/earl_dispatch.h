@@ -59,7 +59,7 @@
 extern "C" {
 #endif
 
-#define EARL_ABI_VERSION 1
+#define EARL_ABI_VERSION 2
 #define EARL_MAX_WORLD 8        /* reading c21: one box, W <= 8 */
 #define EARL_MAX_FIELDS 16
 #define EARL_HANDLE_BYTES 128   /* size of the exported window handle */
@@ -87,17 +87,30 @@ typedef enum {
   EARL_ASSIGN_EXPLICIT = 3      /* g(i) = group_of_seq[i]                                    */
 } earl_assign_t;
 
+/* How an SP group splits its sequences' tokens (readings c7, n1-n3). */
+typedef enum {
+  EARL_SP_BLOCK = 0,     /* SP rank k holds BLOCK chunk k = [k*q+min(k,r), (k+1)*q+min(k+1,r)),
+                            q = L/sp, r = L%sp, of every sequence (reading c7)               */
+  EARL_SP_ZIGZAG = 1,    /* 2*sp BLOCK chunks; rank k holds chunks k and 2*sp-1-k (ring-attention
+                            / context-parallel load balance, reading n1)                      */
+  EARL_SP_FLAT = 2,      /* the group's sequences concatenated (ascending i) into one stream,
+                            BLOCK-split over the sp ranks, no padding (Ulysses, reading n2)   */
+  EARL_SP_THRESHOLD = 3  /* sequences with L >= sp_min_len are BLOCK-split; shorter ones go whole
+                            to SP rank (position in group) mod sp (reading n3)                */
+} earl_sp_split_t;
+
 /* A parallel layout (reading c1/c3): ranks rank0 .. rank0+dp*sp*tp-1 of the comm, with
  * rank(g,k,t) = rank0 + (g*sp + k)*tp + t  (TP fastest, then SP, then DP).
  * DP group g holds the sequences assigned to it in ascending global index (reading c5);
- * SP rank k holds BLOCK chunk k = [k*q+min(k,r), (k+1)*q+min(k+1,r)) with q = L/sp,
- * r = L%sp of every such sequence (reading c7); every TP rank of (g,k) holds a full copy
- * (reading c2).  When the source has several TP replicas, dst replica td is fed by source
- * replica td mod tp_src (reading c9). */
+ * its SP rank k holds, of every such sequence, the tokens the sp_split rule gives it, in
+ * ascending position; every TP rank of (g,k) holds a full copy (reading c2).  When the source
+ * has several TP replicas, dst replica td is fed by source replica td mod tp_src (reading c9). */
 typedef struct {
   int32_t rank0, dp, sp, tp;
   int32_t assign;               /* earl_assign_t */
-  int32_t sp_split;             /* 0 = BLOCK (the only value in scope) */
+  int32_t sp_split;             /* earl_sp_split_t */
+  int32_t sp_min_len;           /* EARL_SP_THRESHOLD: shortest sequence that is split (>= 0) */
+  int32_t reserved;             /* 0 */
   const int64_t* counts;        /* HOST [dp], GIVEN_COUNTS only */
   const int32_t* group_of_seq;  /* DEVICE [N], EXPLICIT only */
 } earl_layout_t;
@@ -172,7 +185,8 @@ EARL_API earl_status_t earl_plan_local_sizes(earl_plan_t plan, int32_t rank, int
                                     int64_t* n_local_tokens);
 /* Destination metadata of rank `rank` written to DEVICE buffers on `stream`:
  * cu_seqlens int32 [n_local_seqs+1], seq_ids int64 [n_local_seqs] (global index),
- * tok_start int32 [n_local_seqs] (first token of the chunk inside its sequence).
+ * tok_start int32 [n_local_seqs] (first token this rank holds of the sequence, i.e. the start
+ * of its first chunk; for ZIGZAG the second chunk starts at L - (its length)).
  * Any pointer may be NULL to skip it. */
 EARL_API earl_status_t earl_plan_local_meta(earl_plan_t plan, int32_t rank, int32_t* cu_seqlens,
                                    int64_t* seq_ids, int32_t* tok_start, void* stream);

@@ -267,7 +267,10 @@ earl_status_t check_layout(const earl_layout_t* L, const char* which, int64_t N,
   if (L->rank0 < 0 || L->rank0 + nr > world)
     return fail(EARL_ERR_LAYOUT, "%s layout: ranks [%d, %lld) outside the comm of %d", which,
                 L->rank0, (long long)(L->rank0 + nr), world);
-  if (L->sp_split != 0) return fail(EARL_ERR_UNSUPPORTED, "%s layout: only BLOCK SP split", which);
+  if (L->sp_split < EARL_SP_BLOCK || L->sp_split > EARL_SP_THRESHOLD)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "%s layout: unknown sp_split %d", which, L->sp_split);
+  if (L->sp_min_len < 0)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "%s layout: sp_min_len < 0", which);
   switch (L->assign) {
     case EARL_ASSIGN_GIVEN_COUNTS: {
       if (!L->counts) return fail(EARL_ERR_LAYOUT, "%s layout: GIVEN_COUNTS without counts", which);
@@ -299,6 +302,7 @@ earl_status_t check_layout(const earl_layout_t* L, const char* which, int64_t N,
 LayoutDesc to_desc(const earl_layout_t& L) {
   LayoutDesc d{};
   d.rank0 = L.rank0; d.dp = L.dp; d.sp = L.sp; d.tp = L.tp; d.assign = L.assign;
+  d.split = L.sp_split; d.min_len = L.sp_min_len;
   d.group_of_seq = L.group_of_seq;
   d.count_start[0] = 0;
   for (int g = 0; g < L.dp; ++g)
@@ -397,7 +401,9 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   for (int f = 0; f < n_fields; ++f) a.Bf[f] = fields[f].bytes_per_elem * fields[f].elems_per_token;
   a.seq_lens = seq_lens;
   const int64_t N = n_seqs;
-  const int64_t max_pieces = N * (src->sp + dst->sp - 1);
+  const int64_t cs = src->sp_split == EARL_SP_ZIGZAG ? 2 * src->sp : src->sp;
+  const int64_t cd = dst->sp_split == EARL_SP_ZIGZAG ? 2 * dst->sp : dst->sp;
+  const int64_t max_pieces = N * (cs + cd - 1);
   const int64_t nts = src->tp < dst->tp ? src->tp : dst->tp;
   const int64_t max_records = max_pieces * nts;
   a.max_pieces = max_pieces;
@@ -410,6 +416,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   total += sz((int64_t)src->sp * N, 8) + sz((int64_t)dst->sp * N, 8);
   total += sz((int64_t)src->sp * (N + 1), 8) + sz((int64_t)dst->sp * (N + 1), 8);
   total += sz(N + 1, 8);
+  total += 2 * sz(N, 8) + 2 * sz(N, 4);
   total += 8 * sz(max_pieces, 4) + sz(max_pieces + 1, 8);
   total += sz(kMaxPlanGrid, 8) + sz((int64_t)kMaxPlanGrid * kMaxKeys, 4);
   const int64_t nscr = (N > max_pieces ? N : max_pieces) + 1;
@@ -435,6 +442,10 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   a.cum[0] = carve<int64_t>(q, (int64_t)src->sp * (N + 1));
   a.cum[1] = carve<int64_t>(q, (int64_t)dst->sp * (N + 1));
   a.pbase = carve<int64_t>(q, N + 1);
+  a.gpos[0] = carve<int64_t>(q, N);
+  a.gpos[1] = carve<int64_t>(q, N);
+  a.pos[0] = carve<int32_t>(q, N);
+  a.pos[1] = carve<int32_t>(q, N);
   a.pc_i = carve<int32_t>(q, max_pieces);
   a.pc_x = carve<int32_t>(q, max_pieces);
   a.pc_y = carve<int32_t>(q, max_pieces);

@@ -19,6 +19,8 @@ constexpr int kMaxPlanGrid = 256;           // planner CTAs (cooperative grid) a
 // Layout as the device sees it.  shard = g*sp + k ; rank = rank0 + shard*tp + t.
 struct LayoutDesc {
   int32_t rank0, dp, sp, tp, assign;
+  int32_t split;            // earl_sp_split_t
+  int32_t min_len;          // EARL_SP_THRESHOLD
   int32_t pad_;
   int64_t count_start[kMaxShards + 1];  // GIVEN_COUNTS: prefix of counts
   const int32_t* group_of_seq;          // EXPLICIT
@@ -36,6 +38,7 @@ struct PlanHeader {
   int64_t group_count[2][kMaxShards];
   int64_t group_start[2][kMaxShards + 1];
   int64_t shard_tokens[2][kMaxShards];      // tokens held per shard (g*sp+k) of each layout
+  int64_t group_tokens[2][kMaxShards];      // tokens of every DP group (FLAT stream length)
   int64_t key_pieces[kMaxKeys];
   int64_t key_piece_start[kMaxKeys + 1];
   int64_t key_tokens[kMaxKeys];             // tokens of message key (ss, ds)
@@ -76,7 +79,9 @@ struct PlanArgs {
   int32_t* grp[2];           // [N]
   int32_t* perm[2];          // [N] sorted position -> i
   int64_t* off[2];           // [sp][N] local token offset of chunk k of sequence i
-  int64_t* cum[2];           // [sp][N+1] scan of chunk lengths in sorted order
+  int64_t* cum[2];           // [sp][N+1] scan of held lengths in sorted order
+  int64_t* gpos[2];          // [N] FLAT: offset of sequence i in its group's token stream
+  int32_t* pos[2];           // [N] THRESHOLD: position of sequence i in its group
   int64_t* pbase;            // [N+1] piece base per sequence
   // pieces (unsorted, then sorted by key)
   int32_t* pc_i; int32_t* pc_x; int32_t* pc_y; int32_t* pc_kk;  // kk = ks | kd<<8 | key<<16

@@ -250,19 +250,86 @@ __device__ __noinline__ void partition_array(const int32_t* keys, int64_t n, int
       [&](int64_t i, int64_t pos) { perm_out[pos] = (int32_t)i; }, ghist, ps);
 }
 
-// Two-pointer intersection of the BLOCK partitions of [0, L) into sps and spd chunks:
-// calls f(ks, kd, x, y) for every non-empty overlap in increasing x.
+// 64-bit BLOCK split (FLAT splits a whole group's token stream, which may exceed 2^32).
+__device__ __forceinline__ int64_t block_lo64(int64_t S, int sp, int k) {
+  const int64_t q = S / sp, r = S - q * sp;
+  return (int64_t)k * q + ((int64_t)k < r ? (int64_t)k : r);
+}
+
+// The virtual chunks of one sequence under one layout's SP split (readings c7, n1-n3).  They are
+// consecutive intervals covering [0, L) in chunk order; chunk c is held by SP rank owner(c).
+struct Chunker {
+  int split, sp, C;      // C virtual chunks: 2*sp for ZIGZAG, sp otherwise
+  int64_t L;
+  int64_t gpos, S;       // FLAT: the sequence's offset in its group stream, the stream length
+  int owner_short;       // THRESHOLD: the SP rank holding a short sequence whole, else -1
+
+  __device__ __forceinline__ int owner(int c) const {
+    return (split == EARL_SP_ZIGZAG && c >= sp) ? 2 * sp - 1 - c : c;
+  }
+  __device__ __forceinline__ void bounds(int c, int64_t& lo, int64_t& hi) const {
+    if (split == EARL_SP_ZIGZAG) {
+      lo = chunk_lo(L, 2 * sp, c);
+      hi = lo + chunk_len(L, 2 * sp, c);
+    } else if (split == EARL_SP_FLAT) {
+      const int64_t a = block_lo64(S, sp, c) - gpos, b = block_lo64(S, sp, c + 1) - gpos;
+      lo = a < 0 ? 0 : (a > L ? L : a);
+      hi = b < 0 ? 0 : (b > L ? L : b);
+    } else if (owner_short >= 0) {
+      lo = c <= owner_short ? 0 : L;
+      hi = c < owner_short ? 0 : L;
+    } else {
+      lo = chunk_lo(L, sp, c);
+      hi = lo + chunk_len(L, sp, c);
+    }
+  }
+  // tokens SP rank k holds of this sequence
+  __device__ __forceinline__ int64_t held(int k) const {
+    int64_t lo, hi;
+    bounds(k, lo, hi);
+    int64_t n = hi - lo;
+    if (split == EARL_SP_ZIGZAG) {
+      bounds(2 * sp - 1 - k, lo, hi);
+      n += hi - lo;
+    }
+    return n;
+  }
+};
+
+__device__ __forceinline__ Chunker make_chunker(const PlanArgs& a, int l, int64_t i,
+                                                const int64_t* group_tokens) {
+  const LayoutDesc& D = a.lay[l];
+  Chunker c;
+  c.split = D.split;
+  c.sp = D.sp;
+  c.C = D.split == EARL_SP_ZIGZAG ? 2 * D.sp : D.sp;
+  c.L = a.lens[i];
+  c.gpos = 0;
+  c.S = 0;
+  c.owner_short = -1;
+  if (D.split == EARL_SP_FLAT) {
+    c.gpos = a.gpos[l][i];
+    c.S = group_tokens[a.grp[l][i]];
+  } else if (D.split == EARL_SP_THRESHOLD && c.L < D.min_len) {
+    c.owner_short = a.pos[l][i] % D.sp;
+  }
+  return c;
+}
+
+// Two-pointer intersection of two chunkings of [0, L): calls f(cs, cd, x, y) for every
+// non-empty overlap in increasing x.
 template <class F>
-__device__ __forceinline__ int for_each_piece(int64_t L, int sps, int spd, F f) {
-  int ks = 0, kd = 0, cnt = 0;
-  while (ks < sps && kd < spd) {
-    const int64_t as = chunk_lo(L, sps, ks), bs = as + chunk_len(L, sps, ks);
-    const int64_t ad = chunk_lo(L, spd, kd), bd = ad + chunk_len(L, spd, kd);
+__device__ __forceinline__ int for_each_piece(const Chunker& cs, const Chunker& cd, F f) {
+  int p = 0, q = 0, cnt = 0;
+  while (p < cs.C && q < cd.C) {
+    int64_t as, bs, ad, bd;
+    cs.bounds(p, as, bs);
+    cd.bounds(q, ad, bd);
     const int64_t x = as > ad ? as : ad, y = bs < bd ? bs : bd;
-    if (x < y) { f(ks, kd, x, y); ++cnt; }
-    if (bs < bd) ++ks;
-    else if (bd < bs) ++kd;
-    else { ++ks; ++kd; }
+    if (x < y) { f(p, q, x, y); ++cnt; }
+    if (bs < bd) ++p;
+    else if (bd < bs) ++q;
+    else { ++p; ++q; }
   }
   return cnt;
 }
@@ -407,6 +474,7 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
 
   // ---- phase 2: per-layout group order and local token offsets ------------------------
   stamp(a, 2);
+  __shared__ int64_t s_gtok[2][kMaxShards];
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp, SP = L.sp;
@@ -420,10 +488,33 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     __shared__ int64_t s_gstart[kMaxShards + 1];
     if (tid <= D) s_gstart[tid] = ps.bstart[tid];
     gsync();
+    if (L.split == EARL_SP_FLAT || L.split == EARL_SP_THRESHOLD) {
+      // position of every sequence in its group, and its offset in the group's token stream
+      int64_t* cum0 = a.cum[l];
+      for (int64_t j = gtid; j < N; j += gstride) {
+        const int i = perm[j];
+        a.pos[l][i] = (int32_t)(j - s_gstart[grp[i]]);
+        a.vtmp[j] = a.lens[i];
+      }
+      gsync();
+      const int64_t tot = scan_array(a.vtmp, cum0, N, a.cta_sums, sm_scan);
+      if (lead && tid == 0) cum0[N] = tot;
+      gsync();
+      for (int64_t j = gtid; j < N; j += gstride) {
+        const int i = perm[j];
+        a.gpos[l][i] = cum0[j] - cum0[s_gstart[grp[i]]];
+      }
+      if (tid < D) s_gtok[l][tid] = cum0[s_gstart[tid + 1]] - cum0[s_gstart[tid]];
+      gsync();
+    } else if (tid < D) {
+      s_gtok[l][tid] = 0;
+    }
+    if (lead && tid < D) h->group_tokens[l][tid] = s_gtok[l][tid];
     for (int k = 0; k < SP; ++k) {
       int64_t* cum = a.cum[l] + (int64_t)k * (N + 1);
       int64_t* off = a.off[l] + (int64_t)k * N;
-      for (int64_t j = gtid; j < N; j += gstride) a.vtmp[j] = chunk_len(a.lens[perm[j]], SP, k);
+      for (int64_t j = gtid; j < N; j += gstride)
+        a.vtmp[j] = make_chunker(a, l, perm[j], s_gtok[l]).held(k);
       gsync();
       const int64_t tot = scan_array(a.vtmp, cum, N, a.cta_sums, sm_scan);
       if (lead && tid == 0) cum[N] = tot;
@@ -437,8 +528,8 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
         h->shard_tokens[l][tid * SP + k] = st;
         if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid * SP + k);
       }
-      // the next grid_scan / phase begins with a barrier-free read of lens/perm only; off and
-      // shard_tokens are consumed after later barriers
+      // the next scan begins with a barrier-free read of lens/perm only; off and shard_tokens
+      // are consumed after later barriers
     }
     gsync();
   }
@@ -449,7 +540,8 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   const LayoutDesc& Dl = a.lay[1];
   const int Sd = Dl.dp * Dl.sp;
   for (int64_t i = gtid; i < N; i += gstride)
-    a.vtmp[i] = for_each_piece(a.lens[i], S.sp, Dl.sp, [](int, int, int64_t, int64_t) {});
+    a.vtmp[i] = for_each_piece(make_chunker(a, 0, i, s_gtok[0]), make_chunker(a, 1, i, s_gtok[1]),
+                               [](int, int, int64_t, int64_t) {});
   gsync();
   const int64_t M = scan_array(a.vtmp, a.pbase, N, a.cta_sums, sm_scan);
   if (lead && tid == 0) { a.pbase[N] = M; h->n_pieces = M; }
@@ -457,12 +549,14 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   for (int64_t i = gtid; i < N; i += gstride) {
     int64_t p = a.pbase[i];
     const int ss0 = a.grp[0][i] * S.sp, ds0 = a.grp[1][i] * Dl.sp;
-    for_each_piece(a.lens[i], S.sp, Dl.sp, [&](int ks, int kd, int64_t x, int64_t y) {
+    const Chunker ch_s = make_chunker(a, 0, i, s_gtok[0]), ch_d = make_chunker(a, 1, i, s_gtok[1]);
+    for_each_piece(ch_s, ch_d, [&](int cs, int cd, int64_t x, int64_t y) {
+      const int key = (ss0 + ch_s.owner(cs)) * Sd + ds0 + ch_d.owner(cd);
       a.pc_i[p] = (int32_t)i;
       a.pc_x[p] = (int32_t)x;
       a.pc_y[p] = (int32_t)y;
-      a.pc_kk[p] = ks | (kd << 8) | (((ss0 + ks) * Sd + ds0 + kd) << 16);
-      a.ktmp[p] = (ss0 + ks) * Sd + ds0 + kd;
+      a.pc_kk[p] = cs | (cd << 8) | (key << 16);
+      a.ktmp[p] = key;
       ++p;
     });
   }
@@ -600,14 +694,26 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     const int64_t j = s_rbase[s][ds] + rho;
     const int i = a.ps_i[q];
     const int64_t x = a.ps_x[q], y = a.ps_y[q];
-    const int64_t L = a.lens[i];
     const int64_t msg_tok = a.ps_scan[q] - s_kscan0[key];
     a.rec.seq[j] = i;
     a.rec.x[j] = (int32_t)x;
     a.rec.n[j] = (int32_t)(y - x);
     a.rec.code[j] = (uint32_t)s | ((uint32_t)ss << 8) | ((uint32_t)ds << 16) | ((uint32_t)ts << 24);
-    a.rec.src_tok[j] = a.off[0][(int64_t)ks * N + i] + (x - chunk_lo(L, S.sp, ks));
-    a.rec.dst_tok[j] = a.off[1][(int64_t)kd * N + i] + (x - chunk_lo(L, Dl.sp, kd));
+    {
+      // local offset of virtual chunk c = offset of the sequence's holding on SP rank owner(c)
+      // (+ the first chunk's length for ZIGZAG's second chunk)
+      const Chunker ch_s = make_chunker(a, 0, i, s_gtok[0]), ch_d = make_chunker(a, 1, i, s_gtok[1]);
+      int64_t lo, hi, lo0, hi0;
+      const int os = ch_s.owner(ks), od = ch_d.owner(kd);
+      ch_s.bounds(ks, lo, hi);
+      int64_t so = a.off[0][(int64_t)os * N + i] + (x - lo);
+      if (ks != os) { ch_s.bounds(os, lo0, hi0); so += hi0 - lo0; }
+      ch_d.bounds(kd, lo, hi);
+      int64_t dof = a.off[1][(int64_t)od * N + i] + (x - lo);
+      if (kd != od) { ch_d.bounds(od, lo0, hi0); dof += hi0 - lo0; }
+      a.rec.src_tok[j] = so;
+      a.rec.dst_tok[j] = dof;
+    }
     a.rec.msg_tok[j] = msg_tok;
     a.rec.tok_prefix[j] = s_tbase[s][ds] + msg_tok;
   }
@@ -622,14 +728,17 @@ __global__ void local_meta_kernel(const __grid_constant__ PlanArgs a, int g, int
   const int64_t n = h->group_count[1][g];
   const int64_t gs = h->group_start[1][g];
   const int64_t* cum = a.cum[1] + (int64_t)k * (N + 1);
-  const int sp = a.lay[1].sp;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= n;
        j += (int64_t)gridDim.x * blockDim.x) {
     if (cu) cu[j] = (int32_t)(cum[gs + j] - cum[gs]);
     if (j < n) {
       const int i = a.perm[1][gs + j];
       if (ids) ids[j] = i;
-      if (tok_start) tok_start[j] = (int32_t)chunk_lo(a.lens[i], sp, k);
+      if (tok_start) {
+        int64_t lo, hi;
+        make_chunker(a, 1, i, h->group_tokens[1]).bounds(k, lo, hi);
+        tok_start[j] = (int32_t)lo;
+      }
     }
   }
 }

@@ -48,9 +48,13 @@ class EarlError(RuntimeError):
         self.name = STATUS.get(status, str(status))
 
 
+SP_SPLIT = {"block": 0, "zigzag": 1, "flat": 2, "threshold": 3}
+
+
 class Layout(C.Structure):
     _fields_ = [("rank0", C.c_int32), ("dp", C.c_int32), ("sp", C.c_int32), ("tp", C.c_int32),
-                ("assign", C.c_int32), ("sp_split", C.c_int32),
+                ("assign", C.c_int32), ("sp_split", C.c_int32), ("sp_min_len", C.c_int32),
+                ("reserved", C.c_int32),
                 ("counts", C.POINTER(C.c_int64)), ("group_of_seq", C.c_void_p)]
 
 
@@ -178,7 +182,10 @@ def make_layout(d) -> Layout:
     lay.sp, lay.tp = int(d.get("sp", 1)), int(d.get("tp", 1))
     a = d.get("assign", "contig")
     lay.assign = ASSIGN[a] if isinstance(a, str) else int(a)
-    lay.sp_split = 0
+    sp = d.get("sp_split", "block")
+    lay.sp_split = SP_SPLIT[sp] if isinstance(sp, str) else int(sp)
+    lay.sp_min_len = int(d.get("sp_min_len", 0))
+    lay.reserved = 0
     counts = d.get("counts")
     if counts is not None:
         arr = (C.c_int64 * len(counts))(*[int(c) for c in counts])

@@ -65,8 +65,8 @@ static int gpu_part(void) {
     CHECK(cudaMalloc(&d_src[r], 128 * 4) == cudaSuccess, "malloc");
     CHECK(cudaMemcpy(d_src[r], host_src[r], n_tok[r] * 4, cudaMemcpyHostToDevice) == cudaSuccess, "copy");
   }
-  earl_layout_t src = {0, 2, 1, 1, EARL_ASSIGN_GIVEN_COUNTS, 0, counts, NULL};
-  earl_layout_t dst = {0, 1, 1, 1, EARL_ASSIGN_CONTIG, 0, NULL, NULL};
+  earl_layout_t src = {0, 2, 1, 1, EARL_ASSIGN_GIVEN_COUNTS, EARL_SP_BLOCK, 0, 0, counts, NULL};
+  earl_layout_t dst = {0, 1, 1, 1, EARL_ASSIGN_CONTIG, EARL_SP_BLOCK, 0, 0, NULL, NULL};
   earl_field_t field = {4, 1};
   earl_plan_t plan = NULL;
   CHECK(earl_dispatch_plan(comm, &src, &dst, d_lens, 8, &field, 1, NULL, &plan) == EARL_OK,

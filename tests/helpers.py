@@ -60,7 +60,7 @@ def run_gpu_case(src, dst, lens, fields, world, mode="exec", seed=0, check_plan=
     for r in range(world):
         n_tok = int(st["n_local_tokens"][r])
         if r in want:
-            assert n_tok * 1 == sum(b - a for (_, a, b) in O.holdings(dst, lens, O.assign_groups(dst, lens))[r]["chunks"])
+            assert n_tok == O.holdings(dst, lens, O.assign_groups(dst, lens))[r]["n_tokens"]
         for f in range(len(fields)):
             n = n_tok * Bf[f]
             buf = torch.full((n + 2 * guard,), 0xA5, dtype=torch.uint8, device=dev)

@@ -287,3 +287,48 @@ def test_plan_independent_of_planner_grid():
         assert r.returncode == 0, r.stderr[-2000:]
         outs[g] = r.stdout.strip().splitlines()[-1]
     assert len(set(outs.values())) == 1, outs
+
+
+# ---------------------------------------------------------------------------------------
+# SP split variants (readings n1 zigzag, n2 flat, n3 threshold)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("split,extra", [("zigzag", {}), ("flat", {}),
+                                         ("threshold", {"sp_min_len": 20})])
+def test_golden_sp_variants_on_gpu(split, extra):
+    dst = W.layout(dp=1, sp=2, assign="contig", sp_split=split, **extra)
+    run_gpu_case(W.rollout_layout(8, 2), dst, GOLD_LENS, W.field_set("tiny3"), 2)
+
+
+@pytest.mark.parametrize("split", ["zigzag", "flat", "threshold"])
+@pytest.mark.parametrize("n_gpus", [4, 8])
+def test_c4_sp_variants(split, n_gpus):
+    """Config 4's DPn -> DP n/2 x SP2 with each split rule (threshold: split sequences >= 8K)."""
+    lens = W.c4_lengths(0)[:24].tolist()
+    src, dst = W.config_layouts("c4", n_gpus, len(lens))
+    dst = dict(dst, sp_split=split, sp_min_len=8192 if split == "threshold" else 0)
+    run_gpu_case(src, dst, lens, W.field_set("scalar6-bf16"), n_gpus, seed=30 + n_gpus,
+                 mode="stage" if split == "flat" else "exec")
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_variant_layouts_on_gpu(seed):
+    from tests.test_oracle_sp_variants import with_split
+    rng = random.Random(5000 + seed)
+    world = rng.randint(1, 8)
+    n = rng.choice([0, 1, 5, rng.randint(0, 60), rng.randint(60, 250)])
+    lens = [rng.choice([0, 1, 2, 7, rng.randint(0, 100), rng.randint(0, 1500)]) for _ in range(n)]
+    src = with_split(rng, random_layout(rng, world, n))
+    dst = with_split(rng, random_layout(rng, world, n))
+    fields = rng.sample(ODD_FIELDS, rng.randint(1, 4))
+    run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
+
+
+def test_large_n_variants_cooperative():
+    rng = np.random.default_rng(77)
+    n = 30000
+    lens = rng.integers(0, 40, size=n).tolist()
+    for dst in (W.layout(dp=2, sp=4, assign="contig", sp_split="zigzag"),
+                W.layout(dp=4, sp=2, assign="contig", sp_split="flat"),
+                W.layout(dp=2, sp=2, tp=2, assign="contig", sp_split="threshold", sp_min_len=20)):
+        run_gpu_case(W.rollout_layout(n, 8), dst, lens, [("m", 1, 1, "x")], 8, seed=11)
