@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c3", choices=["c3", "c4", "c2-lpt", "c5", "c5-lt"])
     ap.add_argument("--n-seqs", type=int, default=512, help="c5/c5-lt: sequences in the batch")
+    ap.add_argument("--sp-split", default="block", choices=["block", "zigzag", "flat", "threshold"],
+                    help="SP split rule of the destination layout (c4: DP4 x SP2)")
+    ap.add_argument("--sp-min-len", type=int, default=8192, help="threshold split: shortest split sequence")
     ap.add_argument("--fields", default="scalar6-fp32+hidden2560")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -75,7 +78,7 @@ def ncu_traffic(desc):
     return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
 
 
-def workload(config, n_ranks, fields_name, n_seqs=512):
+def workload(config, n_ranks, fields_name, n_seqs=512, sp_split="block", sp_min_len=0):
     from paper_2510_05943_b200 import workloads as W
     if config in ("c3", "c2-lpt"):
         lens = W.c2_lengths(0)
@@ -88,6 +91,8 @@ def workload(config, n_ranks, fields_name, n_seqs=512):
     import numpy as np
     lens = np.asarray(lens, dtype=np.int64)
     src, dst = W.config_layouts("c5" if config == "c5-lt" else config, n_ranks, len(lens))
+    if sp_split != "block":
+        dst = dict(dst, sp_split=sp_split, sp_min_len=sp_min_len if sp_split == "threshold" else 0)
     fields = W.field_set(fields_name)
     names = {
         "c3": "C2/C3 4B-class Tic-Tac-Toe batch: 512 episodes, lognormal(2048, 0.75) clip [64,8192]",
@@ -97,6 +102,7 @@ def workload(config, n_ranks, fields_name, n_seqs=512):
         "c5-lt": f"C5 long-tail all-to-allv, {n_seqs} episodes lognormal(2048, 0.75) clip [64,8192]",
     }
     lay = lambda L: (f"DP{L['dp']}" + (f"xSP{L['sp']}" if L['sp'] > 1 else "")
+                     + (f"({L['sp_split']})" if L.get("sp_split", "block") != "block" else "")
                      + (f"xTP{L['tp']}" if L['tp'] > 1 else "") + f"[{L['assign']}]")
     desc = f"{names[config]}; fields {fields_name}; {lay(src)} -> {lay(dst)}"
     return lens, src, dst, fields, desc
@@ -231,7 +237,7 @@ def run_single(args):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     R = 8
-    lens, src, dst, fields, desc = workload(args.config, R, args.fields, args.n_seqs)
+    lens, src, dst, fields, desc = workload(args.config, R, args.fields, args.n_seqs, args.sp_split, args.sp_min_len)
     F = len(fields)
     Bf = [b * e for (_, b, e, _) in fields]
     ed = EmulatedDispatch(R)
@@ -428,7 +434,7 @@ def run_multi(args):
     else:
         dist.init_process_group("nccl", device_id=dev)
     rank, world = dist.get_rank(), dist.get_world_size()
-    lens, src, dst, fields, desc = workload(args.config, world, args.fields, args.n_seqs)
+    lens, src, dst, fields, desc = workload(args.config, world, args.fields, args.n_seqs, args.sp_split, args.sp_min_len)
     F = len(fields)
     B = W.bytes_per_token(fields)
     T = int(lens.sum())

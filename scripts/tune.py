@@ -16,6 +16,8 @@ for cfg in cfgs:
             args += ["--n-seqs", parts[1]]
         if len(parts) > 2 and parts[2]:
             args += ["--fields", parts[2]]
+        if len(parts) > 3 and parts[3]:
+            args += ["--sp-split", parts[3]]
         env = dict(os.environ, EARL_COPY_CFG=cfg)
         r = subprocess.run([sys.executable, "bench.py", "--steps", "10", "--warmup", "3", "--no-e2e",
                             "--no-cpu-baseline"] + args, capture_output=True, text=True, env=env)
