@@ -1,0 +1,24 @@
+"""A handful of GPU dispatch cases for compute-sanitizer runs (each bit-exact vs the oracle)."""
+import random
+import sys
+import os
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_05943_b200 import workloads as W  # noqa: E402
+from tests.helpers import random_layout, run_gpu_case  # noqa: E402
+from tests.test_oracle_sp_variants import with_split  # noqa: E402
+
+fields = [("a", 4, 1, "x"), ("m", 1, 1, "x"), ("h", 2, 8, "x")]
+lens8 = W.TINY_LENGTHS.tolist()
+run_gpu_case(W.rollout_layout(8, 2), W.layout(dp=1, tp=2, assign="contig"), lens8, fields, 2, mode="exec")
+run_gpu_case(W.rollout_layout(8, 2), W.layout(dp=1, sp=2, assign="contig", sp_split="zigzag"), lens8, fields, 2, mode="stage")
+run_gpu_case(W.rollout_layout(8, 2), W.layout(dp=2, assign="lpt"), lens8, fields, 2)
+for seed in range(4):
+    rng = random.Random(900 + seed)
+    world = rng.randint(2, 8)
+    n = rng.randint(5, 60)
+    lens = [rng.randint(0, 300) for _ in range(n)]
+    src = with_split(rng, random_layout(rng, world, n))
+    dst = with_split(rng, random_layout(rng, world, n))
+    run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
+print("sanitize cases ok")
