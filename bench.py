@@ -450,8 +450,6 @@ def run_multi(args):
     st = plan.stats()
     recv_ptrs, _views = D.alloc_recv(plan, fields)
     staged = args.exchange == "staged"
-    if staged:
-        send_stage, recv_stage, msgs = D.alloc_stage(plan)
     plan.destroy()
 
     def step(ev=None):
@@ -461,8 +459,9 @@ def run_multi(args):
         p = D.plan(src, dst, gl, fields, stream)
         if ev is not None:
             ev[1].record(stream)
-        if staged:  # pack -> grouped NCCL send/recv -> unpack (the exchange comparator)
-            D.exec_staged(p, send, recv_ptrs, send_stage, recv_stage, msgs, stream)
+        if staged:  # pack -> grouped NCCL send/recv -> unpack (the exchange comparator); the
+            # per-peer byte table is read from the plan every step (a host sync NCCL needs)
+            D.exec_staged(p, send, recv_ptrs, stream=stream)
         else:       # fused P2P: one pass, stores straight into the peers' windows
             p.exec(send, recv_ptrs, stream)
         if ev is not None:
@@ -512,7 +511,7 @@ def run_multi(args):
             gl, _ = D.allgather_lens(my_lens)
             p = D.plan(src, dst, gl, fields, stream)
             if staged:
-                D.exec_staged(p, send, recv_ptrs, send_stage, recv_stage, msgs, stream)
+                D.exec_staged(p, send, recv_ptrs, stream=stream)
             else:
                 p.exec(send, recv_ptrs, stream)
             p.local_meta(rank, cu_dev, None, None, stream)

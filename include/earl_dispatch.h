@@ -178,6 +178,13 @@ EARL_API earl_status_t earl_dispatch_plan(earl_comm_t comm, const earl_layout_t*
                                  const earl_layout_t* dst, const int32_t* seq_lens,
                                  int64_t n_seqs, const earl_field_t* fields, int32_t n_fields,
                                  void* stream, earl_plan_t* plan);
+/* Re-plan the same N sequences (same comm, layouts, fields) for new lengths seq_lens (DEVICE
+ * int32 [N]) into the plan's existing device memory: nothing is allocated, so a training loop
+ * re-plans every batch at the planner's cost only.  Stream-ordered: work still using the
+ * previous plan must precede it on `stream` (or be synchronised).  earl_dispatch_plan followed
+ * by earl_plan_replan / earl_dispatch_exec is capturable into a CUDA graph; after replaying one,
+ * synchronise the stream before host queries (earl_plan_stats, ...). */
+EARL_API earl_status_t earl_plan_replan(earl_plan_t plan, const int32_t* seq_lens, void* stream);
 /* Wait for the plan and report device-latched errors. */
 EARL_API earl_status_t earl_plan_sync(earl_plan_t plan);
 /* Destination rank `rank`'s holding (host; synchronises): sequences and tokens. */

@@ -105,6 +105,8 @@ struct earl_plan {
   cudaEvent_t ev = nullptr;
   bool synced = false;
   PlanHeader host_hdr{};
+  size_t lpt_smem = 0;
+  int grid = 1;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -317,10 +319,11 @@ T* carve(uint8_t*& p, int64_t count) {
   return r;
 }
 
+// Host view of the plan header: always re-read after synchronising the plan's stream (a plan
+// may have been re-planned on the device -- replan, CUDA-graph replay -- since the last query).
 earl_status_t plan_wait(earl_plan_t p) {
-  if (p->synced) return EARL_OK;
   DeviceGuard g(p->comm->device);
-  CUDA_TRY(cudaEventSynchronize(p->ev));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
   CUDA_TRY(cudaMemcpy(&p->host_hdr, p->args.hdr, sizeof(PlanHeader), cudaMemcpyDeviceToHost));
   p->synced = true;
   return EARL_OK;
@@ -357,6 +360,38 @@ bool coords(const earl_layout_t& L, int rank, int* g, int* k, int* t) {
 }
 
 }  // namespace
+
+// Run the planner into the plan's memory on stream s: reset the header, launch, and record the
+// plan's event (not while the stream is being captured into a CUDA graph: the caller then
+// synchronises the stream itself before host queries).
+cudaError_t plan_launch(earl_plan* p, cudaStream_t s) {
+  PlanArgs& a = p->args;
+  cudaError_t e = cudaMemsetAsync(a.hdr, 0, sizeof(PlanHeader), s);
+  if (e != cudaSuccess) return e;
+  static const char* plan_trace = getenv("EARL_PLAN_TRACE");
+  if (plan_trace) cudaMallocAsync((void**)&a.phase_ts, 16 * sizeof(uint64_t), s);
+  clear_stale_error();
+  e = launch_planner(a, p->lpt_smem, p->grid, s);
+  if (plan_trace && e == cudaSuccess) {  // debug only: synchronous read-back of phase times
+    uint64_t ts[16];
+    cudaMemcpyAsync(ts, a.phase_ts, sizeof(ts), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "earl plan trace N=%lld G=%d us:", (long long)a.N, p->grid);
+    for (int k = 1; k < 8; ++k) fprintf(stderr, " p%d=%.1f", k - 1, (ts[k] - ts[k - 1]) / 1e3);
+    fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]\n", (ts[7] - ts[0]) / 1e3,
+            (ts[8] - ts[5]) / 1e3, (ts[9] - ts[8]) / 1e3, (ts[6] - ts[9]) / 1e3);
+    cudaFreeAsync(a.phase_ts, s);
+    a.phase_ts = nullptr;
+  }
+  if (e != cudaSuccess) return e;
+  g_launches.fetch_add(1);
+  p->stream = s;
+  p->synced = false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cap);
+  if (cap == cudaStreamCaptureStatusNone) e = cudaEventRecord(p->ev, s);
+  return e;
+}
 
 extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* src,
                                             const earl_layout_t* dst, const int32_t* seq_lens,
@@ -475,37 +510,32 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
     delete p;
     return fail(code, "%s: %s", what, cudaGetErrorString(err));
   };
-  e = cudaMemsetAsync(a.hdr, 0, sizeof(PlanHeader), s);
-  if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "header memset", e);
   const bool lpt = src->assign == EARL_ASSIGN_LPT || dst->assign == EARL_ASSIGN_LPT;
-  size_t lpt_smem = 0;
   if (lpt) {
     int64_t n2 = 1;
     while (n2 < N) n2 <<= 1;
-    lpt_smem = (size_t)n2 * sizeof(uint64_t);
+    p->lpt_smem = (size_t)n2 * sizeof(uint64_t);
   }
-  const int grid = planner_grid(N, max_pieces, c->sm_count, lpt_smem);
-  static const char* plan_trace = getenv("EARL_PLAN_TRACE");
-  if (plan_trace) cudaMallocAsync((void**)&a.phase_ts, 16 * sizeof(uint64_t), s);
-  clear_stale_error();
-  e = launch_planner(a, lpt_smem, grid, s);
-  if (plan_trace && e == cudaSuccess) {  // debug only: synchronous read-back of phase times
-    uint64_t ts[16];
-    cudaMemcpyAsync(ts, a.phase_ts, sizeof(ts), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    fprintf(stderr, "earl plan trace N=%lld G=%d us:", (long long)N, grid);
-    for (int k = 1; k < 8; ++k) fprintf(stderr, " p%d=%.1f", k - 1, (ts[k] - ts[k - 1]) / 1e3);
-    fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]\n", (ts[7] - ts[0]) / 1e3,
-            (ts[8] - ts[5]) / 1e3, (ts[9] - ts[8]) / 1e3, (ts[6] - ts[9]) / 1e3);
-    cudaFreeAsync(a.phase_ts, s);
-    a.phase_ts = nullptr;
-  }
-  if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "planner launch", e);
-  g_launches.fetch_add(1);
+  p->grid = planner_grid(N, max_pieces, c->sm_count, p->lpt_smem);
   e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventRecord(p->ev, s);
   if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "plan event", e);
+  e = plan_launch(p, s);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(p->ev);
+    p->ev = nullptr;
+    return abort_plan(EARL_ERR_CUDA, "planner launch", e);
+  }
   *out = p;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_replan(earl_plan_t p, const int32_t* seq_lens, void* stream) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (p->N > 0 && !seq_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens is NULL");
+  DeviceGuard g(p->comm->device);
+  p->args.seq_lens = seq_lens;
+  cudaError_t e = plan_launch(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "replan: %s", cudaGetErrorString(e));
   return EARL_OK;
 }
 
@@ -815,14 +845,12 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
   }
   if (!c->emulated && c->world > 1) {
     a.protocol = 1;
-    c->epoch += 1;
-    a.epoch = c->epoch;
     a.my_pad = reinterpret_cast<uint64_t*>(c->win[c->rank]);
     uint64_t* pads[kMaxWorld] = {};
     for (int q = 0; q < c->world; ++q) pads[q] = reinterpret_cast<uint64_t*>(c->peer[q]);
     for (int q = 0; q < kMaxWorld; ++q) a.peer_pad[q] = pads[q];
     clear_stale_error();
-    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, a.epoch, c->timeout_ns,
+    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, c->timeout_ns,
                                          a.err, a.err_detail, s);
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1);

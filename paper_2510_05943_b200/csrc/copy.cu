@@ -71,9 +71,17 @@ __device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad,
   return __reduce_or_sync(kFull, missing);
 }
 
+// The exec epoch lives in this rank's pad (slot kEpochSlot, written only by this rank): the
+// entry barrier of every exec advances it and the copy kernel that follows on the stream reads
+// it, so an exec captured into a CUDA graph gets a fresh epoch on every replay.
 __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world, int me,
-                                     uint64_t epoch, uint64_t timeout_ns, int32_t* err,
-                                     int32_t* err_detail) {
+                                     uint64_t timeout_ns, int32_t* err, int32_t* err_detail) {
+  uint64_t epoch = 0;
+  if (threadIdx.x == 0) {
+    epoch = my_pad[kEpochSlot] + 1;
+    my_pad[kEpochSlot] = epoch;
+  }
+  epoch = __shfl_sync(kFull, epoch, 0);
   const unsigned miss = signal_and_wait(my_pad, pads.p, world, me, kReadySlot, epoch, timeout_ns);
   if (threadIdx.x == 0 && miss) {
     if (atomicCAS(err, 0, EARL_ERR_TIMEOUT) == 0) *err_detail = (int32_t)miss;
@@ -394,7 +402,13 @@ struct Walker {
       if (!claim(a, v)) return false;
     const uint32_t off = (uint32_t)((uintptr_t)psrc & 15);
     const uint64_t room = space - off;
-    const uint32_t len = (uint32_t)(prem < room ? prem : room);
+    uint32_t len = (uint32_t)(prem < room ? prem : room);
+    if (len < prem) {
+      // more of this piece follows: end the range on a 128-B source boundary so the following
+      // bulk copies cover whole cache lines
+      const uint32_t cut = (uint32_t)(((uintptr_t)psrc + len) & 127);
+      if (cut < len) len -= cut;
+    }
     d.src_al = psrc - off;
     d.dst0 = pdst;
     d.off = (uint8_t)off;
@@ -611,8 +625,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     if (s_last && threadIdx.x < 32) {
       if (threadIdx.x == 0) *a.done_ctr = 0;
       __threadfence_system();
-      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.world, a.me, kDoneSlot,
-                                            a.epoch, a.timeout_ns);
+      const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(a.my_pad + kEpochSlot);
+      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.world, a.me, kDoneSlot, epoch,
+                                            a.timeout_ns);
       if (threadIdx.x == 0 && miss) {
         if (atomicCAS(a.err, 0, EARL_ERR_TIMEOUT) == 0) *a.err_detail = (int32_t)miss;
       }
@@ -658,17 +673,18 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cu
     case 4: return launch_cfg<2, 8, 8192>(a, sm_count, s);
     case 5: return launch_cfg<16, 2, 4096>(a, sm_count, s);
     case 6: return launch_cfg<8, 4, 6144>(a, sm_count, s);
+    case 7: return launch_cfg<4, 3, 16384>(a, sm_count, s);
+    case 8: return launch_cfg<2, 6, 16384>(a, sm_count, s);
     default: return launch_cfg<8, 3, 8192>(a, sm_count, s);
   }
 }
 
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 uint64_t epoch, uint64_t timeout_ns, int32_t* err,
-                                 int32_t* err_detail, cudaStream_t s) {
+                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
+                                 cudaStream_t s) {
   PeerPads pads;
   for (int p = 0; p < kMaxWorld; ++p) pads.p[p] = peer_pad[p];
-  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, epoch, timeout_ns, err,
-                                        err_detail);
+  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, timeout_ns, err, err_detail);
   return cudaGetLastError();
 }
 

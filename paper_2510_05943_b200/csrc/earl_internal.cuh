@@ -125,7 +125,6 @@ struct CopyArgs {
   unsigned int* done_ctr;                     // device counter for the last-CTA pattern
   uint64_t* my_pad;                           // this rank's signal pad (local)
   uint64_t* peer_pad[kMaxWorld];              // peers' signal pads (mapped)
-  uint64_t epoch;
   uint64_t timeout_ns;
   int32_t* err;                               // where to latch TIMEOUT (plan header)
   int32_t* err_detail;
@@ -137,14 +136,15 @@ struct CopyArgs {
 // signal pad slots (uint64 each): [0, 8) ready flags written by peer p at p; [8, 16) done flags
 constexpr int kReadySlot = 0;
 constexpr int kDoneSlot = 8;
+constexpr int kEpochSlot = 16;  // this rank's exec epoch (written by its own entry barrier)
 
 // launchers (defined in the .cu files)
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 uint64_t epoch, uint64_t timeout_ns, int32_t* err,
-                                 int32_t* err_detail, cudaStream_t s);
+                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
+                                 cudaStream_t s);
 cudaError_t launch_local_meta(const PlanArgs& a, int rank_g, int rank_k, int32_t* cu, int64_t* ids,
                               int32_t* tok_start, cudaStream_t s);
 

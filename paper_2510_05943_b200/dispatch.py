@@ -208,8 +208,24 @@ class Dispatcher:
         for p, hbuf in host_recv.items():
             recv_stage[ro[p]:ro[p] + rb[p]].copy_(hbuf)
 
-    def exec_staged(self, plan, send_bufs, recv_bufs, send_stage, recv_stage, msgs, stream=None):
-        """pack (this rank's records) -> grouped send/recv -> unpack (this rank's arrays)."""
+    def exec_staged(self, plan, send_bufs, recv_bufs, send_stage=None, recv_stage=None, msgs=None,
+                    stream=None):
+        """pack (this rank's records) -> grouped send/recv -> unpack (this rank's arrays).
+
+        Without an explicit `msgs` the per-peer byte table is read from the plan on every call
+        -- a device->host synchronisation that the NCCL path inherently needs (its sizes are
+        host arguments), unlike the fused exec.  Stage buffers grow on demand and are cached."""
+        if msgs is None:
+            msgs = plan.messages(self.rank)
+        if send_stage is None or recv_stage is None:
+            st_bytes = int(plan.stats()["stage_bytes"][self.rank])
+            need_s, need_r = max(16, st_bytes), max(16, int(sum(msgs[3])))
+            cache = getattr(self, "_stage_cache", None)
+            if cache is None or cache[0].numel() < need_s or cache[1].numel() < need_r:
+                cache = (torch.empty(need_s, dtype=torch.uint8, device=self.device),
+                         torch.empty(need_r, dtype=torch.uint8, device=self.device))
+                self._stage_cache = cache
+            send_stage, recv_stage = cache
         plan.pack(send_bufs, [send_stage], stream)
         self.exchange(send_stage, recv_stage, msgs)
         plan.unpack([recv_stage], recv_bufs, stream)

@@ -34,7 +34,7 @@ ASSIGN = {"given_counts": 0, "contig": 1, "lpt": 2, "explicit": 3}
 EXPORTED = [
     "earl_comm_create", "earl_comm_export_handle", "earl_comm_import_peers", "earl_comm_alloc",
     "earl_comm_reset_alloc", "earl_comm_info", "earl_comm_destroy", "earl_dispatch_plan",
-    "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
+    "earl_plan_replan", "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
     "earl_plan_export", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
     "earl_dispatch_unpack", "earl_plan_messages", "earl_status_string", "earl_last_error",
     "earl_abi_version", "earl_kernel_launch_count",
@@ -118,6 +118,7 @@ def lib():
         "earl_dispatch_plan": [vp, C.POINTER(Layout), C.POINTER(Layout), vp, i64,
                                C.POINTER(Field), i32, vp, pvp],
         "earl_plan_sync": [vp],
+        "earl_plan_replan": [vp, vp, vp],
         "earl_plan_local_sizes": [vp, i32, C.POINTER(i64), C.POINTER(i64)],
         "earl_plan_local_meta": [vp, i32, vp, vp, vp, vp],
         "earl_plan_stats": [vp, C.POINTER(PlanStats)],
@@ -270,6 +271,12 @@ class Plan:
         self.h = h
         self.n_seqs = n
         self._seq_lens = seq_lens  # keep alive until the planner ran
+
+    def replan(self, seq_lens, stream=None):
+        """Re-run the device planner for new lengths (same N) into this plan's memory."""
+        assert int(seq_lens.numel()) == self.n_seqs
+        check(lib().earl_plan_replan(self.h, _ptr(seq_lens) or None, _stream(stream)))
+        self._seq_lens = seq_lens
 
     # -- queries (host-synchronising) --
     def sync(self):

@@ -75,8 +75,11 @@ def gpu_main(rank, world, port, q, case):
             for v in views:
                 v.fill_(0xA5)
             if staged:  # pack -> grouped send/recv -> unpack
-                send_stage, recv_stage, msgs = D.alloc_stage(plan)
-                D.exec_staged(plan, mine, ptrs, send_stage, recv_stage, msgs)
+                if it == 0:
+                    send_stage, recv_stage, msgs = D.alloc_stage(plan)
+                    D.exec_staged(plan, mine, ptrs, send_stage, recv_stage, msgs)
+                else:
+                    D.exec_staged(plan, mine, ptrs)
             else:
                 plan.exec(mine, ptrs)
             torch.cuda.synchronize()

@@ -332,3 +332,74 @@ def test_large_n_variants_cooperative():
                 W.layout(dp=4, sp=2, assign="contig", sp_split="flat"),
                 W.layout(dp=2, sp=2, tp=2, assign="contig", sp_split="threshold", sp_min_len=20)):
         run_gpu_case(W.rollout_layout(n, 8), dst, lens, [("m", 1, 1, "x")], 8, seed=11)
+
+
+# ---------------------------------------------------------------------------------------
+# plan reuse and CUDA graphs
+# ---------------------------------------------------------------------------------------
+
+def _fill_and_expect(src, dst, lens, fields, world, cap_tok, dev, seed):
+    """Source buffers (capacity cap_tok tokens per rank) filled for `lens`, and the oracle."""
+    import torch
+    glob = W.gen_global_fields(fields, sum(lens), seed_base=seed, random_bits=True)
+    src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+    want, meta, segs = O.dispatch(src, dst, lens, src_arrays, fields, world)
+    return src_arrays, want, segs
+
+
+def test_replan_and_cuda_graph_replay():
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    world, n = 8, 200
+    fields = [("a", 4, 1, "x"), ("m", 1, 1, "x"), ("h", 2, 16, "x")]
+    Bf = O.field_bytes(fields)
+    rng = np.random.default_rng(3)
+    batches = [rng.integers(0, 400, size=n).tolist() for _ in range(4)]
+    src = W.rollout_layout(n, world)
+    dst = W.layout(dp=2, sp=2, tp=2, assign="contig", sp_split="zigzag")
+    cap = max(sum(b) for b in batches)
+    ed = EmulatedDispatch(world)
+    dev = ed.device
+    send = [torch.zeros(cap * b, dtype=torch.uint8, device=dev) for _ in range(world) for b in Bf]
+    recv = [torch.zeros(cap * b, dtype=torch.uint8, device=dev) for _ in range(world) for b in Bf]
+    lens_dev = torch.tensor(batches[0], dtype=torch.int32, device=dev)
+    plan = ed.plan(src, dst, lens_dev, fields)
+
+    def load(lens, seed):
+        src_arrays, want, segs = _fill_and_expect(src, dst, lens, fields, world, cap, dev, seed)
+        for r in range(world):
+            for f in range(len(fields)):
+                a = src_arrays[r][f]
+                if a.size:
+                    send[r * len(fields) + f][: a.size].copy_(torch.from_numpy(a))
+        return want, segs
+
+    def check(want):
+        for r, arrs in want.items():
+            for f in range(len(fields)):
+                got = recv[r * len(fields) + f][: arrs[f].size].cpu().numpy()
+                assert np.array_equal(got, arrs[f]), (r, f)
+
+    # 1) replan: new lengths into the same plan memory
+    want, segs = load(batches[1], 11)
+    lens_dev.copy_(torch.tensor(batches[1], dtype=torch.int32))
+    plan.replan(lens_dev)
+    assert plan.export() == segs
+    plan.exec(send, recv)
+    torch.cuda.synchronize()
+    check(want)
+    # 2) capture replan + exec in a CUDA graph, replay for two more batches
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.replan(lens_dev, stream=s)
+        plan.exec(send, recv, stream=s)
+    for k, lens in enumerate(batches[2:]):
+        want, segs = load(lens, 20 + k)
+        lens_dev.copy_(torch.tensor(lens, dtype=torch.int32))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        check(want)
+        assert plan.export() == segs
