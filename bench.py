@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c2-lpt", "c5", "c5-lt"])
+    ap.add_argument("--config", default="c3", choices=["c3", "c4", "c2-lpt", "c5", "c5-lt", "c0"])
     ap.add_argument("--n-seqs", type=int, default=512, help="c5/c5-lt: sequences in the batch")
     ap.add_argument("--sp-split", default="block", choices=["block", "zigzag", "flat", "threshold"],
                     help="SP split rule of the destination layout (c4: DP4 x SP2)")
@@ -82,6 +82,8 @@ def workload(config, n_ranks, fields_name, n_seqs=512, sp_split="block", sp_min_
     from paper_2510_05943_b200 import workloads as W
     if config in ("c3", "c2-lpt"):
         lens = W.c2_lengths(0)
+    elif config == "c0":  # fixed-overhead floor: the c3 layouts with every length 0
+        lens = [0] * 512
     elif config == "c4":
         lens = W.c4_lengths(0)
     elif config == "c5":  # sweep series, uniform lengths, round-robin all-to-allv
@@ -90,12 +92,14 @@ def workload(config, n_ranks, fields_name, n_seqs=512, sp_split="block", sp_min_
         lens = W.lognormal_lengths(n_seqs, 2048, 0.75, 64, 8192, 0)
     import numpy as np
     lens = np.asarray(lens, dtype=np.int64)
-    src, dst = W.config_layouts("c5" if config == "c5-lt" else config, n_ranks, len(lens))
+    lay_cfg = {"c5-lt": "c5", "c0": "c3"}.get(config, config)
+    src, dst = W.config_layouts(lay_cfg, n_ranks, len(lens))
     if sp_split != "block":
         dst = dict(dst, sp_split=sp_split, sp_min_len=sp_min_len if sp_split == "threshold" else 0)
     fields = W.field_set(fields_name)
     names = {
         "c3": "C2/C3 4B-class Tic-Tac-Toe batch: 512 episodes, lognormal(2048, 0.75) clip [64,8192]",
+        "c0": "C0 fixed-overhead floor: 512 episodes of length 0",
         "c4": "C4 70B-class long context: 256 episodes, lognormal(8192, 0.6) clip [4096,32768]",
         "c2-lpt": "C2 batch, LPT rebalance",
         "c5": f"C5 uniform all-to-allv, {n_seqs} x L=4096",
@@ -263,16 +267,19 @@ def run_single(args):
     alg_unpack = read_b + write_b
     peak, peak_src = measured_peaks()
 
+    # the plan object (device scratch) is made once; every step re-plans the batch on the
+    # device (earl_plan_replan: header reset + planner) and dispatches it -- no allocation
+    splan = ed.plan(src, dst, lens_dev, fields, stream)
+
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        p = ed.plan(src, dst, lens_dev, fields, stream)
+        splan.replan(lens_dev, stream)
         if ev is not None:
             ev[1].record(stream)
-        p.exec(send, recv, stream)
+        splan.exec(send, recv, stream)
         if ev is not None:
             ev[2].record(stream)
-        p.destroy()
 
     clocks = None if args.profile else ClockSampler(0)
     for _ in range(args.warmup):
@@ -319,19 +326,41 @@ def run_single(args):
            "plan_stats": {"records": st["records"], "segments": st["segments"],
                           "read_bytes": int(read_b), "write_bytes": int(write_b)}}
 
+    # the same step captured once as a CUDA graph (replan + exec) and replayed: the device-side
+    # cost without host launch overhead (matters for the latency-bound small batches)
+    if not args.profile:
+        gs = torch.cuda.Stream()
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            splan.replan(lens_dev, gs)
+            splan.exec(send, recv, gs)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        gb.record(stream)
+        torch.cuda.synchronize()
+        gms = ga.elapsed_time(gb) / args.steps
+        out["graph"] = {"ms_per_step": gms, "value": payload / (gms * 1e-3) / 1e9,
+                        "note": "replan + exec captured once as a CUDA graph, replayed per step"}
+        del graph
+
     # staged path: plan + pack + unpack
     if not args.no_staged:
         ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
         for k in range(args.warmup + args.steps):
             e = ev2[k - args.warmup] if k >= args.warmup else None
             if e: e[0].record(stream)
-            p = ed.plan(src, dst, lens_dev, fields, stream)
+            splan.replan(lens_dev, stream)
             if e: e[1].record(stream)
-            p.pack(send, stage, stream)
+            splan.pack(send, stage, stream)
             if e: e[2].record(stream)
-            p.unpack(stage, recv, stream)
+            splan.unpack(stage, recv, stream)
             if e: e[3].record(stream)
-            p.destroy()
         ta = time.time()
         torch.cuda.synchronize()
         if clocks:
@@ -366,12 +395,11 @@ def run_single(args):
             for h, d in zip(host_send, send):
                 d.copy_(h, non_blocking=True)
             lens_dev.copy_(lens_host, non_blocking=True)
-            p = ed.plan(src, dst, lens_dev, fields, stream)
-            p.exec(send, recv, stream)
+            splan.replan(lens_dev, stream)
+            splan.exec(send, recv, stream)
             for r in dst_ranks:
-                p.local_meta(r, metas[r], None, None, stream)
+                splan.local_meta(r, metas[r], None, None, stream)
                 meta_host[r].copy_(metas[r], non_blocking=True)
-            p.destroy()
 
         n_e2e = max(3, min(args.steps, 10))
         for _ in range(2):
@@ -452,11 +480,14 @@ def run_multi(args):
     staged = args.exchange == "staged"
     plan.destroy()
 
+    mplan = D.plan(src, dst, glens, fields, stream)
+
     def step(ev=None):
         gl, _ = D.allgather_lens(my_lens)
         if ev is not None:
             ev[0].record(stream)
-        p = D.plan(src, dst, gl, fields, stream)
+        p = mplan
+        p.replan(gl, stream)
         if ev is not None:
             ev[1].record(stream)
         if staged:  # pack -> grouped NCCL send/recv -> unpack (the exchange comparator); the
@@ -466,7 +497,6 @@ def run_multi(args):
             p.exec(send, recv_ptrs, stream)
         if ev is not None:
             ev[2].record(stream)
-        p.destroy()
 
     clocks = ClockSampler(local) if rank == 0 and not args.profile else None
     for _ in range(args.warmup):
@@ -509,14 +539,13 @@ def run_multi(args):
             for hs, d in zip(host_send, send):
                 d.copy_(hs, non_blocking=True)
             gl, _ = D.allgather_lens(my_lens)
-            p = D.plan(src, dst, gl, fields, stream)
+            mplan.replan(gl, stream)
             if staged:
-                D.exec_staged(p, send, recv_ptrs, stream=stream)
+                D.exec_staged(mplan, send, recv_ptrs, stream=stream)
             else:
-                p.exec(send, recv_ptrs, stream)
-            p.local_meta(rank, cu_dev, None, None, stream)
+                mplan.exec(send, recv_ptrs, stream)
+            mplan.local_meta(rank, cu_dev, None, None, stream)
             cu_host.copy_(cu_dev, non_blocking=True)
-            p.destroy()
 
         n_e2e = max(3, min(args.steps, 10))
         for _ in range(2):
