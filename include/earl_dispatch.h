@@ -197,6 +197,12 @@ EARL_API earl_status_t earl_plan_local_sizes(earl_plan_t plan, int32_t rank, int
  * Any pointer may be NULL to skip it. */
 EARL_API earl_status_t earl_plan_local_meta(earl_plan_t plan, int32_t rank, int32_t* cu_seqlens,
                                    int64_t* seq_ids, int32_t* tok_start, void* stream);
+/* The plan's group assignment g(i) of every sequence under src and dst (DEVICE int32 [N]
+ * outputs, either may be NULL), stream-ordered.  Used to route per-sequence fields (rewards,
+ * returns) with their sequences: a second plan over unit lengths with these groups as EXPLICIT
+ * layouts and the SP degree folded into TP (reading n4). */
+EARL_API earl_status_t earl_plan_groups(earl_plan_t plan, int32_t* src_groups, int32_t* dst_groups,
+                                        void* stream);
 /* Byte accounting of SPEC.md:239-247 (host; synchronises). */
 EARL_API earl_status_t earl_plan_stats(earl_plan_t plan, earl_plan_stats_t* stats);
 /* Debug: the canonical, uncoalesced segment table in (s, d, i, x) order (reading c19),
@@ -248,6 +254,26 @@ EARL_API earl_status_t earl_dispatch_unpack(earl_plan_t plan, const void* const*
 EARL_API earl_status_t earl_plan_messages(earl_plan_t plan, int32_t rank, int64_t* send_off,
                                           int64_t* send_bytes, int64_t* recv_off,
                                           int64_t* recv_bytes);
+
+/* ---- NEXT-2: distributed aggregation before the dispatch ---------- */
+
+/* On the source ranks (the plan's src layout must have sp == 1: sequences whole, as rollout DPn
+ * holds them), per sequence, the discounted returns G_t = m_t r_t + gamma G_{t+1} (G_L = 0):
+ * rewards fp32, mask u8 (1 = response token) and returns fp32 are this rank's token arrays
+ * ([world] in an emulated comm), seq_return (optional, NULL) fp32 [n_local_seqs] gets G_0.
+ * Accumulates the fp64 partials (sum m, sum m G, sum m G^2) of TP replica 0 into the DEVICE
+ * array partial[3] (caller zeroes it).  Readings n5 in DESIGN.md.  Errors: UNSUPPORTED if the
+ * source layout splits sequences (sp > 1). */
+EARL_API earl_status_t earl_returns(earl_plan_t plan, float gamma, const void* const* rewards,
+                                    const void* const* mask, void* const* returns,
+                                    void* const* seq_return, double* partial, void* stream);
+/* A_t = m_t (G_t - mu) / (sigma + eps) with mu, sigma the mean and (population) standard
+ * deviation of G over the batch's masked tokens, from stats[3] = the partials of earl_returns
+ * summed over every rank (an all-reduce of 3 doubles in a multi-process comm: no controller
+ * aggregates the rewards; REINFORCE++-style global normalisation). */
+EARL_API earl_status_t earl_advantages(earl_plan_t plan, const double* stats, float eps,
+                                       const void* const* returns, const void* const* mask,
+                                       void* const* adv, void* stream);
 
 /* ---- misc -------------------------------------------------------------------------- */
 EARL_API const char* earl_status_string(earl_status_t status);

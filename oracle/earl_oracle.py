@@ -544,3 +544,93 @@ def group_loads(g_of, seq_lens, D):
     for i, g in enumerate(g_of):
         loads[g] += int(seq_lens[i])
     return loads
+
+
+# ---------------------------------------------------------------------------
+# NEXT-2: per-sequence fields (reading n4) and distributed advantage estimation (reading n5)
+# ---------------------------------------------------------------------------
+
+def seq_holdings(lay, seq_lens, g_of):
+    """Every rank (g, k, t) of a layout holds one record per sequence of its group, ascending i
+    -- every SP rank and TP replica holds a copy (reading n4).  rank -> [i, ...]."""
+    out = {}
+    for g, members in group_members(seq_lens, g_of, lay["dp"]).items():
+        for k in range(lay["sp"]):
+            for t in range(lay["tp"]):
+                out[rank_of(lay, g, k, t)] = list(members)
+    return out
+
+
+def dispatch_seq_fields(src, dst, seq_lens, src_seq_arrays, sfields, world):
+    """Route per-sequence fields (rewards, returns) with their sequences:
+    destination rank d = (g, k, t) receives, at the position of sequence i in its group, the
+    record the source holds for i -- read from source rank (g_src(i), SP 0, t mod TP_src), as for
+    per-token fields (reading c9; all source copies are equal)."""
+    seq_lens = [int(x) for x in seq_lens]
+    validate_layout(src, len(seq_lens), world)
+    validate_layout(dst, len(seq_lens), world)
+    gs = assign_groups(src, seq_lens)
+    gd = assign_groups(dst, seq_lens)
+    hs = seq_holdings(src, seq_lens, gs)
+    hd = seq_holdings(dst, seq_lens, gd)
+    Bs = field_bytes(sfields)
+    out = {}
+    for d, members in hd.items():
+        _, _, td = coords_of(dst, d)
+        per_field = []
+        for f in range(len(sfields)):
+            parts = []
+            for i in members:
+                s = rank_of(src, gs[i], 0, td % src["tp"])
+                p = hs[s].index(i)
+                parts.append(src_seq_arrays[s][f][p * Bs[f]:(p + 1) * Bs[f]])
+            per_field.append(np.concatenate(parts) if parts else np.zeros(0, dtype=np.uint8))
+        out[d] = per_field
+    return out
+
+
+def discounted_returns(r, m, gamma):
+    """Reading n5: G_t = m_t r_t + gamma G_{t+1} over one sequence, G_L = 0 (fp64)."""
+    G = np.zeros(len(r), dtype=np.float64)
+    nxt = 0.0
+    for t in range(len(r) - 1, -1, -1):
+        nxt = float(m[t]) * float(r[t]) + gamma * nxt
+        G[t] = nxt
+    return G
+
+
+def distributed_advantages(src, seq_lens, rewards, masks, gamma, eps, world):
+    """Reading n5 (REINFORCE++-style globally normalised returns), computed
+    where the rollout holds the tokens (src layout, sp == 1) with no controller:
+      1. every source rank: per sequence, G_t = m_t r_t + gamma G_{t+1};
+      2. batch statistics over masked tokens (TP replica 0 counted once):
+         mu = sum m G / sum m, sigma = sqrt(sum m G^2 / sum m - mu^2);
+      3. A_t = m_t (G_t - mu) / (sigma + eps).
+    rewards / masks: rank -> fp32 / u8 token arrays.  Returns (G, A, seq_return, stats)."""
+    if src["sp"] != 1:
+        raise OracleError(ERR_UNSUPPORTED, "returns need whole sequences on the source")
+    seq_lens = [int(x) for x in seq_lens]
+    gs = assign_groups(src, seq_lens)
+    hs = holdings(src, seq_lens, gs)
+    G, R = {}, {}
+    n = s1 = s2 = 0.0
+    for rank, h in hs.items():
+        g_r = np.zeros(h["n_tokens"], dtype=np.float64)
+        ret = []
+        for (i, c, lo, hi) in h["chunks"]:
+            o = h["local_off"][(i, c)]
+            g_r[o:o + hi - lo] = discounted_returns(rewards[rank][o:o + hi - lo],
+                                                    masks[rank][o:o + hi - lo], gamma)
+            ret.append(g_r[o] if hi > lo else 0.0)
+        G[rank], R[rank] = g_r, np.array(ret, dtype=np.float64)
+        if coords_of(src, rank)[2] == 0:
+            mk = masks[rank].astype(bool)
+            n += float(mk.sum())
+            s1 += float(g_r[mk].sum())
+            s2 += float((g_r[mk] ** 2).sum())
+    mu = s1 / n if n else 0.0
+    var = max(s2 / n - mu * mu, 0.0) if n else 0.0
+    sigma = var ** 0.5
+    A = {rank: np.where(masks[rank].astype(bool), (G[rank] - mu) / (sigma + eps), 0.0)
+         for rank in G}
+    return G, A, R, (n, s1, s2)

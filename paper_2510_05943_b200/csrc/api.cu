@@ -574,6 +574,19 @@ extern "C" earl_status_t earl_plan_local_meta(earl_plan_t p, int32_t rank, int32
   return EARL_OK;
 }
 
+extern "C" earl_status_t earl_plan_groups(earl_plan_t p, int32_t* src_groups, int32_t* dst_groups,
+                                          void* stream) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  DeviceGuard dg(p->comm->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t bytes = (size_t)p->N * sizeof(int32_t);
+  if (bytes && src_groups)
+    CUDA_TRY(cudaMemcpyAsync(src_groups, p->args.grp[0], bytes, cudaMemcpyDeviceToDevice, s));
+  if (bytes && dst_groups)
+    CUDA_TRY(cudaMemcpyAsync(dst_groups, p->args.grp[1], bytes, cudaMemcpyDeviceToDevice, s));
+  return EARL_OK;
+}
+
 extern "C" earl_status_t earl_plan_stats(earl_plan_t p, earl_plan_stats_t* out) {
   if (!p || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   earl_status_t st = plan_check(p);
@@ -968,5 +981,82 @@ extern "C" earl_status_t earl_plan_messages(earl_plan_t p, int32_t rank, int64_t
       off += recv_bytes[s];
     }
   }
+  return EARL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// NEXT-2: distributed advantage estimation on the source ranks (aggregate.cu)
+// ---------------------------------------------------------------------------------------
+
+namespace {
+
+earl_status_t agg_args(earl_plan_t p, AggArgs& a) {
+  std::memset(&a, 0, sizeof(a));
+  if (p->lay[0].sp != 1)
+    return fail(EARL_ERR_UNSUPPORTED, "returns/advantages need whole sequences on the source (sp == 1)");
+  a.plan = p->args;
+  a.hdr = p->args.hdr;
+  a.world = p->comm->world;
+  a.view_rank = p->comm->emulated ? -1 : p->comm->rank;
+  return EARL_OK;
+}
+
+template <class T>
+earl_status_t set_per_rank(earl_plan_t p, T** dst, const void* const* src, const char* what,
+                           bool required) {
+  earl_comm* c = p->comm;
+  if (!src) {
+    if (required) return fail(EARL_ERR_INVALID_ARGUMENT, "%s is NULL", what);
+    return EARL_OK;
+  }
+  const int nr = c->emulated ? c->world : 1;
+  for (int r = 0; r < nr; ++r) {
+    const int rr = c->emulated ? r : c->rank;
+    dst[rr] = const_cast<T*>(static_cast<const T*>(src[r]));
+  }
+  return EARL_OK;
+}
+
+}  // namespace
+
+extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* const* rewards,
+                                      const void* const* mask, void* const* returns,
+                                      void* const* seq_return, double* partial, void* stream) {
+  if (!p || !partial) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  AggArgs a;
+  earl_status_t st = agg_args(p, a);
+  if (st != EARL_OK) return st;
+  a.gamma = gamma;
+  a.partial = partial;
+  if ((st = set_per_rank<const float>(p, a.rewards, rewards, "rewards", true)) != EARL_OK) return st;
+  if ((st = set_per_rank<const uint8_t>(p, a.mask, mask, "mask", true)) != EARL_OK) return st;
+  if ((st = set_per_rank<float>(p, a.returns, (const void* const*)returns, "returns", true)) != EARL_OK) return st;
+  if ((st = set_per_rank<float>(p, a.seq_return, (const void* const*)seq_return, "seq_return", false)) != EARL_OK)
+    return st;
+  DeviceGuard g(p->comm->device);
+  clear_stale_error();
+  cudaError_t e = launch_returns(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "returns launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_advantages(earl_plan_t p, const double* stats, float eps,
+                                         const void* const* returns, const void* const* mask,
+                                         void* const* adv, void* stream) {
+  if (!p || !stats) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  AggArgs a;
+  earl_status_t st = agg_args(p, a);
+  if (st != EARL_OK) return st;
+  a.stats = stats;
+  a.eps = eps;
+  if ((st = set_per_rank<float>(p, a.returns, returns, "returns", true)) != EARL_OK) return st;
+  if ((st = set_per_rank<const uint8_t>(p, a.mask, mask, "mask", true)) != EARL_OK) return st;
+  if ((st = set_per_rank<float>(p, a.adv, (const void* const*)adv, "adv", true)) != EARL_OK) return st;
+  DeviceGuard g(p->comm->device);
+  clear_stale_error();
+  cudaError_t e = launch_advantages(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "advantages launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
   return EARL_OK;
 }

@@ -138,7 +138,25 @@ constexpr int kReadySlot = 0;
 constexpr int kDoneSlot = 8;
 constexpr int kEpochSlot = 16;  // this rank's exec epoch (written by its own entry barrier)
 
+// NEXT-2 (aggregate.cu): returns / advantages on the source ranks (SP = 1)
+struct AggArgs {
+  PlanArgs plan;
+  const PlanHeader* hdr;
+  int32_t world;
+  int32_t view_rank;       // -1: every source rank (emulated comm); else this rank
+  float gamma, eps;
+  const float* rewards[kMaxWorld];   // per source comm rank: token rewards (fp32)
+  const uint8_t* mask[kMaxWorld];    // token mask (u8, 1 = counted)
+  float* returns[kMaxWorld];         // token returns G (fp32)
+  float* adv[kMaxWorld];             // token advantages A (fp32)
+  float* seq_return[kMaxWorld];      // per-sequence return G_0 (fp32), optional
+  double* partial;                   // [3] sum m, sum m G, sum m G^2 (accumulated)
+  const double* stats;               // [3] the same over the whole batch (after the all-reduce)
+};
+
 // launchers (defined in the .cu files)
+cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_advantages(const AggArgs& a, int sm_count, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s);

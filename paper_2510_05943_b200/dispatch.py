@@ -229,3 +229,31 @@ class Dispatcher:
         plan.pack(send_bufs, [send_stage], stream)
         self.exchange(send_stage, recv_stage, msgs)
         plan.unpack([recv_stage], recv_bufs, stream)
+
+
+# ---------------------------------------------------------------------------------------
+# per-sequence fields (reading n4)
+# ---------------------------------------------------------------------------------------
+
+def fold_layout(lay: dict, groups_dev) -> dict:
+    """The layout a per-sequence field travels on: the token plan's groups as EXPLICIT, its SP
+    degree folded into TP (rank(g,k,t) = rank0 + g*SP*TP + (k*TP + t) is rank (g, 0, k*TP+t) of
+    the folded layout), so every SP rank and TP replica of a group holds one record per sequence."""
+    out = dict(lay)
+    out.update(sp=1, tp=int(lay.get("sp", 1)) * int(lay.get("tp", 1)), assign="explicit",
+               counts=None, group_of_seq=None, group_of_seq_dev=groups_dev, sp_split="block",
+               sp_min_len=0)
+    return out
+
+
+def plan_seq_fields(comm, token_plan, src, dst, sfields, device, stream=None):
+    """Plan the routing of per-sequence fields along `token_plan`: unit lengths (one record per
+    sequence) over the folded layouts with the token plan's own group assignment."""
+    n = token_plan.n_seqs
+    gs = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    gd = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    token_plan.groups(gs, gd, stream)
+    ones = torch.ones(n, dtype=torch.int32, device=device)
+    sp = comm.plan(fold_layout(src, gs), fold_layout(dst, gd), ones, sfields, stream)
+    sp._keep = (gs, gd, ones)
+    return sp

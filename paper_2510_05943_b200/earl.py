@@ -35,8 +35,8 @@ EXPORTED = [
     "earl_comm_create", "earl_comm_export_handle", "earl_comm_import_peers", "earl_comm_alloc",
     "earl_comm_reset_alloc", "earl_comm_info", "earl_comm_destroy", "earl_dispatch_plan",
     "earl_plan_replan", "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
-    "earl_plan_export", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
-    "earl_dispatch_unpack", "earl_plan_messages", "earl_status_string", "earl_last_error",
+    "earl_plan_export", "earl_plan_groups", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
+    "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
     "earl_abi_version", "earl_kernel_launch_count",
 ]
 
@@ -124,10 +124,13 @@ def lib():
         "earl_plan_stats": [vp, C.POINTER(PlanStats)],
         "earl_plan_export": [vp, i64, C.POINTER(i64), vp, vp, vp, vp, vp, vp, vp],
         "earl_plan_destroy": [vp],
+        "earl_plan_groups": [vp, vp, vp, vp],
         "earl_dispatch_exec": [vp, pvp, pvp, vp],
         "earl_dispatch_pack": [vp, pvp, pvp, vp],
         "earl_dispatch_unpack": [vp, pvp, pvp, vp],
         "earl_plan_messages": [vp, i32, vp, vp, vp, vp],
+        "earl_returns": [vp, C.c_float, pvp, pvp, pvp, pvp, vp, vp],
+        "earl_advantages": [vp, vp, C.c_float, pvp, pvp, pvp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -308,6 +311,11 @@ class Plan:
         check(lib().earl_plan_export(self.h, m, C.byref(n), *ptrs))
         return [tuple(int(c[j]) for c in cols) for j in range(m)]
 
+    def groups(self, src_groups=None, dst_groups=None, stream=None):
+        """Device copies of g_src(i) and g_dst(i) (int32 [N] tensors)."""
+        check(lib().earl_plan_groups(self.h, _ptr(src_groups) or None, _ptr(dst_groups) or None,
+                                     _stream(stream)))
+
     def messages(self, rank: int):
         """Per-peer (send_off, send_bytes, recv_off, recv_bytes) of `rank` (host-synchronising)."""
         W = self.comm.world
@@ -327,6 +335,17 @@ class Plan:
     def unpack(self, stage_bufs, recv_bufs, stream=None):
         t, r = _ptr_array(stage_bufs), _ptr_array(recv_bufs)
         check(lib().earl_dispatch_unpack(self.h, t, r, _stream(stream)))
+
+    # -- NEXT-2: distributed advantage estimation on the source ranks --
+    def returns(self, gamma, rewards, mask, returns, partial, seq_return=None, stream=None):
+        check(lib().earl_returns(self.h, float(gamma), _ptr_array(rewards), _ptr_array(mask),
+                                 _ptr_array(returns),
+                                 _ptr_array(seq_return) if seq_return is not None else None,
+                                 _ptr(partial) or None, _stream(stream)))
+
+    def advantages(self, stats, eps, returns, mask, adv, stream=None):
+        check(lib().earl_advantages(self.h, _ptr(stats) or None, float(eps), _ptr_array(returns),
+                                    _ptr_array(mask), _ptr_array(adv), _stream(stream)))
 
     def destroy(self):
         if getattr(self, "h", None):

@@ -403,3 +403,110 @@ def test_replan_and_cuda_graph_replay():
         torch.cuda.synchronize()
         check(want)
         assert plan.export() == segs
+
+
+# ---------------------------------------------------------------------------------------
+# NEXT-2: per-sequence fields routed with their sequences (reading n4)
+# ---------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("seed", range(20))
+def test_seq_fields_on_gpu(seed):
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch, plan_seq_fields
+    from tests.test_oracle_sp_variants import with_split
+    rng = random.Random(7000 + seed)
+    world = rng.randint(1, 8)
+    n = rng.choice([0, 1, rng.randint(1, 40), rng.randint(40, 400)])
+    lens = [rng.randint(0, 500) for _ in range(n)]
+    src = with_split(rng, random_layout(rng, world, n))
+    dst = with_split(rng, random_layout(rng, world, n))
+    sf = [("reward", 4, 1, "x"), ("score", 2, 3, "x")]
+    Bs = O.field_bytes(sf)
+    gs = O.assign_groups(src, lens)
+    hs = O.seq_holdings(src, lens, gs)
+    glob = [np.random.default_rng(seed * 3 + f).integers(0, 256, size=n * Bs[f], dtype=np.uint8)
+            for f in range(len(sf))]
+    src_arrays = {r: [np.concatenate([glob[f][i * Bs[f]:(i + 1) * Bs[f]] for i in m])
+                      if m else np.zeros(0, dtype=np.uint8) for f in range(len(sf))]
+                  for r, m in hs.items()}
+    want = O.dispatch_seq_fields(src, dst, lens, src_arrays, sf, world)
+    ed = EmulatedDispatch(world)
+    tp = ed.plan(src, dst, lens, W.field_set("tiny3"))
+    sp = plan_seq_fields(ed.comm, tp, ed._src, ed._dst, sf, ed.device)
+    st = sp.stats()
+    send = [torch.from_numpy(src_arrays[r][f]).cuda() if r in src_arrays and src_arrays[r][f].size
+            else None for r in range(world) for f in range(len(sf))]
+    recv = [torch.zeros(max(1, int(st["n_local_tokens"][r]) * Bs[f]), dtype=torch.uint8, device="cuda")
+            for r in range(world) for f in range(len(sf))]
+    sp.exec(send, recv)
+    torch.cuda.synchronize()
+    for d, arrs in want.items():
+        for f in range(len(sf)):
+            got = recv[d * len(sf) + f][: arrs[f].size].cpu().numpy()
+            assert np.array_equal(got, arrs[f]), (d, f)
+
+
+@pytest.mark.parametrize("gamma", [1.0, 0.97, 0.0])
+@pytest.mark.parametrize("tp", [1, 2])
+def test_distributed_advantages_on_gpu(gamma, tp):
+    """Reading n5 on the GPU (fp32 tokens, fp64 statistics) against the fp64 oracle.
+    Tolerance: the fp32 recurrence G_t = v_t + gamma G_{t+1} accumulates at most
+    u * min(L, 1/(1-gamma)) * max|G| rounding error (u = 2^-24), times 4 for the warp-parallel
+    composition; A inherits it divided by sigma."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    rng = np.random.default_rng(int(gamma * 100) + tp)
+    world = 8
+    n = 300
+    lens = W.lognormal_lengths(n, 600, 0.8, 1, 3000, seed=5).tolist()
+    lens[3] = 0
+    src = W.layout(dp=world // tp, tp=tp, assign="contig")
+    T = sum(lens)
+    glob_r = rng.standard_normal(T).astype(np.float32)
+    glob_m = (rng.random(T) < 0.75).astype(np.uint8)
+    fr = [("r", 4, 1, "x"), ("m", 1, 1, "x")]
+    arrs = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens),
+                                     [glob_r.view(np.uint8), glob_m], fr)
+    rewards = {k: v[0].view(np.float32) for k, v in arrs.items()}
+    masks = {k: v[1] for k, v in arrs.items()}
+    G, A, R, stats = O.distributed_advantages(src, lens, rewards, masks, gamma, 1e-8, world)
+
+    ed = EmulatedDispatch(world)
+    plan = ed.plan(src, W.layout(dp=2, sp=2, tp=2, assign="contig"), lens, W.field_set("tiny3"))
+    dev = ed.device
+    d_r = [torch.from_numpy(rewards[r].copy()).to(dev) for r in range(world)]
+    d_m = [torch.from_numpy(masks[r].copy()).to(dev) for r in range(world)]
+    d_G = [torch.zeros(max(1, rewards[r].size), dtype=torch.float32, device=dev) for r in range(world)]
+    d_A = [torch.zeros(max(1, rewards[r].size), dtype=torch.float32, device=dev) for r in range(world)]
+    ns = plan.stats()["n_local_seqs"]
+    d_R = [torch.zeros(max(1, len(R[r])), dtype=torch.float32, device=dev) for r in range(world)]
+    partial = torch.zeros(3, dtype=torch.float64, device=dev)
+    plan.returns(gamma, d_r, d_m, d_G, partial, seq_return=d_R)
+    plan.advantages(partial, 1e-8, d_G, d_m, d_A)  # emulated: partials already cover the batch
+    torch.cuda.synchronize()
+    assert ns is not None
+    Lmax = max(lens)
+    horizon = Lmax if gamma >= 1.0 else min(Lmax, 1.0 / (1.0 - gamma))
+    gmax = max(np.abs(G[r]).max() if G[r].size else 0 for r in G)
+    atol_g = 4 * 2.0 ** -24 * horizon * gmax + 1e-6
+    got_stats = partial.cpu().numpy()
+    assert got_stats[0] == stats[0]
+    assert np.allclose(got_stats[1:], stats[1:], rtol=1e-5, atol=atol_g * stats[0])
+    sigma = np.sqrt(max(stats[2] / stats[0] - (stats[1] / stats[0]) ** 2, 0))
+    for r in range(world):
+        n_r = rewards[r].size
+        assert np.allclose(d_G[r][:n_r].cpu().numpy(), G[r], rtol=0, atol=atol_g), r
+        assert np.allclose(d_A[r][:n_r].cpu().numpy(), A[r], rtol=0, atol=atol_g / sigma + 1e-5), r
+        assert np.allclose(d_R[r][: len(R[r])].cpu().numpy(), R[r], rtol=0, atol=atol_g), r
+
+
+def test_returns_need_whole_sequences():
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    import torch
+    ed = EmulatedDispatch(2)
+    plan = ed.plan(W.layout(dp=1, sp=2), W.layout(dp=2), [4, 4], W.field_set("tiny3"))
+    p = torch.zeros(3, dtype=torch.float64, device="cuda")
+    with pytest.raises(EarlError) as e:
+        plan.returns(1.0, [None, None], [None, None], [None, None], p)
+    assert e.value.name == "EARL_ERR_UNSUPPORTED"
