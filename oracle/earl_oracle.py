@@ -590,11 +590,12 @@ def dispatch_seq_fields(src, dst, seq_lens, src_seq_arrays, sfields, world):
 
 
 def discounted_returns(r, m, gamma):
-    """Reading n5: G_t = m_t r_t + gamma G_{t+1} over one sequence, G_L = 0 (fp64)."""
+    """Reading n5: G_t = m_t r_t + gamma G_{t+1} over one sequence, G_L = 0 (fp64).
+    m is the boolean response mask: any nonzero byte is m_t = 1 (as in the statistics)."""
     G = np.zeros(len(r), dtype=np.float64)
     nxt = 0.0
     for t in range(len(r) - 1, -1, -1):
-        nxt = float(m[t]) * float(r[t]) + gamma * nxt
+        nxt = (1.0 if m[t] else 0.0) * float(r[t]) + gamma * nxt
         G[t] = nxt
     return G
 

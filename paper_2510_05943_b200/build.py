@@ -47,6 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
+    # tuning experiments only (e.g. EARL_NVCC_DEFINES="EARL_AGG_CTAS_PER_SM=2")
+    cmd += ["-D" + d for d in os.environ.get("EARL_NVCC_DEFINES", "").split()]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:

@@ -10,6 +10,17 @@
 //                                                                               -- advantage_kernel
 // (REINFORCE++-style globally normalised returns; reading n5).  Both kernels are
 // HBM-bound elementwise/scan work; no tensor cores.
+//
+// returns_kernel: one segmented backward scan over each rank's token buffer.  Token t carries
+// the affine map x -> v_t + g_t x with v_t = m_t r_t and g_t = 0 if t is the last token of its
+// sequence, else gamma; G_t is the composition of the maps of t..end applied to 0.  The buffer
+// is cut into aligned windows of up to 4096 tokens; a warp claims windows right to left from
+// an atomic counter and streams its window twice in 512-token batches (16 contiguous tokens
+// per lane: 4 float4 + 1 uint4 loads, register double buffer): pass 1 composes the window's map and publishes it, a lane-parallel
+// look-back over the windows to its right stops at the first inclusive value or zero slope (a
+// sequence end), pass 2 re-reads the window from L2 and writes G with float4 stores.  HBM sees
+// every token read and written once; long sequences are spread over many warps (decoupled
+// look-back).
 #include "earl_internal.cuh"
 
 namespace earl {
@@ -17,113 +28,418 @@ namespace earl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kTokPerLane = 8;
-constexpr int kTile = 32 * kTokPerLane;
+constexpr int kTokLane = 16;              // contiguous tokens of a lane in a batch
+constexpr int kBatch = 32 * kTokLane;     // 512 tokens per batch
+constexpr int kMaxNB = 8;                 // batches per window (at most)
+constexpr int kMaxWin = kBatch * kMaxNB;  // 4096 tokens
+constexpr int kWarps = 8;                 // warps per CTA
+#ifndef EARL_AGG_CTAS_PER_SM
+#define EARL_AGG_CTAS_PER_SM 3
+#endif
+constexpr int kCtasPerSm = EARL_AGG_CTAS_PER_SM;
 
-// Source ranks of the launch, each with its sequence count and the start of its sequences in
-// the group order (SP = 1: rank = rank0 + g*TP + t, group g).
+__device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
+  if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
+}
+
+__device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_word(uint64_t* p, uint32_t tag, float x) {
+  const uint64_t v = ((uint64_t)tag << 32) | __float_as_uint(x);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ bool word_is(uint64_t w, uint32_t tag) { return (uint32_t)(w >> 32) == tag; }
+__device__ __forceinline__ float word_val(uint64_t w) { return __uint_as_float((uint32_t)w); }
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// L2 prefetch of batch b of a window (token bytes, then mask bytes): lanes 0..15 take the 16
+// lines of rewards, lanes 16..19 the 4 lines of mask
+__device__ __forceinline__ void prefetch_batch(const float* rw, const uint8_t* mk, int64_t t0,
+                                               int64_t w1, int lane) {
+  if (lane < 16) {
+    const int64_t t = t0 + 32 * lane;
+    if (t < w1) prefetch_l2(rw + t);
+  } else if (lane < 20) {
+    const int64_t t = t0 + 128 * (lane - 16);
+    if (t < w1) prefetch_l2(mk + t);
+  }
+}
+
+__device__ __forceinline__ bool aligned(const void* p, unsigned a) {
+  return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0;
+}
+
+// Source ranks of the launch (SP = 1: rank = rank0 + g*TP + t holds group g whole).
 struct RankTable {
   int n;
+  int nb;                           // batches per window of this launch
   int rank[kMaxWorld];
-  int g[kMaxWorld];
   int t[kMaxWorld];
-  int64_t count[kMaxWorld];   // sequences of the rank
-  int64_t start[kMaxWorld];   // first work item of the rank
-  int64_t gstart[kMaxWorld];  // first position of group g in the sorted order
+  int64_t gs[kMaxWorld];            // first sorted position of the rank's group
+  int64_t cnt[kMaxWorld];           // sequences of the rank
+  int64_t ntok[kMaxWorld];          // tokens of the rank
+  int64_t wbeg[kMaxWorld + 1];      // first window (work unit) of the rank
 };
 
-__device__ void rank_table(const AggArgs& a, RankTable& rt) {
+// The window size adapts to the batch: 4096 tokens once there are two windows per warp of
+// the grid, down to one 512-token batch for small batches (every warp busy, short chains).
+__device__ void rank_table(const AggArgs& a, RankTable& rt, int64_t warps) {
   const PlanHeader* h = a.hdr;
   const LayoutDesc& S = a.plan.lay[0];
   rt.n = 0;
-  int64_t acc = 0;
+  int64_t batches = 0;
   for (int r = 0; r < a.world; ++r) {
     if (a.view_rank >= 0 && r != a.view_rank) continue;
     const int q = r - S.rank0;
     if (q < 0 || q >= S.dp * S.tp) continue;
-    const int g = q / S.tp, t = q % S.tp;
-    rt.rank[rt.n] = r;
-    rt.g[rt.n] = g;
-    rt.t[rt.n] = t;
-    rt.count[rt.n] = h->group_count[0][g];
-    rt.gstart[rt.n] = h->group_start[0][g];
-    rt.start[rt.n] = acc;
-    acc += rt.count[rt.n];
-    ++rt.n;
+    const int g = q / S.tp;
+    const int n = rt.n;
+    rt.rank[n] = r;
+    rt.t[n] = q % S.tp;
+    rt.gs[n] = h->group_start[0][g];
+    rt.cnt[n] = h->group_count[0][g];
+    rt.ntok[n] = h->shard_tokens[0][g];
+    batches += (rt.ntok[n] + kBatch - 1) / kBatch;
+    rt.n = n + 1;
+  }
+  rt.nb = (int)max((int64_t)1, min((int64_t)kMaxNB, batches / (2 * warps)));
+  const int64_t win = (int64_t)kBatch * rt.nb;
+  rt.wbeg[0] = 0;
+  for (int n = 0; n < rt.n; ++n) rt.wbeg[n + 1] = rt.wbeg[n] + (rt.ntok[n] + win - 1) / win;
+}
+
+// Smallest p in [lo, hi] with cum[p] - base >= key (cum[hi] - base >= key holds): 32-ary
+// warp search, one gather per level.
+__device__ int64_t first_at_least(const int64_t* cum, int64_t base, int64_t lo, int64_t hi,
+                                  int64_t key, int lane) {
+  while (hi - lo >= 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    int64_t p = lo + (int64_t)lane * step;
+    if (p > hi) p = hi;
+    const unsigned b = __ballot_sync(kFull, cum[p] - base >= key);
+    if (b == 0) {
+      lo = lo + 31 * step + 1;
+    } else {
+      const int f = __ffs(b) - 1;
+      const int64_t pf = min(lo + (int64_t)f * step, hi);
+      lo = f ? lo + (int64_t)(f - 1) * step + 1 : lo;
+      hi = pf;
+    }
+  }
+  const int64_t p = lo + lane;
+  const unsigned b = __ballot_sync(kFull, p <= hi && cum[min(p, hi)] - base >= key);
+  return lo + (__ffs(b) - 1);
+}
+
+// In-order composition of the 32 lane maps (lane l's map applies after lane l+1's):
+// (rS, rP) = exclusive suffix (lanes right of this one), (tS, tP) = all 32 lanes.
+__device__ __forceinline__ void warp_compose(float S, float P, int lane, float& rS, float& rP,
+                                             float& tS, float& tP) {
+  float sS = S, sP = P;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float oS = __shfl_down_sync(kFull, sS, off), oP = __shfl_down_sync(kFull, sP, off);
+    if (lane + off < 32) { sS = sS + sP * oS; sP = sP * oP; }
+  }
+  rS = __shfl_down_sync(kFull, sS, 1);
+  rP = __shfl_down_sync(kFull, sP, 1);
+  if (lane == 31) { rS = 0.f; rP = 1.f; }
+  tS = __shfl_sync(kFull, sS, 0);
+  tP = __shfl_sync(kFull, sP, 0);
+}
+
+// A lane's 16 tokens of a batch.  Tokens past the buffer load as r = 0, m = 0: they add nothing
+// and sit right of the buffer's last token, which ends its sequence, so their slopes are moot.
+struct Batch {
+  float4 r[4];
+  uint4 m;  // the 16 mask bytes
+};
+
+template <bool kLastUse>
+__device__ __forceinline__ void load_batch(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
+                                           int64_t w1, bool vec) {
+  if (vec && t + kTokLane <= w1) {
+    const float4* rp = reinterpret_cast<const float4*>(rw + t);
+    const uint4* mp = reinterpret_cast<const uint4*>(mk + t);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) B.r[k] = kLastUse ? __ldcs(rp + k) : __ldca(rp + k);
+    B.m = kLastUse ? __ldcs(mp) : __ldca(mp);
+  } else {
+    float x[kTokLane];
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < kTokLane; ++i) {
+      x[i] = 0.f;
+      if (t + i < w1) {
+        x[i] = rw[t + i];
+        m[i >> 2] |= (uint32_t)mk[t + i] << (8 * (i & 3));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) B.r[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+    B.m = make_uint4(m[0], m[1], m[2], m[3]);
   }
 }
 
-// One warp per (rank, sequence) work item; the sequence is walked backwards in tiles of 256
-// tokens: every lane reduces its 8 tokens to the affine map x -> S + gamma^8 x, a warp suffix
-// scan composes the maps of the lanes to its right, then each lane emits its 8 returns.
-__global__ void __launch_bounds__(256) returns_kernel(const __grid_constant__ AggArgs a) {
+__device__ __forceinline__ float tok_r(const Batch& B, int i) {
+  const float4& v = B.r[i >> 2];
+  const int c = i & 3;
+  return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
+}
+
+__device__ __forceinline__ bool tok_m(const Batch& B, int i) {
+  const int k = i >> 2;
+  const uint32_t w = k == 0 ? B.m.x : k == 1 ? B.m.y : k == 2 ? B.m.z : B.m.w;
+  return (w >> (8 * (i & 3))) & 0xffu;
+}
+
+// v_t = m_t r_t with the boolean mask (reading n5)
+__device__ __forceinline__ float tok_v(const Batch& B, int i) { return tok_m(B, i) ? tok_r(B, i) : 0.f; }
+
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
-  if (threadIdx.x == 0) rank_table(a, rt);
+  __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
+  __shared__ float2 bmap[kWarps][kMaxNB];   // per batch: its map (pass 1), then its carry
+  __shared__ double red[3][kWarps];
+  __shared__ uint32_t s_tag;
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    rank_table(a, rt, (int64_t)gridDim.x * kWarps);
+    s_tag = (*(volatile uint32_t*)&a.ws->epoch + 1u) << 2;  // | 1 aggregate, | 2 inclusive
+    s_ok = rt.wbeg[rt.n] <= a.win_cap;
+    if (!s_ok && blockIdx.x == 0)
+      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(rt.wbeg[rt.n], (int64_t)INT32_MAX));
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t total = rt.n ? rt.start[rt.n - 1] + rt.count[rt.n - 1] : 0;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int wid = threadIdx.x >> 5;
+  const uint32_t tag = s_tag;
+  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
+  const int NB = rt.nb;
+  const int64_t win = (int64_t)kBatch * NB;
   const float gamma = a.gamma;
+  float g16 = 1.f;  // gamma^16: the slope of a lane's 16 tokens without a sequence end
+#pragma unroll
+  for (int i = 0; i < kTokLane; ++i) g16 *= gamma;
+  uint32_t* bm = ends_bm[wid];
+  float2* bmp = bmap[wid];
   double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
-  for (int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < total;
-       item += nwarps) {
+
+  // windows are claimed in increasing order and every window only waits on smaller ones, so
+  // holding the next claim while processing the current one cannot deadlock
+  uint32_t next = 0;
+  if (lane == 0) next = atomicAdd(&a.ws->work_ctr, 1u);
+  while (true) {
+    const int64_t u = __shfl_sync(kFull, next, 0);
+    if (u >= total) break;
+    if (lane == 0) next = atomicAdd(&a.ws->work_ctr, 1u);
     int ri = 0;
-    while (ri + 1 < rt.n && item >= rt.start[ri + 1]) ++ri;
+    while (u >= rt.wbeg[ri + 1]) ++ri;
     const int r = rt.rank[ri];
-    const int64_t pos = rt.gstart[ri] + (item - rt.start[ri]);
-    const int i = a.plan.perm[0][pos];
-    const int64_t L = a.plan.lens[i];
-    const int64_t o = a.plan.off[0][i];  // SP = 1: chunk 0 is the whole sequence
-    const float* rw = a.rewards[r] + o;
-    const uint8_t* mk = a.mask[r] + o;
-    float* G = a.returns[r] + o;
-    const bool count_stats = rt.t[ri] == 0;
-    float carry = 0.f;  // G of the first token right of the current tile
-    for (int64_t tile_end = L; tile_end > 0; tile_end -= kTile) {
-      const int64_t tile_beg = tile_end > kTile ? tile_end - kTile : 0;
-      const int64_t t0 = tile_beg + (int64_t)lane * kTokPerLane;
-      float v[kTokPerLane];
+    const int64_t nwin = rt.wbeg[ri + 1] - rt.wbeg[ri];
+    const int64_t w = nwin - 1 - (u - rt.wbeg[ri]);  // right to left within the rank
+    const int64_t w0 = w * win;
+    const int64_t w1 = min(rt.ntok[ri], w0 + win);
+    const int nb = (int)((w1 - w0 + kBatch - 1) / kBatch);
+    const float* rw = a.rewards[r];
+    const uint8_t* mk = a.mask[r];
+    float* G = a.returns[r];
+    const bool vec = aligned(rw, 16) && aligned(G, 16) && aligned(mk, 16);
+    const int64_t lt = w0 + (int64_t)kTokLane * lane;  // this lane's tokens in batch b: lt + 512 b
+
+    Batch cur, nxt;
+    load_batch<false>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
+    if (nb >= 2) load_batch<false>(nxt, rw, mk, lt + (int64_t)(nb - 2) * kBatch, w1, vec);
+    if (nb >= 3) prefetch_batch(rw, mk, w0 + (int64_t)(nb - 3) * kBatch, w1, lane);
+
+    // sequence ends inside the window: token s-1 for every sequence start s in (w0, w1]
+    // (starts are cum[0][p] - cum[0][gs], p in [gs, gs+cnt]; the last one ends the buffer)
+    const int64_t* cum = a.plan.cum[0];
+    const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
+    const int64_t base = cum[gs];
+    for (int j = lane; j < nb * (kBatch / 32); j += 32) bm[j] = 0u;
+    __syncwarp();
+    const int64_t lo = first_at_least(cum, base, gs, pend, w0, lane);
+    for (int64_t p0 = lo;; p0 += 32) {
+      const int64_t p = p0 + lane;
+      const int64_t s = p <= pend ? cum[p] - base : INT64_MAX;
+      const bool in = s <= w1;
+      if (in && s > w0) atomicOr(&bm[(s - 1 - w0) >> 5], 1u << ((s - 1 - w0) & 31));
+      if (__ballot_sync(kFull, in) != kFull) break;
+    }
+    __syncwarp();
+    // bit i: token i of this lane's 16 in batch b ends its sequence
+    auto ends16 = [&](int b) { return (bm[16 * b + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu; };
+
+    // pass 1: batch maps (kept in shared memory) and the window's map; batch b-1 is in flight
+    // in registers and batch b-2 in L2 while batch b is composed
+    float wS = 0.f, wP = 1.f;
+#pragma unroll 1
+    for (int b = nb - 1; b >= 0; --b) {
+      if (b >= 3) prefetch_batch(rw, mk, w0 + (int64_t)(b - 3) * kBatch, w1, lane);
+      const uint32_t e = ends16(b);
+      float S = 0.f;
 #pragma unroll
-      for (int k = 0; k < kTokPerLane; ++k) {
-        const int64_t tt = t0 + k;
-        v[k] = (tt < tile_end) ? rw[tt] * (float)mk[tt] : 0.f;
+      for (int i = kTokLane - 1; i >= 0; --i) {
+        const float v = tok_v(cur, i);
+        S = ((e >> i) & 1u) ? v : fmaf(gamma, S, v);
       }
-      // lane's own map: S = sum_k gamma^k v[k] (over its valid tokens), P = gamma^(#valid)
+      float rS, rP, bS, bP;
+      warp_compose(S, e ? 0.f : g16, lane, rS, rP, bS, bP);
+      if (lane == 0) bmp[b] = make_float2(bS, bP);
+      wS = bS + bP * wS;
+      wP = bP * wP;
+      cur = nxt;
+      if (b >= 2) load_batch<false>(nxt, rw, mk, lt + (int64_t)(b - 2) * kBatch, w1, vec);
+    }
+
+    // publish the window's map, then look back (32 windows per round trip) for the carry:
+    // compose the maps of windows w+1, w+2, ... up to the first inclusive value or zero slope
+    AggWindow* W = a.win + rt.wbeg[ri];
+    if (lane == 0 && w + 1 < nwin) {
+      st_word(&W[w].S, tag | 1u, wS);
+      st_word(&W[w].P, tag | 1u, wP);
+    }
+    float cS = 0.f, cP = 1.f;
+    for (int64_t j0 = w + 1; j0 < nwin;) {
+      const int64_t j = j0 + lane;
+      bool ready = false, stop = false;
       float S = 0.f, P = 1.f;
-#pragma unroll
-      for (int k = kTokPerLane - 1; k >= 0; --k) {
-        if (t0 + k < tile_end) { S = v[k] + gamma * S; P *= gamma; }
-      }
-      // suffix composition over lanes > lane: (S1,P1) o (S2,P2) = (S1 + P1 S2, P1 P2)
-      float sS = S, sP = P;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const float oS = __shfl_down_sync(kFull, sS, off), oP = __shfl_down_sync(kFull, sP, off);
-        if (lane + off < 32) { sS = sS + sP * oS; sP = sP * oP; }
-      }
-      // exclusive suffix: the map of lanes right of this one, applied to the tile's carry
-      float rS = __shfl_down_sync(kFull, sS, 1), rP = __shfl_down_sync(kFull, sP, 1);
-      if (lane == 31) { rS = 0.f; rP = 1.f; }
-      float g_next = rS + rP * carry;
-#pragma unroll
-      for (int k = kTokPerLane - 1; k >= 0; --k) {
-        const int64_t tt = t0 + k;
-        if (tt < tile_end) {
-          const float gk = v[k] + gamma * g_next;
-          G[tt] = gk;
-          if (count_stats && mk[tt]) {
-            s_m += 1.0;
-            s_g += (double)gk;
-            s_g2 += (double)gk * (double)gk;
+      if (j < nwin) {
+        const uint64_t wi = ld_word(&W[j].inc);
+        if (word_is(wi, tag | 2u)) {
+          ready = stop = true;
+          S = word_val(wi);
+          P = 0.f;
+        } else {
+          const uint64_t ws = ld_word(&W[j].S), wp = ld_word(&W[j].P);
+          if (word_is(ws, tag | 1u) && word_is(wp, tag | 1u)) {
+            ready = true;
+            S = word_val(ws);
+            P = word_val(wp);
+            stop = P == 0.f;
           }
-          g_next = gk;
         }
       }
-      carry = __shfl_sync(kFull, sS + sP * carry, 0);
+      // usable prefix: ready lanes up to (and including) the first stopper
+      const unsigned rmask = __ballot_sync(kFull, ready);
+      const unsigned smask = __ballot_sync(kFull, stop);
+      const int n_ready = (~rmask) ? __ffs(~rmask) - 1 : 32;
+      const int first_stop = smask ? __ffs(smask) - 1 : 32;
+      const int n_use = min(n_ready, first_stop + 1);
+      if (n_use == 0) { __nanosleep(32); continue; }
+      if (lane >= n_use) { S = 0.f; P = 1.f; }
+      float rS, rP, tS, tP;
+      warp_compose(S, P, lane, rS, rP, tS, tP);
+      cS = cS + cP * tS;
+      cP = cP * tP;
+      if (cP == 0.f || first_stop < n_use) break;
+      j0 += n_use;
     }
-    if (lane == 0 && a.seq_return != nullptr && a.seq_return[r] != nullptr)
-      a.seq_return[r][item - rt.start[ri]] = (L > 0) ? G[0] : 0.f;
+    const float carry = cS;  // past the buffer end: G = 0
+    if (lane == 0) {
+      st_word(&W[w].inc, tag | 2u, wS + wP * carry);
+      float c = carry;  // carries into the batches, right to left
+      for (int b = nb - 1; b >= 0; --b) {
+        const float2 m = bmp[b];
+        bmp[b] = make_float2(c, 0.f);
+        c = m.x + m.y * c;
+      }
+    }
+    __syncwarp();
+
+    // pass 2: returns (the window's second read hits L2), float4 stores, statistics; the head
+    // of the next claimed window is prefetched meanwhile
+    const bool count_stats = rt.t[ri] == 0;
+    load_batch<true>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
+    {
+      const int64_t un = __shfl_sync(kFull, next, 0);
+      if (un < total) {
+        int rn = 0;
+        while (un >= rt.wbeg[rn + 1]) ++rn;
+        const int64_t wn = rt.wbeg[rn + 1] - 1 - un;
+        const int64_t n0 = wn * win, n1 = min(rt.ntok[rn], n0 + win);
+        const int64_t top = n0 + ((n1 - n0 - 1) / kBatch) * kBatch;  // its first (rightmost) batch
+        prefetch_batch(a.rewards[rt.rank[rn]], a.mask[rt.rank[rn]], top, n1, lane);
+        if (top - kBatch >= n0) prefetch_batch(a.rewards[rt.rank[rn]], a.mask[rt.rank[rn]], top - kBatch, n1, lane);
+      }
+    }
+#pragma unroll 1
+    for (int b = nb - 1; b >= 0; --b) {
+      if (b > 0) load_batch<true>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
+      const uint32_t e = ends16(b);
+      float S = 0.f;
+#pragma unroll
+      for (int i = kTokLane - 1; i >= 0; --i) {
+        const float v = tok_v(cur, i);
+        S = ((e >> i) & 1u) ? v : fmaf(gamma, S, v);
+      }
+      float rS, rP, tS, tP;
+      warp_compose(S, e ? 0.f : g16, lane, rS, rP, tS, tP);
+      float g_next = rS + rP * bmp[b].x;
+      float out[kTokLane];
+      float sg = 0.f, sg2 = 0.f;
+      int cnt = 0;
+#pragma unroll
+      for (int i = kTokLane - 1; i >= 0; --i) {
+        const bool m = tok_m(cur, i);
+        const float v = m ? tok_r(cur, i) : 0.f;
+        out[i] = ((e >> i) & 1u) ? v : fmaf(gamma, g_next, v);
+        g_next = out[i];
+        if (m) { sg += out[i]; sg2 = fmaf(out[i], out[i], sg2); ++cnt; }
+      }
+      if (count_stats) { s_m += (double)cnt; s_g += (double)sg; s_g2 += (double)sg2; }
+      const int64_t t = lt + (int64_t)b * kBatch;
+      if (vec && t + kTokLane <= w1) {
+        float4* gp = reinterpret_cast<float4*>(G + t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          __stcs(gp + k, make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i)
+          if (t + i < w1) G[t + i] = out[i];
+      }
+      cur = nxt;
+    }
+
+    // per-sequence return G_0 of the sequences starting in the window (zero-length sequences
+    // at the buffer end belong to the last window)
+    float* SR = a.seq_return[r];
+    if (SR != nullptr) {
+      __syncwarp();
+      for (int64_t p0 = lo;; p0 += 32) {
+        const int64_t p = p0 + lane;
+        bool in = false;
+        if (p < pend) {
+          const int64_t s = cum[p] - base;
+          const int64_t L = cum[p + 1] - base - s;
+          in = s < w1 || (s == w1 && w1 == rt.ntok[ri]);
+          if (in) SR[p - gs] = L > 0 ? G[s] : 0.f;
+        }
+        if (__ballot_sync(kFull, in) != kFull) break;
+      }
+    }
+    __syncwarp();
   }
+
+  // ranks without tokens still owe their (zero-length) sequences a return
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    for (int ri = 0; ri < rt.n; ++ri) {
+      float* SR = a.seq_return[rt.rank[ri]];
+      if (SR == nullptr || rt.ntok[ri] != 0) continue;
+      for (int64_t j = lane; j < rt.cnt[ri]; j += 32) SR[j] = 0.f;
+    }
+  }
+
   // warp, then block reduction of the fp64 partials; one atomic per block
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -131,23 +447,44 @@ __global__ void __launch_bounds__(256) returns_kernel(const __grid_constant__ Ag
     s_g += __shfl_xor_sync(kFull, s_g, off);
     s_g2 += __shfl_xor_sync(kFull, s_g2, off);
   }
-  __shared__ double red[3][8];
-  const int w = threadIdx.x >> 5;
-  if (lane == 0) { red[0][w] = s_m; red[1][w] = s_g; red[2][w] = s_g2; }
+  if (lane == 0) { red[0][wid] = s_m; red[1][wid] = s_g; red[2][wid] = s_g2; }
   __syncthreads();
   if (threadIdx.x < 3) {
     double acc = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) acc += red[threadIdx.x][k];
+    for (int k = 0; k < kWarps; ++k) acc += red[threadIdx.x][k];
     if (acc != 0.0) atomicAdd(a.partial + threadIdx.x, acc);
+  }
+  // the last CTA out resets the claim counter and advances the epoch (no host reset between
+  // launches or graph replays)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.ws->fin_ctr, 1u) == gridDim.x - 1) {
+      a.ws->work_ctr = 0;
+      a.ws->fin_ctr = 0;
+      a.ws->epoch = a.ws->epoch + 1u;
+      __threadfence();
+    }
   }
 }
 
-// A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks.
+// A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks: one
+// flattened stream of 4-token quads over all ranks (4 quads in flight per thread), then the
+// unaligned remainders token by token.
 __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
+  __shared__ int64_t qbeg[kMaxWorld + 1];   // vector quads of the ranks (prefix)
+  __shared__ int64_t tbeg[kMaxWorld + 1];   // scalar remainder tokens of the ranks (prefix)
   __shared__ float s_mu, s_inv;
   if (threadIdx.x == 0) {
-    rank_table(a, rt);
+    rank_table(a, rt, 1);
+    qbeg[0] = tbeg[0] = 0;
+    for (int ri = 0; ri < rt.n; ++ri) {
+      const int r = rt.rank[ri];
+      const bool vec = aligned(a.returns[r], 16) && aligned(a.adv[r], 16) && aligned(a.mask[r], 4);
+      const int64_t nq = vec ? rt.ntok[ri] >> 2 : 0;
+      qbeg[ri + 1] = qbeg[ri] + nq;
+      tbeg[ri + 1] = tbeg[ri] + rt.ntok[ri] - 4 * nq;
+    }
     const double n = a.stats[0];
     const double mu = n > 0 ? a.stats[1] / n : 0.0;
     double var = n > 0 ? a.stats[2] / n - mu * mu : 0.0;
@@ -157,22 +494,55 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
   }
   __syncthreads();
   const float mu = s_mu, inv = s_inv;
-  for (int ri = 0; ri < rt.n; ++ri) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t Q = qbeg[rt.n];
+  constexpr int kU = 4;
+  for (int64_t q0 = tid; q0 < Q; q0 += kU * stride) {
+    float4 g[kU];
+    uint32_t m[kU];
+    int rr[kU];
+    int64_t qq[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t q = q0 + u * stride;
+      rr[u] = -1;
+      if (q < Q) {
+        int ri = 0;
+        while (q >= qbeg[ri + 1]) ++ri;
+        rr[u] = rt.rank[ri];
+        qq[u] = q - qbeg[ri];
+        g[u] = __ldcs(reinterpret_cast<const float4*>(a.returns[rr[u]]) + qq[u]);
+        m[u] = __ldcs(reinterpret_cast<const unsigned int*>(a.mask[rr[u]]) + qq[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (rr[u] < 0) continue;
+      float4 o;
+      o.x = (m[u] & 0xffu) ? (g[u].x - mu) * inv : 0.f;
+      o.y = (m[u] & 0xff00u) ? (g[u].y - mu) * inv : 0.f;
+      o.z = (m[u] & 0xff0000u) ? (g[u].z - mu) * inv : 0.f;
+      o.w = (m[u] & 0xff000000u) ? (g[u].w - mu) * inv : 0.f;
+      __stcs(reinterpret_cast<float4*>(a.adv[rr[u]]) + qq[u], o);
+    }
+  }
+  const int64_t Tt = tbeg[rt.n];
+  for (int64_t j = tid; j < Tt; j += stride) {
+    int ri = 0;
+    while (j >= tbeg[ri + 1]) ++ri;
     const int r = rt.rank[ri];
-    const int64_t ntok = a.hdr->shard_tokens[0][rt.g[ri]];
-    const float* G = a.returns[r];
-    const uint8_t* mk = a.mask[r];
-    float* A = a.adv[r];
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < ntok;
-         t += (int64_t)gridDim.x * blockDim.x)
-      A[t] = mk[t] ? (G[t] - mu) * inv : 0.f;
+    const int64_t t = rt.ntok[ri] - (tbeg[ri + 1] - j);  // the remainder is the rank's tail
+    a.adv[r][t] = a.mask[r][t] ? (a.returns[r][t] - mu) * inv : 0.f;
   }
 }
 
 }  // namespace
 
+int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWin + 16384; }
+
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
-  returns_kernel<<<sm_count * 4, 256, 0, s>>>(a);
+  returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 

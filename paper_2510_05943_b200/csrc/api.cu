@@ -107,6 +107,8 @@ struct earl_plan {
   PlanHeader host_hdr{};
   size_t lpt_smem = 0;
   int grid = 1;
+  void* agg_ws = nullptr;     // returns_kernel look-back workspace (AggWork + AggWindow[agg_cap])
+  int64_t agg_cap = 0;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -704,6 +706,7 @@ extern "C" earl_status_t earl_plan_destroy(earl_plan_t p) {
   {
     DeviceGuard g(p->comm->device);
     if (p->mem) cudaFreeAsync(p->mem, p->stream);
+    if (p->agg_ws) cudaFree(p->agg_ws);
     if (p->ev) cudaEventDestroy(p->ev);
     cudaGetLastError();
   }
@@ -1001,6 +1004,29 @@ earl_status_t agg_args(earl_plan_t p, AggArgs& a) {
   return EARL_OK;
 }
 
+// The look-back workspace of returns_kernel: allocated (zeroed) on first use, outside any graph
+// capture, for at least 2^20 windows (2^30 tokens per source rank set) or the plan's known token
+// count; the kernel latches EARL_ERR_CAPACITY in the plan header beyond it.
+earl_status_t agg_workspace(earl_plan_t p, cudaStream_t s) {
+  int64_t need = int64_t(1) << 20;
+  if (p->synced) need = std::max(need, returns_windows(p->host_hdr.T) + kMaxWorld);
+  if (p->agg_ws && p->agg_cap >= need) return EARL_OK;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(EARL_ERR_UNSUPPORTED,
+                "the first earl_returns on a plan allocates its workspace: call it once before graph capture");
+  if (p->agg_ws) {
+    CUDA_TRY(cudaFree(p->agg_ws));
+    p->agg_ws = nullptr;
+  }
+  const size_t bytes = sizeof(AggWork) + sizeof(AggWindow) * (size_t)need;
+  CUDA_TRY(cudaMalloc(&p->agg_ws, bytes));
+  p->agg_cap = need;
+  CUDA_TRY(cudaMemsetAsync(p->agg_ws, 0, bytes, s));
+  return EARL_OK;
+}
+
 template <class T>
 earl_status_t set_per_rank(earl_plan_t p, T** dst, const void* const* src, const char* what,
                            bool required) {
@@ -1035,6 +1061,10 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
     return st;
   DeviceGuard g(p->comm->device);
   clear_stale_error();
+  if ((st = agg_workspace(p, static_cast<cudaStream_t>(stream))) != EARL_OK) return st;
+  a.ws = static_cast<AggWork*>(p->agg_ws);
+  a.win = reinterpret_cast<AggWindow*>(a.ws + 1);
+  a.win_cap = p->agg_cap;
   cudaError_t e = launch_returns(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "returns launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);

@@ -139,7 +139,26 @@ constexpr int kDoneSlot = 8;
 constexpr int kEpochSlot = 16;  // this rank's exec epoch (written by its own entry barrier)
 
 // NEXT-2 (aggregate.cu): returns / advantages on the source ranks (SP = 1)
+// returns_kernel look-back state: one descriptor per token window of a source rank.  Each word
+// is {tag << 32 | float bits}, tag = (epoch << 2) | kind, written with one 64-bit store and
+// validated on its own by the reader: no fences between the value and its flag.
+struct AggWindow {
+  uint64_t S;    // kind 1: the window's map x -> S + P x ...
+  uint64_t P;    // ... (both words must carry the current tag)
+  uint64_t inc;  // kind 2: G at the window's first token
+  uint64_t pad;
+};
+struct AggWork {
+  uint32_t work_ctr;  // window claims (reset by the last CTA)
+  uint32_t fin_ctr;   // finished CTAs
+  uint32_t epoch;     // launches so far: flags of older launches never match
+  uint32_t pad;
+};
+
 struct AggArgs {
+  AggWork* ws;
+  AggWindow* win;
+  int64_t win_cap;
   PlanArgs plan;
   const PlanHeader* hdr;
   int32_t world;
@@ -156,6 +175,7 @@ struct AggArgs {
 
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
+int64_t returns_windows(int64_t tokens);
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);

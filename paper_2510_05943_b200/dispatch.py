@@ -257,3 +257,23 @@ def plan_seq_fields(comm, token_plan, src, dst, sfields, device, stream=None):
     sp = comm.plan(fold_layout(src, gs), fold_layout(dst, gd), ones, sfields, stream)
     sp._keep = (gs, gd, ones)
     return sp
+
+
+def distributed_advantages(dispatcher, plan, gamma, rewards, mask, returns, adv, eps=1e-8,
+                           seq_return=None, stream=None):
+    """NEXT-2 (reading n5) on one process per GPU: discounted returns where the rollout holds
+    the tokens, a 3-double all-reduce of the masked-token statistics (no controller gathers any
+    reward), then the normalised advantages.  rewards fp32 / mask u8 / returns, adv fp32 are this
+    rank's token tensors; returns the reduced statistics (sum m, sum m G, sum m G^2)."""
+    dist = dispatcher.dist
+    partial = torch.zeros(3, dtype=torch.float64, device=dispatcher.device)
+    plan.returns(gamma, [rewards], [mask], [returns], partial,
+                 seq_return=[seq_return] if seq_return is not None else None, stream=stream)
+    if dist.get_backend(dispatcher.group) == "nccl":
+        dist.all_reduce(partial, group=dispatcher.group)
+    else:
+        host = partial.cpu()
+        dist.all_reduce(host, group=dispatcher.group)
+        partial.copy_(host)
+    plan.advantages(partial, eps, [returns], [mask], [adv], stream=stream)
+    return partial

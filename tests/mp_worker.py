@@ -95,3 +95,49 @@ def gpu_main(rank, world, port, q, case):
         q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_adv_main(rank, world, port, q, case):
+    """Reading n5 with one process per rank: returns on each rank, 3-double all-reduce over the
+    process group, advantages -- equal to the oracle within the fp32 tolerance."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher, distributed_advantages
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, src, gamma = case
+        T = sum(lens)
+        rng = np.random.default_rng(5)
+        glob_r = rng.standard_normal(T).astype(np.float32)
+        glob_m = (rng.random(T) < 0.75).astype(np.uint8)
+        fr = [("r", 4, 1, "x"), ("m", 1, 1, "x")]
+        arrs = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens),
+                                         [glob_r.view(np.uint8), glob_m], fr)
+        rewards = {k: v[0].view(np.float32) for k, v in arrs.items()}
+        masks = {k: v[1] for k, v in arrs.items()}
+        G, A, R, stats = O.distributed_advantages(src, lens, rewards, masks, gamma, 1e-8, world)
+        D = Dispatcher(window_bytes=1 << 20, device=0)
+        plan = D.plan(src, W.layout(dp=1, tp=world, assign="contig"),
+                      torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda(), W.field_set("tiny3"))
+        n = rewards[rank].size
+        r = torch.from_numpy(rewards[rank].copy()).cuda()
+        m = torch.from_numpy(masks[rank].copy()).cuda()
+        Gd = torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+        Ad = torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+        got = distributed_advantages(D, plan, gamma, r, m, Gd, Ad)
+        torch.cuda.synchronize()
+        assert got[0].item() == stats[0]
+        gmax = max(np.abs(G[k]).max() if G[k].size else 0 for k in G)
+        atol = 4 * 2.0 ** -24 * max(lens) * gmax + 1e-6
+        sigma = np.sqrt(max(stats[2] / stats[0] - (stats[1] / stats[0]) ** 2, 0))
+        assert np.allclose(Gd[:n].cpu().numpy(), G[rank], rtol=0, atol=atol)
+        assert np.allclose(Ad[:n].cpu().numpy(), A[rank], rtol=0, atol=atol / sigma + 1e-5)
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

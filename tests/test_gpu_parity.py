@@ -510,3 +510,102 @@ def test_returns_need_whole_sequences():
     with pytest.raises(EarlError) as e:
         plan.returns(1.0, [None, None], [None, None], [None, None], p)
     assert e.value.name == "EARL_ERR_UNSUPPORTED"
+
+
+def _adv_case(lens, src, gamma, world, shift=0, repeats=1, graph=False, seed=0):
+    """Run earl_returns + earl_advantages (emulated comm) and compare with the fp64 oracle.
+    shift > 0 offsets every device buffer by `shift` elements (the unaligned scalar path)."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    rng = np.random.default_rng(seed)
+    T = sum(lens)
+    glob_r = rng.standard_normal(T).astype(np.float32)
+    glob_m = (rng.random(T) < 0.75).astype(np.uint8)
+    fr = [("r", 4, 1, "x"), ("m", 1, 1, "x")]
+    arrs = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens),
+                                     [glob_r.view(np.uint8), glob_m], fr)
+    rewards = {k: v[0].view(np.float32) for k, v in arrs.items()}
+    masks = {k: v[1] for k, v in arrs.items()}
+    G, A, R, stats = O.distributed_advantages(src, lens, rewards, masks, gamma, 1e-8, world)
+    ed = EmulatedDispatch(world)
+    plan = ed.plan(src, W.layout(dp=1, assign="contig"), lens, W.field_set("tiny3"))
+    dev = ed.device
+
+    def buf(host, dtype):
+        t = torch.zeros(host.size + shift + 4, dtype=dtype, device=dev)
+        t[shift:shift + host.size] = torch.from_numpy(host.copy()).to(dev)
+        return t[shift:]
+    empty_f = np.zeros(0, np.float32)
+    d_r = [buf(rewards.get(r, empty_f), torch.float32) for r in range(world)]
+    d_m = [buf(masks.get(r, np.zeros(0, np.uint8)), torch.uint8) for r in range(world)]
+    d_G = [buf(np.full(rewards.get(r, empty_f).size, np.nan, np.float32), torch.float32) for r in range(world)]
+    d_A = [buf(np.full(rewards.get(r, empty_f).size, np.nan, np.float32), torch.float32) for r in range(world)]
+    d_R = [buf(np.full(len(R.get(r, [])), np.nan, np.float32), torch.float32) for r in range(world)]
+    partial = torch.zeros(3, dtype=torch.float64, device=dev)
+
+    def step():
+        partial.zero_()
+        plan.returns(gamma, d_r, d_m, d_G, partial, seq_return=d_R)
+        plan.advantages(partial, 1e-8, d_G, d_m, d_A)
+    step()  # allocates the workspace outside any capture
+    if graph:
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            partial.zero_()
+            plan.returns(gamma, d_r, d_m, d_G, partial, seq_return=d_R,
+                         stream=torch.cuda.current_stream().cuda_stream)
+            plan.advantages(partial, 1e-8, d_G, d_m, d_A,
+                            stream=torch.cuda.current_stream().cuda_stream)
+        for x in d_G + d_A + d_R:
+            x.fill_(float("nan"))
+        for _ in range(repeats):
+            g.replay()
+    else:
+        for _ in range(repeats - 1):
+            step()
+    torch.cuda.synchronize()
+    plan.sync()
+    Lmax = max(lens) if lens else 1
+    horizon = Lmax if gamma >= 1.0 else min(Lmax, 1.0 / (1.0 - gamma))
+    gmax = max([np.abs(G[r]).max() for r in G if G[r].size] + [1.0])
+    atol_g = 4 * 2.0 ** -24 * horizon * gmax + 1e-6
+    got = partial.cpu().numpy()
+    assert got[0] == stats[0]
+    assert np.allclose(got[1:], stats[1:], rtol=1e-5, atol=atol_g * max(stats[0], 1))
+    sigma = np.sqrt(max(stats[2] / stats[0] - (stats[1] / stats[0]) ** 2, 0)) if stats[0] else 1.0
+    for r in G:
+        n_r = rewards[r].size
+        assert np.allclose(d_G[r][:n_r].cpu().numpy(), G[r], rtol=0, atol=atol_g), r
+        assert np.allclose(d_A[r][:n_r].cpu().numpy(), A[r], rtol=0, atol=atol_g / sigma + 1e-5), r
+        assert np.allclose(d_R[r][:len(R[r])].cpu().numpy(), R[r], rtol=0, atol=atol_g), r
+    plan.destroy()
+
+
+ADV_EDGE_CASES = {
+    # one 50K-token sequence: 49 windows chained through the look-back (gamma = 1: no decay)
+    "one_long": ([50_000], 1),
+    # lengths straddling the 1024-token window and the 4-token quad
+    "window_edges": ([1023, 1024, 1025, 1, 2, 3, 4, 5, 2047, 2048, 2049, 128, 127, 129], 2),
+    # zero-length sequences in the middle and at the end of a rank; a rank with only empties
+    "zeros": ([0, 7, 0, 0, 1500, 0, 0, 0, 0, 3, 0, 0], 4),
+    # thousands of 1..3-token sequences: many ends per window
+    "tiny": ([1 + (i % 3) for i in range(5000)], 8),
+}
+
+
+@pytest.mark.parametrize("case", sorted(ADV_EDGE_CASES))
+@pytest.mark.parametrize("gamma", [1.0, 0.9])
+@pytest.mark.parametrize("shift", [0, 1])
+def test_returns_edge_cases(case, gamma, shift):
+    lens, dp = ADV_EDGE_CASES[case]
+    src = W.layout(dp=dp, assign="given_counts", counts=W.near_equal_counts(len(lens), dp))
+    _adv_case(list(lens), src, gamma, 8, shift=shift, seed=len(lens))
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_returns_repeat_and_graph(graph):
+    """The look-back workspace is reused across launches and graph replays (device epoch)."""
+    lens = W.lognormal_lengths(200, 1500, 0.8, 1, 6000, seed=9).tolist()
+    _adv_case(lens, W.layout(dp=4, tp=2, assign="lpt"), 0.99, 8, repeats=5, graph=graph)

@@ -81,3 +81,16 @@ def test_p2p_exec_processes_share_one_gpu(name, mode):
         src = random_layout(rng, world, n, allow_lpt=True)
         dst = random_layout(rng, world, n, allow_lpt=True)
     run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 3, mode),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,tp", [(2, 1), (4, 2)])
+def test_distributed_advantages_processes(world, tp):
+    """Reading n5 across processes: the only cross-rank traffic is the 3-double all-reduce."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    lens = W.c2_lengths(0)[:48].tolist()
+    src = W.layout(dp=world // tp, tp=tp, assign="contig")
+    run_procs(mp_worker.gpu_adv_main, world, extra=((lens, src, 0.99),), timeout=600)

@@ -83,6 +83,9 @@ def test_discounted_returns_closed_forms():
     z[-1] = 3.0
     want = 3.0 * 0.9 ** (19 - np.arange(20))
     assert np.allclose(O.discounted_returns(z, np.ones(20), 0.9), want, rtol=1e-12)
+    # the mask is boolean (reading n5): a byte of 2 or 255 selects the reward like 1 does
+    m2 = m * np.where(rng.random(50) < 0.5, 2, 255).astype(np.uint8)
+    assert np.array_equal(O.discounted_returns(r, m2, 0.9), O.discounted_returns(r, m, 0.9))
 
 
 @pytest.mark.parametrize("seed", range(6))
