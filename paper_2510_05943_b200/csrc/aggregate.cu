@@ -30,7 +30,13 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTokLane = 16;              // contiguous tokens of a lane in a batch
 constexpr int kBatch = 32 * kTokLane;     // 512 tokens per batch
-constexpr int kMaxNB = 8;                 // batches per window (at most)
+#ifndef EARL_AGG_MAX_NB
+#define EARL_AGG_MAX_NB 8
+#endif
+#ifndef EARL_AGG_PF
+#define EARL_AGG_PF 0
+#endif
+constexpr int kMaxNB = EARL_AGG_MAX_NB;   // batches per window (at most)
 constexpr int kMaxWin = kBatch * kMaxNB;  // 4096 tokens
 constexpr int kWarps = 8;                 // warps per CTA
 #ifndef EARL_AGG_CTAS_PER_SM
@@ -163,6 +169,24 @@ struct Batch {
   uint4 m;  // the 16 mask bytes
 };
 
+// unaligned buffers or the rank's tail: token by token (rare; a rolled loop keeps it small)
+__device__ __forceinline__ void load_batch_scalar(Batch& B, const float* rw, const uint8_t* mk,
+                                                  int64_t t, int64_t w1) {
+  float x[kTokLane];
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 1
+  for (int i = 0; i < kTokLane; ++i) {
+    x[i] = 0.f;
+    if (t + i < w1) {
+      x[i] = rw[t + i];
+      m[i >> 2] |= (uint32_t)mk[t + i] << (8 * (i & 3));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) B.r[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+  B.m = make_uint4(m[0], m[1], m[2], m[3]);
+}
+
 template <bool kLastUse>
 __device__ __forceinline__ void load_batch(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
                                            int64_t w1, bool vec) {
@@ -173,20 +197,16 @@ __device__ __forceinline__ void load_batch(Batch& B, const float* rw, const uint
     for (int k = 0; k < 4; ++k) B.r[k] = kLastUse ? __ldcs(rp + k) : __ldca(rp + k);
     B.m = kLastUse ? __ldcs(mp) : __ldca(mp);
   } else {
-    float x[kTokLane];
-    uint32_t m[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-    for (int i = 0; i < kTokLane; ++i) {
-      x[i] = 0.f;
-      if (t + i < w1) {
-        x[i] = rw[t + i];
-        m[i >> 2] |= (uint32_t)mk[t + i] << (8 * (i & 3));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) B.r[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
-    B.m = make_uint4(m[0], m[1], m[2], m[3]);
+    load_batch_scalar(B, rw, mk, t, w1);
   }
+}
+
+// token i of the lane's 16 is masked in: its mask byte is nonzero (boolean mask, reading n5);
+// one LOP3 with a byte-wide immediate per token
+__device__ __forceinline__ bool tok_on(const Batch& B, int i) {
+  const int k = i >> 2;
+  const uint32_t w = k == 0 ? B.m.x : k == 1 ? B.m.y : k == 2 ? B.m.z : B.m.w;
+  return (w & (0xffu << (8 * (i & 3)))) != 0u;
 }
 
 __device__ __forceinline__ float tok_r(const Batch& B, int i) {
@@ -195,19 +215,11 @@ __device__ __forceinline__ float tok_r(const Batch& B, int i) {
   return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
-__device__ __forceinline__ bool tok_m(const Batch& B, int i) {
-  const int k = i >> 2;
-  const uint32_t w = k == 0 ? B.m.x : k == 1 ? B.m.y : k == 2 ? B.m.z : B.m.w;
-  return (w >> (8 * (i & 3))) & 0xffu;
-}
-
-// v_t = m_t r_t with the boolean mask (reading n5)
-__device__ __forceinline__ float tok_v(const Batch& B, int i) { return tok_m(B, i) ? tok_r(B, i) : 0.f; }
-
 __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
   __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
   __shared__ float2 bmap[kWarps][kMaxNB];   // per batch: its map (pass 1), then its carry
+  __shared__ float2 lmap[kWarps][kMaxNB][32];  // per batch and lane: exclusive suffix map (pass 1)
   __shared__ double red[3][kWarps];
   __shared__ uint32_t s_tag;
   __shared__ int s_ok;
@@ -226,21 +238,21 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   const int NB = rt.nb;
   const int64_t win = (int64_t)kBatch * NB;
   const float gamma = a.gamma;
-  float g16 = 1.f;  // gamma^16: the slope of a lane's 16 tokens without a sequence end
-#pragma unroll
-  for (int i = 0; i < kTokLane; ++i) g16 *= gamma;
+  const float g16 = a.gamma16;  // the slope of a lane's 16 tokens without a sequence end
   uint32_t* bm = ends_bm[wid];
   float2* bmp = bmap[wid];
+  float2 (*lmp)[32] = lmap[wid];
   double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
 
-  // windows are claimed in increasing order and every window only waits on smaller ones, so
-  // holding the next claim while processing the current one cannot deadlock
-  uint32_t next = 0;
-  if (lane == 0) next = atomicAdd(&a.ws->work_ctr, 1u);
+  // windows are claimed in increasing order and every window only waits on smaller ones (no
+  // deadlock); a warp claims its next window only when it starts it, so a window's right
+  // neighbour is always already in progress (claiming ahead would make the left neighbour wait
+  // a whole window for it)
   while (true) {
-    const int64_t u = __shfl_sync(kFull, next, 0);
+    uint32_t claim = 0;
+    if (lane == 0) claim = atomicAdd(&a.ws->work_ctr, 1u);
+    const int64_t u = __shfl_sync(kFull, claim, 0);
     if (u >= total) break;
-    if (lane == 0) next = atomicAdd(&a.ws->work_ctr, 1u);
     int ri = 0;
     while (u >= rt.wbeg[ri + 1]) ++ri;
     const int r = rt.rank[ri];
@@ -255,10 +267,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     const bool vec = aligned(rw, 16) && aligned(G, 16) && aligned(mk, 16);
     const int64_t lt = w0 + (int64_t)kTokLane * lane;  // this lane's tokens in batch b: lt + 512 b
 
-    Batch cur, nxt;
+    Batch cur, nxt;  // batch b, and b-1 in flight
     load_batch<false>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
-    if (nb >= 2) load_batch<false>(nxt, rw, mk, lt + (int64_t)(nb - 2) * kBatch, w1, vec);
-    if (nb >= 3) prefetch_batch(rw, mk, w0 + (int64_t)(nb - 3) * kBatch, w1, lane);
+    for (int d = 3; d < 3 + EARL_AGG_PF; ++d)
+      if (nb >= d) prefetch_batch(rw, mk, w0 + (int64_t)(nb - d) * kBatch, w1, lane);
 
     // sequence ends inside the window: token s-1 for every sequence start s in (w0, w1]
     // (starts are cum[0][p] - cum[0][gs], p in [gs, gs+cnt]; the last one ends the buffer)
@@ -279,26 +291,27 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     // bit i: token i of this lane's 16 in batch b ends its sequence
     auto ends16 = [&](int b) { return (bm[16 * b + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu; };
 
-    // pass 1: batch maps (kept in shared memory) and the window's map; batch b-1 is in flight
-    // in registers and batch b-2 in L2 while batch b is composed
+    // pass 1: lane maps and batch maps (shared memory) and the window's map
     float wS = 0.f, wP = 1.f;
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
-      if (b >= 3) prefetch_batch(rw, mk, w0 + (int64_t)(b - 3) * kBatch, w1, lane);
+      if (b > 0) load_batch<false>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
+      if (EARL_AGG_PF > 0 && b >= 1 + EARL_AGG_PF)
+        prefetch_batch(rw, mk, w0 + (int64_t)(b - 1 - EARL_AGG_PF) * kBatch, w1, lane);
       const uint32_t e = ends16(b);
       float S = 0.f;
 #pragma unroll
       for (int i = kTokLane - 1; i >= 0; --i) {
-        const float v = tok_v(cur, i);
-        S = ((e >> i) & 1u) ? v : fmaf(gamma, S, v);
+        const float v = tok_on(cur, i) ? tok_r(cur, i) : 0.f;
+        S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, v);
       }
       float rS, rP, bS, bP;
       warp_compose(S, e ? 0.f : g16, lane, rS, rP, bS, bP);
+      lmp[b][lane] = make_float2(rS, rP);
       if (lane == 0) bmp[b] = make_float2(bS, bP);
       wS = bS + bP * wS;
       wP = bP * wP;
       cur = nxt;
-      if (b >= 2) load_batch<false>(nxt, rw, mk, lt + (int64_t)(b - 2) * kBatch, w1, vec);
     }
 
     // publish the window's map, then look back (32 windows per round trip) for the carry:
@@ -356,47 +369,38 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     }
     __syncwarp();
 
-    // pass 2: returns (the window's second read hits L2), float4 stores, statistics; the head
-    // of the next claimed window is prefetched meanwhile
+    // pass 2: returns from the lane maps and batch carries (the window's second read hits L2),
+    // float4 stores, statistics
     const bool count_stats = rt.t[ri] == 0;
     load_batch<true>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
-    {
-      const int64_t un = __shfl_sync(kFull, next, 0);
-      if (un < total) {
-        int rn = 0;
-        while (un >= rt.wbeg[rn + 1]) ++rn;
-        const int64_t wn = rt.wbeg[rn + 1] - 1 - un;
-        const int64_t n0 = wn * win, n1 = min(rt.ntok[rn], n0 + win);
-        const int64_t top = n0 + ((n1 - n0 - 1) / kBatch) * kBatch;  // its first (rightmost) batch
-        prefetch_batch(a.rewards[rt.rank[rn]], a.mask[rt.rank[rn]], top, n1, lane);
-        if (top - kBatch >= n0) prefetch_batch(a.rewards[rt.rank[rn]], a.mask[rt.rank[rn]], top - kBatch, n1, lane);
-      }
-    }
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
       if (b > 0) load_batch<true>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
       const uint32_t e = ends16(b);
-      float S = 0.f;
-#pragma unroll
-      for (int i = kTokLane - 1; i >= 0; --i) {
-        const float v = tok_v(cur, i);
-        S = ((e >> i) & 1u) ? v : fmaf(gamma, S, v);
-      }
-      float rS, rP, tS, tP;
-      warp_compose(S, e ? 0.f : g16, lane, rS, rP, tS, tP);
-      float g_next = rS + rP * bmp[b].x;
+      const float2 rm = lmp[b][lane];
+      float g_next = rm.x + rm.y * bmp[b].x;
       float out[kTokLane];
-      float sg = 0.f, sg2 = 0.f;
-      int cnt = 0;
 #pragma unroll
       for (int i = kTokLane - 1; i >= 0; --i) {
-        const bool m = tok_m(cur, i);
-        const float v = m ? tok_r(cur, i) : 0.f;
-        out[i] = ((e >> i) & 1u) ? v : fmaf(gamma, g_next, v);
+        const float v = tok_on(cur, i) ? tok_r(cur, i) : 0.f;
+        out[i] = fmaf(((e >> i) & 1u) ? 0.f : gamma, g_next, v);
         g_next = out[i];
-        if (m) { sg += out[i]; sg2 = fmaf(out[i], out[i], sg2); ++cnt; }
       }
-      if (count_stats) { s_m += (double)cnt; s_g += (double)sg; s_g2 += (double)sg2; }
+      if (count_stats) {
+        float sg = 0.f, sg2 = 0.f;
+        int cnt = 0;
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i) {
+          if (tok_on(cur, i)) {
+            sg += out[i];
+            sg2 = fmaf(out[i], out[i], sg2);
+            ++cnt;
+          }
+        }
+        s_m += (double)cnt;
+        s_g += (double)sg;
+        s_g2 += (double)sg2;
+      }
       const int64_t t = lt + (int64_t)b * kBatch;
       if (vec && t + kTokLane <= w1) {
         float4* gp = reinterpret_cast<float4*>(G + t);
@@ -404,7 +408,6 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
         for (int k = 0; k < 4; ++k)
           __stcs(gp + k, make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]));
       } else {
-#pragma unroll
         for (int i = 0; i < kTokLane; ++i)
           if (t + i < w1) G[t + i] = out[i];
       }

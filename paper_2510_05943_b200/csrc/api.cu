@@ -1053,6 +1053,8 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   earl_status_t st = agg_args(p, a);
   if (st != EARL_OK) return st;
   a.gamma = gamma;
+  a.gamma16 = 1.f;
+  for (int i = 0; i < 16; ++i) a.gamma16 *= gamma;
   a.partial = partial;
   if ((st = set_per_rank<const float>(p, a.rewards, rewards, "rewards", true)) != EARL_OK) return st;
   if ((st = set_per_rank<const uint8_t>(p, a.mask, mask, "mask", true)) != EARL_OK) return st;

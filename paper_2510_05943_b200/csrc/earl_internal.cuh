@@ -164,6 +164,7 @@ struct AggArgs {
   int32_t world;
   int32_t view_rank;       // -1: every source rank (emulated comm); else this rank
   float gamma, eps;
+  float gamma16;            // gamma^16 (product of 16 fp32 factors, as a lane of 16 tokens)
   const float* rewards[kMaxWorld];   // per source comm rank: token rewards (fp32)
   const uint8_t* mask[kMaxWorld];    // token mask (u8, 1 = counted)
   float* returns[kMaxWorld];         // token returns G (fp32)
