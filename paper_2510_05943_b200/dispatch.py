@@ -277,3 +277,110 @@ def distributed_advantages(dispatcher, plan, gamma, rewards, mask, returns, adv,
         partial.copy_(host)
     plan.advantages(partial, eps, [returns], [mask], [adv], stream=stream)
     return partial
+
+
+# ---------------------------------------------------------------------------------------
+# per-role routing (NEXT-2; "route_noncritical_tensors", §3.3 + §5)
+# ---------------------------------------------------------------------------------------
+
+# role -> route.  Tensors the trainer consumes token by token go all-to-all (§3.3: log
+# probabilities are "not required for aggregation in advantage estimation"); rewards and returns
+# are gathered to the controller by default (§5 "rewards and returns are aggregated"), or
+# dispatched like the rest when the aggregation itself is distributed (§5's extension, built as
+# earl_returns / earl_advantages: DESIGN.md reading n5).
+ROLE_ROUTES = {
+    "tokens": "all_to_all", "log_probs": "all_to_all", "ref_log_probs": "all_to_all",
+    "values": "all_to_all", "advantages": "all_to_all", "response_mask": "all_to_all",
+    "hidden": "all_to_all", "rewards": "gather", "returns": "gather",
+}
+
+
+def route_roles(roles: dict, distributed_aggregation: bool = False) -> dict:
+    """{tensor name: role} -> {tensor name: "all_to_all" | "gather"}; an unknown role is a
+    configuration error (ValueError)."""
+    out = {}
+    for name, role in roles.items():
+        if role not in ROLE_ROUTES:
+            raise ValueError(f"unknown role {role!r} for tensor {name!r} "
+                             f"(known: {', '.join(sorted(ROLE_ROUTES))})")
+        route = ROLE_ROUTES[role]
+        out[name] = "all_to_all" if (route == "gather" and distributed_aggregation) else route
+    return out
+
+
+def controller_layout(controller: int = 0) -> dict:
+    """The gather destination: one DP group held by the controller rank alone."""
+    return {"rank0": int(controller), "dp": 1, "sp": 1, "tp": 1, "assign": "contig",
+            "sp_split": "block", "sp_min_len": 0, "counts": None, "group_of_seq": None}
+
+
+class RolePlans:
+    """The plan set of one batch: one dispatch plan per (route, granularity) with the fields of
+    the tensors routed that way.  groups[(route, per)] = (plan, names, fields), per = "token" or
+    "sequence"; a route with only per-sequence tensors still plans its token routing once (the
+    sequence records follow the token plan's groups)."""
+
+    def __init__(self, local_ranks: int):
+        self.local_ranks = int(local_ranks)
+        self.groups = {}
+        self._token_plans = []
+
+    def dst_layout(self, route, dst, controller):
+        return dst if route == "all_to_all" else controller_layout(controller)
+
+    def exec(self, send: dict, recv: dict, stream=None):
+        """send / recv: tensor name -> list over this process's ranks (emulated: every rank;
+        one process per GPU: one entry) of device buffers (None where a rank holds nothing)."""
+        for (route, per), (plan, names, _) in self.groups.items():
+            s = [send[nm][r] for r in range(self.local_ranks) for nm in names]
+            d = [recv[nm][r] for r in range(self.local_ranks) for nm in names]
+            plan.exec(s, d, stream)
+
+    def destroy(self):
+        for plan, _, _ in self.groups.values():
+            plan.destroy()
+        for p in self._token_plans:
+            p.destroy()
+        self.groups = {}
+        self._token_plans = []
+
+
+def plan_roles(disp, src, dst, seq_lens, tensors, distributed_aggregation=False, controller=0,
+               stream=None):
+    """SPEC route_noncritical_tensors: plan every tensor of the batch by its role.
+
+    disp: EmulatedDispatch or Dispatcher; tensors: [(name, role, field, per)], field = (name,
+    bytes per element, elements per token or sequence, kind), per = "token" | "sequence".
+    Returns RolePlans (empty for an empty tensor list)."""
+    routes = route_roles({t[0]: t[1] for t in tensors}, distributed_aggregation)
+    local = disp.world if isinstance(disp, EmulatedDispatch) else 1
+    rp = RolePlans(local)
+    if not tensors:
+        return rp
+    lens = seq_lens
+    if not isinstance(lens, torch.Tensor):
+        lens = torch.as_tensor(np.asarray(seq_lens, dtype=np.int32))
+    lens = lens.to(disp.device)
+    src_dev = layout_for_device(src, disp.device)
+    for route in ("all_to_all", "gather"):
+        dst_r = rp.dst_layout(route, dst, controller)
+        tok = [t for t in tensors if routes[t[0]] == route and t[3] == "token"]
+        seq = [t for t in tensors if routes[t[0]] == route and t[3] == "sequence"]
+        for t in tok + seq:
+            if t[3] not in ("token", "sequence"):
+                raise ValueError(f"tensor {t[0]!r}: per must be 'token' or 'sequence'")
+        token_plan = None
+        if tok:
+            token_plan = disp.comm.plan(src_dev, layout_for_device(dst_r, disp.device), lens,
+                                        [t[2] for t in tok], stream)
+            rp.groups[(route, "token")] = (token_plan, [t[0] for t in tok], [t[2] for t in tok])
+        if seq:
+            if token_plan is None:  # routing only: the sequences' groups
+                token_plan = disp.comm.plan(src_dev, layout_for_device(dst_r, disp.device), lens,
+                                            [("unit", 1, 1, "x")], stream)
+                rp._token_plans.append(token_plan)
+            sp = plan_seq_fields(disp.comm, token_plan, src_dev,
+                                 layout_for_device(dst_r, disp.device), [t[2] for t in seq],
+                                 disp.device, stream)
+            rp.groups[(route, "sequence")] = (sp, [t[0] for t in seq], [t[2] for t in seq])
+    return rp
