@@ -11,3 +11,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
    python bench.py --steps 5 --warmup 2 --profile > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:copy_kernel -s 1 -c 1 \
    -o $OUT/copy_full -f python bench.py --steps 2 --warmup 1 --profile --no-staged > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
+# NEXT-2: distributed returns / advantages (C2, C4, C5-lt batches) and one full capture each
+timeout 600 python scripts/aggregate_bench.py > $OUT/aggregate.jsonl 2> $OUT/aggregate.err; echo "aggregate rc=$?"; cat $OUT/aggregate.jsonl
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"returns_kernel|advantage_kernel" -s 6 -c 2 \
+   -o $OUT/aggregate_full -f python scripts/aggregate_bench.py --only C5-lt --iters 4 > $OUT/ncu_agg.log 2>&1; echo "ncu agg rc=$?"
