@@ -77,7 +77,9 @@ typedef enum {
   EARL_ERR_NCCL = 5,             /* reserved                                              */
   EARL_ERR_TIMEOUT = 6,          /* peer signals missing; mask in earl_last_error */
   EARL_ERR_MISMATCH = 7,         /* plan hash differs across ranks (debug)                */
-  EARL_ERR_UNSUPPORTED = 8       /* world > 8, wrong comm kind for the call               */
+  EARL_ERR_UNSUPPORTED = 8,      /* world > 8, wrong comm kind for the call               */
+  EARL_ERR_POLICY = 9            /* selector: a context range with no OOM-free configuration,
+                                    or an average length outside every range                */
 } earl_status_t;
 
 typedef enum {
@@ -274,6 +276,47 @@ EARL_API earl_status_t earl_returns(earl_plan_t plan, float gamma, const void* c
 EARL_API earl_status_t earl_advantages(earl_plan_t plan, const double* stats, float eps,
                                        const void* const* returns, const void* const* mask,
                                        void* const* adv, void* stream);
+
+/* ---- parallelism selector (host side of NEXT-4; Eq. (1))
+ * "at the start of the training process, EARL measures the throughput under various
+ * parallelism configurations and context lengths, then maintains the optimal configuration for
+ * each context length range ... monitors the averaged context length ... When the averaged
+ * context length falls into a new context range, EARL switches to the corresponding
+ * parallelism configuration before the next Rollout stage."  Host-only: no CUDA calls, no
+ * device memory.  The chosen configuration's layout is what the caller passes as `dst` (or
+ * `src`) to earl_dispatch_plan.  Readings s1-s4 in DESIGN.md. */
+typedef struct earl_policy* earl_policy_t;
+
+/* Eq. (1): *out = (tgs_b - tgs_a) / tgs_a * 100 (positive: b is faster).
+ * Errors: INVALID_ARGUMENT if tgs_a <= 0 or out is NULL. */
+EARL_API earl_status_t earl_speedup_pct(double tgs_a, double tgs_b, double* out);
+
+/* Build the selection table from a throughput profile.  n_configs configurations (config_tp[c] =
+ * its TP degree, used only to break ties), n_buckets context ranges [bounds[b], bounds[b+1])
+ * (bounds: n_buckets + 1 ascending token counts), tgs[c * n_buckets + b] = measured
+ * tokens/GPU/s of configuration c in range b, oom[c * n_buckets + b] != 0 marks an OOM probe
+ * (oom may be NULL).  Per range: the OOM-free configuration of highest TGS; ties go to the
+ * smaller TP, then the lower index (s2).  hysteresis_tokens >= 0 (s3).  Host pointers, read
+ * during the call only; *out is owned by the caller (earl_policy_destroy).
+ * Errors: INVALID_ARGUMENT (counts <= 0, bounds not ascending, TGS <= 0 on an OOM-free entry,
+ * NULL pointers), POLICY (a range where every configuration OOMs; earl_last_error names it). */
+EARL_API earl_status_t earl_policy_build(int32_t n_configs, const int32_t* config_tp,
+                                         int32_t n_buckets, const int64_t* bounds,
+                                         const double* tgs, const uint8_t* oom,
+                                         int64_t hysteresis_tokens, earl_policy_t* out);
+/* config_of_bucket[n_buckets] <- the table. */
+EARL_API earl_status_t earl_policy_table(earl_policy_t policy, int32_t* config_of_bucket);
+/* The configuration for the next rollout given the observed average length (s3 hysteresis: keep
+ * `current` while avg_len stays within hysteresis_tokens of a boundary shared with a range of
+ * `current`).  *next = the configuration, *switched = (next != current).
+ * Errors: INVALID_ARGUMENT (current outside [0, n_configs), NULL), POLICY (avg_len outside
+ * [bounds[0], bounds[n_buckets])). */
+EARL_API earl_status_t earl_policy_select(earl_policy_t policy, double avg_len, int32_t current,
+                                          int32_t* next, int32_t* switched);
+EARL_API earl_status_t earl_policy_destroy(earl_policy_t policy);
+/* The averaged context length of a planned batch, T / N (s4), from the plan's header
+ * (synchronises with the planner like earl_plan_stats).  Errors: INVALID_ARGUMENT if N = 0. */
+EARL_API earl_status_t earl_plan_mean_length(earl_plan_t plan, double* avg);
 
 /* ---- misc -------------------------------------------------------------------------- */
 EARL_API const char* earl_status_string(earl_status_t status);

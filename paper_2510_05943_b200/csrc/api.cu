@@ -30,6 +30,15 @@ earl_status_t fail(earl_status_t st, const char* fmt, ...) {
   return st;
 }
 
+}  // namespace
+
+namespace earl {
+// the last-error slot shared with selector.cpp (host-only code in another translation unit)
+earl_status_t set_error(earl_status_t st, const char* msg) { return fail(st, "%s", msg); }
+}  // namespace earl
+
+namespace {
+
 #define CUDA_TRY(expr)                                                                     \
   do {                                                                                     \
     cudaError_t e_ = (expr);                                                               \
@@ -126,6 +135,7 @@ extern "C" const char* earl_status_string(earl_status_t st) {
     case EARL_ERR_TIMEOUT: return "EARL_ERR_TIMEOUT";
     case EARL_ERR_MISMATCH: return "EARL_ERR_MISMATCH";
     case EARL_ERR_UNSUPPORTED: return "EARL_ERR_UNSUPPORTED";
+    case EARL_ERR_POLICY: return "EARL_ERR_POLICY";
   }
   return "EARL_ERR_UNKNOWN";
 }
@@ -586,6 +596,15 @@ extern "C" earl_status_t earl_plan_groups(earl_plan_t p, int32_t* src_groups, in
     CUDA_TRY(cudaMemcpyAsync(src_groups, p->args.grp[0], bytes, cudaMemcpyDeviceToDevice, s));
   if (bytes && dst_groups)
     CUDA_TRY(cudaMemcpyAsync(dst_groups, p->args.grp[1], bytes, cudaMemcpyDeviceToDevice, s));
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_mean_length(earl_plan_t p, double* avg) {
+  if (!p || !avg) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  if (p->N == 0) return fail(EARL_ERR_INVALID_ARGUMENT, "empty batch: no average length");
+  *avg = (double)p->host_hdr.T / (double)p->N;
   return EARL_OK;
 }
 

@@ -384,3 +384,11 @@ def plan_roles(disp, src, dst, seq_lens, tensors, distributed_aggregation=False,
                                  disp.device, stream)
             rp.groups[(route, "sequence")] = (sp, [t[0] for t in seq], [t[2] for t in seq])
     return rp
+
+
+def next_layout(policy, plan, current: int, layouts):
+    """The selector's step before the next rollout: observe the averaged
+    context length of the batch just planned (T / N, reading s4), look it up in the policy
+    (earl_policy_select, hysteresis s3) -> (configuration index, its layout, switched)."""
+    nxt, switched = policy.select(plan.mean_length(), current)
+    return nxt, layouts[nxt], switched

@@ -26,7 +26,7 @@ EARL_HANDLE_BYTES = 128
 STATUS = {
     0: "EARL_OK", 1: "EARL_ERR_INVALID_ARGUMENT", 2: "EARL_ERR_LAYOUT", 3: "EARL_ERR_CAPACITY",
     4: "EARL_ERR_CUDA", 5: "EARL_ERR_NCCL", 6: "EARL_ERR_TIMEOUT", 7: "EARL_ERR_MISMATCH",
-    8: "EARL_ERR_UNSUPPORTED",
+    8: "EARL_ERR_UNSUPPORTED", 9: "EARL_ERR_POLICY",
 }
 ASSIGN = {"given_counts": 0, "contig": 1, "lpt": 2, "explicit": 3}
 
@@ -37,7 +37,8 @@ EXPORTED = [
     "earl_plan_replan", "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
     "earl_plan_export", "earl_plan_groups", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
     "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
-    "earl_abi_version", "earl_kernel_launch_count",
+    "earl_abi_version", "earl_kernel_launch_count", "earl_speedup_pct", "earl_policy_build",
+    "earl_policy_table", "earl_policy_select", "earl_policy_destroy", "earl_plan_mean_length",
 ]
 
 
@@ -131,6 +132,12 @@ def lib():
         "earl_plan_messages": [vp, i32, vp, vp, vp, vp],
         "earl_returns": [vp, C.c_float, pvp, pvp, pvp, pvp, vp, vp],
         "earl_advantages": [vp, vp, C.c_float, pvp, pvp, pvp, vp],
+        "earl_speedup_pct": [C.c_double, C.c_double, C.POINTER(C.c_double)],
+        "earl_policy_build": [i32, vp, i32, vp, vp, vp, i64, pvp],
+        "earl_policy_table": [vp, vp],
+        "earl_policy_select": [vp, C.c_double, i32, C.POINTER(i32), C.POINTER(i32)],
+        "earl_policy_destroy": [vp],
+        "earl_plan_mean_length": [vp, C.POINTER(C.c_double)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -295,6 +302,12 @@ class Plan:
                                          _ptr(seq_ids) or None, _ptr(tok_start) or None,
                                          _stream(stream)))
 
+    def mean_length(self) -> float:
+        """Averaged context length of the planned batch, T / N (selector reading s4)."""
+        v = C.c_double()
+        check(lib().earl_plan_mean_length(self.h, C.byref(v)))
+        return v.value
+
     def stats(self) -> dict:
         st = PlanStats()
         check(lib().earl_plan_stats(self.h, C.byref(st)))
@@ -350,6 +363,53 @@ class Plan:
     def destroy(self):
         if getattr(self, "h", None):
             check(lib().earl_plan_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def speedup_pct(tgs_a: float, tgs_b: float) -> float:
+    """Eq. (1) (PAPER.md:233-237)."""
+    v = C.c_double()
+    check(lib().earl_speedup_pct(float(tgs_a), float(tgs_b), C.byref(v)))
+    return v.value
+
+
+class Policy:
+    """The Parallelism Selector's table (host-only).  config_tp[c] is
+    configuration c's TP degree; bounds the n_buckets+1 context-range edges; tgs / oom are
+    [n_configs][n_buckets] profiles."""
+
+    def __init__(self, config_tp, bounds, tgs, oom=None, hysteresis_tokens=0):
+        tp = np.ascontiguousarray(config_tp, dtype=np.int32)
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        t = np.ascontiguousarray(tgs, dtype=np.float64).reshape(-1)
+        o = None if oom is None else np.ascontiguousarray(oom, dtype=np.uint8).reshape(-1)
+        self.n_configs, self.n_buckets = int(tp.size), int(b.size) - 1
+        h = C.c_void_p()
+        check(lib().earl_policy_build(self.n_configs, tp.ctypes.data, self.n_buckets, b.ctypes.data,
+                                      t.ctypes.data, None if o is None else o.ctypes.data,
+                                      int(hysteresis_tokens), C.byref(h)))
+        self.h = h
+
+    def table(self):
+        out = np.zeros(max(self.n_buckets, 1), dtype=np.int32)
+        check(lib().earl_policy_table(self.h, out.ctypes.data))
+        return out[: self.n_buckets].tolist()
+
+    def select(self, avg_len: float, current: int):
+        """-> (next configuration, switched)."""
+        nxt, sw = C.c_int32(), C.c_int32()
+        check(lib().earl_policy_select(self.h, float(avg_len), int(current), C.byref(nxt), C.byref(sw)))
+        return nxt.value, bool(sw.value)
+
+    def destroy(self):
+        if getattr(self, "h", None):
+            check(lib().earl_policy_destroy(self.h))
             self.h = None
 
     def __del__(self):
