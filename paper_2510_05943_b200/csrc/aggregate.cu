@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t Q = qbeg[rt.n];
   constexpr int kU = 4;
+  int ri = 0;  // rank cursor: q only grows
   for (int64_t q0 = tid; q0 < Q; q0 += kU * stride) {
     float4 g[kU];
     uint32_t m[kU];
@@ -511,7 +512,6 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
       const int64_t q = q0 + u * stride;
       rr[u] = -1;
       if (q < Q) {
-        int ri = 0;
         while (q >= qbeg[ri + 1]) ++ri;
         rr[u] = rt.rank[ri];
         qq[u] = q - qbeg[ri];
