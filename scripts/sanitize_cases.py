@@ -1,4 +1,5 @@
-"""A handful of GPU dispatch cases for compute-sanitizer runs (each bit-exact vs the oracle)."""
+"""A handful of GPU cases for compute-sanitizer runs: dispatch (each bit-exact vs the oracle) and
+the NEXT-2 returns / advantages kernels (within the n5 bound)."""
 import random
 import sys
 import os
@@ -21,4 +22,11 @@ for seed in range(4):
     src = with_split(rng, random_layout(rng, world, n))
     dst = with_split(rng, random_layout(rng, world, n))
     run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
+# NEXT-2: per-sequence fields, returns (look-back across windows, zero-length sequences,
+# unaligned scalar path) and advantages, each against the oracle
+from tests.test_gpu_parity import _adv_case  # noqa: E402
+_adv_case([20_000, 3, 0, 1500, 7, 0], W.layout(dp=2, assign="given_counts", counts=[3, 3]), 1.0, 4)
+_adv_case([1 + (i % 5) for i in range(700)], W.layout(dp=3, tp=2, assign="lpt"), 0.9, 8, shift=1)
+_adv_case(W.lognormal_lengths(60, 900, 0.8, 1, 5000, seed=3).tolist(), W.layout(dp=4, assign="contig"),
+          0.99, 4, repeats=2)
 print("sanitize cases ok")
