@@ -150,11 +150,13 @@ class Dispatcher:
         self._dst = layout_for_device(dst, self.device)
         return self.comm.plan(self._src, self._dst, seq_lens, fields, stream)
 
-    def alloc_recv(self, plan, fields):
+    def alloc_recv(self, plan, fields, reset=True):
         """Receive tensors inside the symmetric window: same offsets on every rank, sized for
-        the largest destination rank (every rank knows every size: the plan is replicated)."""
+        the largest destination rank (every rank knows every size: the plan is replicated).
+        reset=False keeps earlier allocations (several plans' buffers side by side)."""
         st = plan.stats()
-        self.comm.reset_alloc()
+        if reset:
+            self.comm.reset_alloc()
         full, views = [], []
         n_max = max(st["n_local_tokens"]) if st["n_local_tokens"] else 0
         mine = int(st["n_local_tokens"][self.rank])
@@ -327,6 +329,25 @@ class RolePlans:
 
     def dst_layout(self, route, dst, controller):
         return dst if route == "all_to_all" else controller_layout(controller)
+
+    def alloc_recv(self, disp):
+        """Receive buffers of every group: (recv, views), both tensor name -> list over this
+        process's ranks.  recv feeds exec (window pointers for a Dispatcher: all groups share the
+        window, allocated side by side); views are this rank's received bytes."""
+        recv, views = {}, {}
+        first = True
+        for plan, names, fields in self.groups.values():
+            if isinstance(disp, EmulatedDispatch):
+                per_rank = disp.alloc_recv(plan, fields)
+                for f, nm in enumerate(names):
+                    recv[nm] = [per_rank[r][f] for r in range(self.local_ranks)]
+                    views[nm] = recv[nm]
+            else:
+                ptrs, vs = disp.alloc_recv(plan, fields, reset=first)
+                for f, nm in enumerate(names):
+                    recv[nm], views[nm] = [ptrs[f]], [vs[f]]
+            first = False
+        return recv, views
 
     def exec(self, send: dict, recv: dict, stream=None):
         """send / recv: tensor name -> list over this process's ranks (emulated: every rank;

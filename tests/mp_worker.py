@@ -141,3 +141,62 @@ def gpu_adv_main(rank, world, port, q, case):
         q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_roles_main(rank, world, port, q, case):
+    """Per-role routing (SPEC route_noncritical_tensors) with one process per rank: token and
+    per-sequence tensors, all-to-all or gathered to the controller, buffers side by side in one
+    IPC window -- byte-exact against the oracle."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200.dispatch import Dispatcher, controller_layout, plan_roles, route_roles
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, src, dst, flag, ctrl = case
+        tensors = [("ids", "tokens", ("ids", 4, 1, "x"), "token"),
+                   ("lp", "log_probs", ("lp", 4, 1, "x"), "token"),
+                   ("G", "returns", ("G", 4, 1, "x"), "token"),
+                   ("R", "rewards", ("R", 4, 1, "x"), "sequence")]
+        routes = route_roles({t[0]: t[1] for t in tensors}, flag)
+        T, N = sum(lens), len(lens)
+        gs = O.assign_groups(src, lens)
+        hs = O.seq_holdings(src, lens, gs)
+        send, want = {}, {}
+        for k, t in enumerate(tensors):
+            nm = t[0]
+            lay_d = dst if routes[nm] == "all_to_all" else controller_layout(ctrl)
+            if t[3] == "token":
+                glob = np.random.default_rng(50 + k).integers(0, 256, T * 4, dtype=np.uint8)
+                arrs = O.rank_arrays_from_global(src, lens, gs, [glob], [("f", 4, 1, "x")])
+                w, _, _ = O.dispatch(src, lay_d, lens, arrs, [("f", 4, 1, "x")], world)
+            else:
+                glob = np.random.default_rng(50 + k).integers(0, 256, N * 4, dtype=np.uint8)
+                arrs = {r: [np.concatenate([glob[4 * i:4 * i + 4] for i in m]) if m
+                            else np.zeros(0, np.uint8)] for r, m in hs.items()}
+                w = O.dispatch_seq_fields(src, lay_d, lens, arrs, [t[2]], world)
+            a = arrs.get(rank, [np.zeros(0, np.uint8)])[0]
+            send[nm] = [torch.from_numpy(a).cuda() if a.size else None]
+            want[nm] = w
+        D = Dispatcher(window_bytes=8 * (T + N) * 4 + (1 << 20), device=0)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        rp = plan_roles(D, src, dst, glens, tensors, distributed_aggregation=flag, controller=ctrl)
+        recv, views = rp.alloc_recv(D)
+        for nm in views:
+            views[nm][0].fill_(0xA5)
+        rp.exec(send, recv)
+        torch.cuda.synchronize()
+        for nm, w in want.items():
+            got = views[nm][0].cpu().numpy()
+            if rank in w:
+                assert np.array_equal(got[: w[rank][0].size], w[rank][0]), (nm, rank)
+            else:
+                assert got.size == 0, (nm, rank, "received bytes it should not")
+        rp.destroy()
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

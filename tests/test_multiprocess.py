@@ -94,3 +94,18 @@ def test_distributed_advantages_processes(world, tp):
     lens = W.c2_lengths(0)[:48].tolist()
     src = W.layout(dp=world // tp, tp=tp, assign="contig")
     run_procs(mp_worker.gpu_adv_main, world, extra=((lens, src, 0.99),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,flag", [(2, False), (4, True), (4, False)])
+def test_role_plans_processes(world, flag):
+    """Per-role routing across processes: several plans' receive buffers side by side in one
+    IPC window, fused P2P exec of each group."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    lens = W.c2_lengths(1)[:40].tolist()
+    src = W.rollout_layout(len(lens), world)
+    dst = W.layout(dp=max(1, world // 2), tp=2 if world >= 2 else 1, assign="lpt")
+    run_procs(mp_worker.gpu_roles_main, world, extra=((lens, src, dst, flag, world - 1),), timeout=600)
