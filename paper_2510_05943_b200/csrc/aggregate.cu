@@ -145,6 +145,26 @@ __device__ int64_t first_at_least(const int64_t* cum, int64_t base, int64_t lo, 
   return lo + (__ffs(b) - 1);
 }
 
+// Sequence ends inside the window [w0, w1): bit (s-1-w0) of bm for every sequence start s in
+// (w0, w1] (starts are cum[p] - base, p in [gs, pend]; the last one ends the buffer).  Clears
+// the window's nwords words first; returns the first sequence p with cum[p] - base >= w0.
+__device__ __forceinline__ int64_t mark_ends(uint32_t* bm, int nwords, const int64_t* cum,
+                                             int64_t base, int64_t gs, int64_t pend, int64_t w0,
+                                             int64_t w1, int lane) {
+  for (int j = lane; j < nwords; j += 32) bm[j] = 0u;
+  __syncwarp();
+  const int64_t lo = first_at_least(cum, base, gs, pend, w0, lane);
+  for (int64_t p0 = lo;; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const int64_t s = p <= pend ? cum[p] - base : INT64_MAX;
+    const bool in = s <= w1;
+    if (in && s > w0) atomicOr(&bm[(s - 1 - w0) >> 5], 1u << ((s - 1 - w0) & 31));
+    if (__ballot_sync(kFull, in) != kFull) break;
+  }
+  __syncwarp();
+  return lo;
+}
+
 // In-order composition of the 32 lane maps (lane l's map applies after lane l+1's):
 // (rS, rP) = exclusive suffix (lanes right of this one), (tS, tP) = all 32 lanes.
 __device__ __forceinline__ void warp_compose(float S, float P, int lane, float& rS, float& rP,
@@ -215,12 +235,120 @@ __device__ __forceinline__ float tok_r(const Batch& B, int i) {
   return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
+// Decoupled look-back for window w of a rank (windows w+1 .. nwin-1 lie to its right), 32
+// windows per round trip: compose their maps up to the first inclusive value or zero slope (a
+// sequence end); returns G just right of the window (0 past the buffer end).
+__device__ __forceinline__ float look_back(AggWindow* W, int64_t w, int64_t nwin, uint32_t tag,
+                                           int lane) {
+  float cS = 0.f, cP = 1.f;
+  for (int64_t j0 = w + 1; j0 < nwin;) {
+    const int64_t j = j0 + lane;
+    bool ready = false, stop = false;
+    float S = 0.f, P = 1.f;
+    if (j < nwin) {
+      const uint64_t wi = ld_word(&W[j].inc);
+      if (word_is(wi, tag | 2u)) {
+        ready = stop = true;
+        S = word_val(wi);
+        P = 0.f;
+      } else {
+        const uint64_t ws = ld_word(&W[j].S), wp = ld_word(&W[j].P);
+        if (word_is(ws, tag | 1u) && word_is(wp, tag | 1u)) {
+          ready = true;
+          S = word_val(ws);
+          P = word_val(wp);
+          stop = P == 0.f;
+        }
+      }
+    }
+    // usable prefix: ready lanes up to (and including) the first stopper
+    const unsigned rmask = __ballot_sync(kFull, ready);
+    const unsigned smask = __ballot_sync(kFull, stop);
+    const int n_ready = (~rmask) ? __ffs(~rmask) - 1 : 32;
+    const int first_stop = smask ? __ffs(smask) - 1 : 32;
+    const int n_use = min(n_ready, first_stop + 1);
+    if (n_use == 0) { __nanosleep(32); continue; }
+    if (lane >= n_use) { S = 0.f; P = 1.f; }
+    float rS, rP, tS, tP;
+    warp_compose(S, P, lane, rS, rP, tS, tP);
+    cS = cS + cP * tS;
+    cP = cP * tP;
+    if (cP == 0.f || first_stop < n_use) break;
+    j0 += n_use;
+  }
+  return cS;
+}
+
+// Per-sequence return G_0 of the sequences starting in the window [.., w1) (from sequence lo
+// on; zero-length sequences at the buffer end belong to the last window).  G was written by this
+// warp: the caller's __syncwarp orders the reads after it.
+__device__ __forceinline__ void seq_returns(float* SR, const float* G, const int64_t* cum,
+                                            int64_t base, int64_t gs, int64_t pend, int64_t lo,
+                                            int64_t w1, int64_t ntok, int lane) {
+  if (SR == nullptr) return;
+  __syncwarp();
+  for (int64_t p0 = lo;; p0 += 32) {
+    const int64_t p = p0 + lane;
+    bool in = false;
+    if (p < pend) {
+      const int64_t s = cum[p] - base;
+      const int64_t L = cum[p + 1] - base - s;
+      in = s < w1 || (s == w1 && w1 == ntok);
+      if (in) SR[p - gs] = L > 0 ? G[s] : 0.f;
+    }
+    if (__ballot_sync(kFull, in) != kFull) break;
+  }
+}
+
+// The end of returns_kernel: zero-length ranks' sequence returns, the block's fp64
+// partials (one atomic per block), and the last CTA's reset of the claim counter + epoch.
+__device__ __forceinline__ void returns_epilogue(const AggArgs& a, const RankTable& rt,
+                                                 double (*red)[32], double s_m, double s_g,
+                                                 double s_g2, int nwarps) {
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  // ranks without tokens still owe their (zero-length) sequences a return
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    for (int ri = 0; ri < rt.n; ++ri) {
+      float* SR = a.seq_return[rt.rank[ri]];
+      if (SR == nullptr || rt.ntok[ri] != 0) continue;
+      for (int64_t j = lane; j < rt.cnt[ri]; j += 32) SR[j] = 0.f;
+    }
+  }
+
+  // warp, then block reduction of the fp64 partials; one atomic per block
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s_m += __shfl_xor_sync(kFull, s_m, off);
+    s_g += __shfl_xor_sync(kFull, s_g, off);
+    s_g2 += __shfl_xor_sync(kFull, s_g2, off);
+  }
+  if (lane == 0) { red[0][wid] = s_m; red[1][wid] = s_g; red[2][wid] = s_g2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double acc = 0.0;
+    for (int k = 0; k < nwarps; ++k) acc += red[threadIdx.x][k];
+    if (acc != 0.0) atomicAdd(a.partial + threadIdx.x, acc);
+  }
+  // the last CTA out resets the claim counter and advances the epoch (no host reset between
+  // launches or graph replays)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&a.ws->fin_ctr, 1u) == gridDim.x - 1) {
+      a.ws->work_ctr = 0;
+      a.ws->fin_ctr = 0;
+      a.ws->epoch = a.ws->epoch + 1u;
+      __threadfence();
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
   __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
   __shared__ float2 bmap[kWarps][kMaxNB];   // per batch: its map (pass 1), then its carry
   __shared__ float2 lmap[kWarps][kMaxNB][32];  // per batch and lane: exclusive suffix map (pass 1)
-  __shared__ double red[3][kWarps];
+  __shared__ double red[3][32];
   __shared__ uint32_t s_tag;
   __shared__ int s_ok;
   if (threadIdx.x == 0) {
@@ -277,17 +405,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     const int64_t* cum = a.plan.cum[0];
     const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
     const int64_t base = cum[gs];
-    for (int j = lane; j < nb * (kBatch / 32); j += 32) bm[j] = 0u;
-    __syncwarp();
-    const int64_t lo = first_at_least(cum, base, gs, pend, w0, lane);
-    for (int64_t p0 = lo;; p0 += 32) {
-      const int64_t p = p0 + lane;
-      const int64_t s = p <= pend ? cum[p] - base : INT64_MAX;
-      const bool in = s <= w1;
-      if (in && s > w0) atomicOr(&bm[(s - 1 - w0) >> 5], 1u << ((s - 1 - w0) & 31));
-      if (__ballot_sync(kFull, in) != kFull) break;
-    }
-    __syncwarp();
+    const int64_t lo = mark_ends(bm, nb * (kBatch / 32), cum, base, gs, pend, w0, w1, lane);
     // bit i: token i of this lane's 16 in batch b ends its sequence
     auto ends16 = [&](int b) { return (bm[16 * b + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu; };
 
@@ -321,43 +439,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
       st_word(&W[w].S, tag | 1u, wS);
       st_word(&W[w].P, tag | 1u, wP);
     }
-    float cS = 0.f, cP = 1.f;
-    for (int64_t j0 = w + 1; j0 < nwin;) {
-      const int64_t j = j0 + lane;
-      bool ready = false, stop = false;
-      float S = 0.f, P = 1.f;
-      if (j < nwin) {
-        const uint64_t wi = ld_word(&W[j].inc);
-        if (word_is(wi, tag | 2u)) {
-          ready = stop = true;
-          S = word_val(wi);
-          P = 0.f;
-        } else {
-          const uint64_t ws = ld_word(&W[j].S), wp = ld_word(&W[j].P);
-          if (word_is(ws, tag | 1u) && word_is(wp, tag | 1u)) {
-            ready = true;
-            S = word_val(ws);
-            P = word_val(wp);
-            stop = P == 0.f;
-          }
-        }
-      }
-      // usable prefix: ready lanes up to (and including) the first stopper
-      const unsigned rmask = __ballot_sync(kFull, ready);
-      const unsigned smask = __ballot_sync(kFull, stop);
-      const int n_ready = (~rmask) ? __ffs(~rmask) - 1 : 32;
-      const int first_stop = smask ? __ffs(smask) - 1 : 32;
-      const int n_use = min(n_ready, first_stop + 1);
-      if (n_use == 0) { __nanosleep(32); continue; }
-      if (lane >= n_use) { S = 0.f; P = 1.f; }
-      float rS, rP, tS, tP;
-      warp_compose(S, P, lane, rS, rP, tS, tP);
-      cS = cS + cP * tS;
-      cP = cP * tP;
-      if (cP == 0.f || first_stop < n_use) break;
-      j0 += n_use;
-    }
-    const float carry = cS;  // past the buffer end: G = 0
+    const float carry = look_back(W, w, nwin, tag, lane);  // past the buffer end: G = 0
     if (lane == 0) {
       st_word(&W[w].inc, tag | 2u, wS + wP * carry);
       float c = carry;  // carries into the batches, right to left
@@ -416,58 +498,11 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
 
     // per-sequence return G_0 of the sequences starting in the window (zero-length sequences
     // at the buffer end belong to the last window)
-    float* SR = a.seq_return[r];
-    if (SR != nullptr) {
-      __syncwarp();
-      for (int64_t p0 = lo;; p0 += 32) {
-        const int64_t p = p0 + lane;
-        bool in = false;
-        if (p < pend) {
-          const int64_t s = cum[p] - base;
-          const int64_t L = cum[p + 1] - base - s;
-          in = s < w1 || (s == w1 && w1 == rt.ntok[ri]);
-          if (in) SR[p - gs] = L > 0 ? G[s] : 0.f;
-        }
-        if (__ballot_sync(kFull, in) != kFull) break;
-      }
-    }
+    seq_returns(a.seq_return[r], G, cum, base, gs, pend, lo, w1, rt.ntok[ri], lane);
     __syncwarp();
   }
 
-  // ranks without tokens still owe their (zero-length) sequences a return
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    for (int ri = 0; ri < rt.n; ++ri) {
-      float* SR = a.seq_return[rt.rank[ri]];
-      if (SR == nullptr || rt.ntok[ri] != 0) continue;
-      for (int64_t j = lane; j < rt.cnt[ri]; j += 32) SR[j] = 0.f;
-    }
-  }
-
-  // warp, then block reduction of the fp64 partials; one atomic per block
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    s_m += __shfl_xor_sync(kFull, s_m, off);
-    s_g += __shfl_xor_sync(kFull, s_g, off);
-    s_g2 += __shfl_xor_sync(kFull, s_g2, off);
-  }
-  if (lane == 0) { red[0][wid] = s_m; red[1][wid] = s_g; red[2][wid] = s_g2; }
-  __syncthreads();
-  if (threadIdx.x < 3) {
-    double acc = 0.0;
-    for (int k = 0; k < kWarps; ++k) acc += red[threadIdx.x][k];
-    if (acc != 0.0) atomicAdd(a.partial + threadIdx.x, acc);
-  }
-  // the last CTA out resets the claim counter and advances the epoch (no host reset between
-  // launches or graph replays)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&a.ws->fin_ctr, 1u) == gridDim.x - 1) {
-      a.ws->work_ctr = 0;
-      a.ws->fin_ctr = 0;
-      a.ws->epoch = a.ws->epoch + 1u;
-      __threadfence();
-    }
-  }
+  returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
 }
 
 // A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks: one

@@ -57,7 +57,8 @@ def _gpu_ok():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("mode", ["fused", "staged"])
-@pytest.mark.parametrize("name", ["c1_dp2_dp1", "c3_dp4_tp4", "c4_dp4_sp2", "random"])
+@pytest.mark.parametrize("name", ["c1_dp2_dp1", "c3_dp4_tp4", "c4_dp4_sp2", "random",
+                                  "c3_dp8_dp2tp4", "c4_dp8_dp4sp2"])
 def test_p2p_exec_processes_share_one_gpu(name, mode):
     if not _gpu_ok():
         pytest.skip("needs a GPU")
@@ -73,6 +74,12 @@ def test_p2p_exec_processes_share_one_gpu(name, mode):
     elif name == "c4_dp4_sp2":
         world, lens = 4, W.c4_lengths(0)[:10].tolist()
         src, dst = W.config_layouts("c4", 4, 10)
+    elif name == "c3_dp8_dp2tp4":  # bench.py's N = 8 layouts (DP8 -> DP2 x TP4), 8 processes
+        world, lens = 8, W.c2_lengths(0)[:64].tolist()
+        src, dst = W.config_layouts("c3", 8, 64)
+    elif name == "c4_dp8_dp4sp2":  # config 4 at 8 ranks (DP8 -> DP4 x SP2)
+        world, lens = 8, W.c4_lengths(0)[:24].tolist()
+        src, dst = W.config_layouts("c4", 8, 24)
     else:
         from tests.helpers import random_layout
         rng = random.Random(3)
