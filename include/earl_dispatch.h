@@ -220,8 +220,11 @@ EARL_API earl_status_t earl_plan_destroy(earl_plan_t plan);
 
 /* Fused dispatch (SURVEY.md §8(a) a6 + a7): every source byte is read once and stored at
  * its final offset on every destination replica.
- * send_bufs: DEVICE field arrays this rank holds under `src` ([n_fields]; emulated:
+ * send_bufs: field arrays this rank holds under `src` ([n_fields]; emulated:
  *   [world][n_fields], rank-major), each n_src_tokens(rank) * B_f bytes, 16-B aligned.
+ *   DEVICE memory, or page-locked HOST memory mapped into the device address space
+ *   (cudaHostAlloc / cudaHostRegister under UVA): the kernel then reads it over PCIe itself
+ *   (zero-copy; no separate host-to-device copy).
  * recv_bufs: DEVICE field arrays under `dst`, sized n_local_tokens * B_f.  Multi-process
  *   comm with world > 1: each must lie inside this rank's window (earl_comm_alloc) at the
  *   same offset on every rank -- peers store into it over NVLink.  Ranks not in the dst
@@ -234,7 +237,8 @@ EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* s
                                  void* const* recv_bufs, void* stream);
 /* Staged path, step a3: gather this rank's segments into one contiguous message per
  * destination shard (field-major, each field block 16-byte aligned) in stage_bufs
- * ([1] or emulated [world]; size earl_plan_stats().stage_bytes[rank]). */
+ * ([1] or emulated [world]; size earl_plan_stats().stage_bytes[rank]).  send_bufs as for
+ * earl_dispatch_exec (device, or mapped pinned host memory). */
 EARL_API earl_status_t earl_dispatch_pack(earl_plan_t plan, const void* const* send_bufs,
                                  void* const* stage_bufs, void* stream);
 /* Staged path, step a5: scatter packed messages into the final field arrays.

@@ -27,10 +27,11 @@ def random_layout(rng: random.Random, world: int, n: int, allow_lpt=True):
 
 
 def run_gpu_case(src, dst, lens, fields, world, mode="exec", seed=0, check_plan=True,
-                 guard=256, ed=None):
+                 guard=256, ed=None, host_src=False):
     """Dispatch on the GPU (emulated comm) and compare byte for byte with the oracle.
 
-    mode: "exec" (fused direct) or "stage" (pack + unpack).  Returns the plan stats."""
+    mode: "exec" (fused direct) or "stage" (pack + unpack).  host_src: the source arrays are
+    pinned HOST memory read by the kernels over PCIe (zero-copy).  Returns the plan stats."""
     import torch
     from paper_2510_05943_b200.dispatch import EmulatedDispatch
 
@@ -53,7 +54,8 @@ def run_gpu_case(src, dst, lens, fields, world, mode="exec", seed=0, check_plan=
     for r in range(world):
         for f in range(len(fields)):
             if r in src_arrays and src_arrays[r][f].size:
-                send.append(torch.from_numpy(src_arrays[r][f]).to(dev))
+                t = torch.from_numpy(src_arrays[r][f])
+                send.append(t.pin_memory() if host_src else t.to(dev))
             else:
                 send.append(None)
     bufs, recv = [], []

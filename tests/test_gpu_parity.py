@@ -58,6 +58,21 @@ def test_random_layouts(seed):
     run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
 
 
+@pytest.mark.parametrize("mode", ["exec", "stage"])
+@pytest.mark.parametrize("seed", range(6))
+def test_host_pinned_sources_zero_copy(seed, mode):
+    """Source arrays in pinned host memory (UVA): the copy kernel's TMA loads read them over
+    PCIe, no separate H2D copy; the result is the same bytes."""
+    rng = random.Random(100 + seed)
+    world = rng.randint(2, 8)
+    n = rng.randint(1, 200)
+    lens = [rng.choice([0, 1, 17, rng.randint(0, 500)]) for _ in range(n)]
+    src = random_layout(rng, world, n)
+    dst = random_layout(rng, world, n)
+    fields = rng.sample(ODD_FIELDS, rng.randint(1, len(ODD_FIELDS)))
+    run_gpu_case(src, dst, lens, fields, world, mode=mode, seed=seed, host_src=True)
+
+
 @pytest.mark.parametrize("n_gpus", [2, 4, 8])
 def test_c3_layouts_scalar6(n_gpus):
     """Config 3 shape (DPn -> DP max(1,n/4) x TP min(4,n)) on a 128-sequence slice of config 2."""
