@@ -390,8 +390,11 @@ cudaError_t plan_launch(earl_plan* p, cudaStream_t s) {
     cudaStreamSynchronize(s);
     fprintf(stderr, "earl plan trace N=%lld G=%d us:", (long long)a.N, p->grid);
     for (int k = 1; k < 8; ++k) fprintf(stderr, " p%d=%.1f", k - 1, (ts[k] - ts[k - 1]) / 1e3);
-    fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]\n", (ts[7] - ts[0]) / 1e3,
+    fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]", (ts[7] - ts[0]) / 1e3,
             (ts[8] - ts[5]) / 1e3, (ts[9] - ts[8]) / 1e3, (ts[6] - ts[9]) / 1e3);
+    fprintf(stderr, " [p2 src: part %.1f, gtok %.1f, scans %.1f; dst: part %.1f, gtok %.1f, scans %.1f]\n",
+            (ts[10] - ts[2]) / 1e3, (ts[11] - ts[10]) / 1e3, (ts[12] - ts[11]) / 1e3,
+            (ts[13] - ts[12]) / 1e3, (ts[14] - ts[13]) / 1e3, (ts[15] - ts[14]) / 1e3);
     cudaFreeAsync(a.phase_ts, s);
     a.phase_ts = nullptr;
   }

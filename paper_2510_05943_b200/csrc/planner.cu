@@ -451,18 +451,28 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
       if (lead) lpt_assign(a, l, lpt_keys);
       continue;
     }
+    // GIVEN_COUNTS and CONTIG groups are monotone in i: their starts are published here and
+    // phase 2 needs no partition for them
+    if (L.assign == EARL_ASSIGN_GIVEN_COUNTS && lead && tid <= D)
+      h->group_start[l][tid] = L.count_start[tid];
+    auto contig = [&](int64_t i) -> int {
+      if (T == 0) {  // count blocks, earlier groups take the extra
+        const int64_t q = N / D, r = N % D;
+        return (i < r * (q + 1)) ? (int)(i / (q + 1)) : (int)(r + (i - r * (q + 1)) / q);
+      }
+      const int64_t m = ((int64_t)D * (2 * a.P[i] + a.lens[i])) / (2 * T);
+      return (int)(m < D - 1 ? m : D - 1);
+    };
     for (int64_t i = gtid; i < N; i += gstride) {
       int g = 0;
       if (L.assign == EARL_ASSIGN_GIVEN_COUNTS) {
         while (g < D - 1 && i >= L.count_start[g + 1]) ++g;
       } else if (L.assign == EARL_ASSIGN_CONTIG) {
-        if (T == 0) {  // count blocks, earlier groups take the extra
-          const int64_t q = N / D, r = N % D;
-          g = (i < r * (q + 1)) ? (int)(i / (q + 1)) : (int)(r + (i - r * (q + 1)) / q);
-        } else {
-          const int64_t m = ((int64_t)D * (2 * a.P[i] + a.lens[i])) / (2 * T);
-          g = (int)(m < D - 1 ? m : D - 1);
-        }
+        g = contig(i);
+        const int gp = i > 0 ? contig(i - 1) : -1;  // groups gp+1 .. g start at i
+        for (int k = gp + 1; k <= g; ++k) h->group_start[l][k] = i;
+        if (i == N - 1)
+          for (int k = g + 1; k <= D; ++k) h->group_start[l][k] = N;
       } else {  // EXPLICIT
         g = L.group_of_seq[i];
         if (g < 0 || g >= D) { latch(h, EARL_ERR_LAYOUT, (int)i); g = 0; }
@@ -475,62 +485,97 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   // ---- phase 2: per-layout group order and local token offsets ------------------------
   stamp(a, 2);
   __shared__ int64_t s_gtok[2][kMaxShards];
+  __shared__ int64_t s_gstart[kMaxShards + 1];
   for (int l = 0; l < 2; ++l) {
     const LayoutDesc& L = a.lay[l];
     const int D = L.dp, SP = L.sp;
     const int32_t* grp = a.grp[l];
     int32_t* perm = a.perm[l];
-    partition_array(grp, N, D, perm, a.ghist, ps);
-    if (lead) {
-      if (tid <= D) h->group_start[l][tid] = ps.bstart[tid];
-      if (tid < D) h->group_count[l][tid] = ps.bstart[tid + 1] - ps.bstart[tid];
+    // monotone groups (GIVEN_COUNTS, CONTIG): the stable partition by group is the identity
+    // and every per-sequence value below is written and first read by the same thread
+    const bool mono = L.assign == EARL_ASSIGN_GIVEN_COUNTS || L.assign == EARL_ASSIGN_CONTIG;
+    if (mono) {
+      for (int64_t j = gtid; j < N; j += gstride) perm[j] = (int32_t)j;
+      if (tid <= D) s_gstart[tid] = __ldcg(&h->group_start[l][tid]);  // phase 1 (other CTAs)
+      __syncthreads();
+    } else {
+      partition_array(grp, N, D, perm, a.ghist, ps);
+      if (lead && tid <= D) h->group_start[l][tid] = ps.bstart[tid];
+      if (tid <= D) s_gstart[tid] = ps.bstart[tid];
+      gsync();
     }
-    __shared__ int64_t s_gstart[kMaxShards + 1];
-    if (tid <= D) s_gstart[tid] = ps.bstart[tid];
-    gsync();
+    stamp(a, 10 + 3 * l);
+    if (lead && tid < D) h->group_count[l][tid] = s_gstart[tid + 1] - s_gstart[tid];
     if (L.split == EARL_SP_FLAT || L.split == EARL_SP_THRESHOLD) {
       // position of every sequence in its group, and its offset in the group's token stream
-      int64_t* cum0 = a.cum[l];
-      for (int64_t j = gtid; j < N; j += gstride) {
-        const int i = perm[j];
-        a.pos[l][i] = (int32_t)(j - s_gstart[grp[i]]);
-        a.vtmp[j] = a.lens[i];
+      if (mono) {  // the group streams are slices of P
+        for (int64_t j = gtid; j < N; j += gstride) {
+          const int64_t s0 = s_gstart[grp[j]];
+          a.pos[l][j] = (int32_t)(j - s0);
+          a.gpos[l][j] = a.P[j] - a.P[s0];
+        }
+        if (tid < D) s_gtok[l][tid] = a.P[s_gstart[tid + 1]] - a.P[s_gstart[tid]];
+        __syncthreads();
+      } else {
+        int64_t* cum0 = a.cum[l];
+        for (int64_t j = gtid; j < N; j += gstride) {
+          const int i = perm[j];
+          a.pos[l][i] = (int32_t)(j - s_gstart[grp[i]]);
+          a.vtmp[j] = a.lens[i];
+        }
+        gsync();
+        const int64_t tot = scan_array(a.vtmp, cum0, N, a.cta_sums, sm_scan);
+        if (lead && tid == 0) cum0[N] = tot;
+        gsync();
+        for (int64_t j = gtid; j < N; j += gstride) {
+          const int i = perm[j];
+          a.gpos[l][i] = cum0[j] - cum0[s_gstart[grp[i]]];
+        }
+        if (tid < D) s_gtok[l][tid] = cum0[s_gstart[tid + 1]] - cum0[s_gstart[tid]];
+        gsync();
       }
-      gsync();
-      const int64_t tot = scan_array(a.vtmp, cum0, N, a.cta_sums, sm_scan);
-      if (lead && tid == 0) cum0[N] = tot;
-      gsync();
-      for (int64_t j = gtid; j < N; j += gstride) {
-        const int i = perm[j];
-        a.gpos[l][i] = cum0[j] - cum0[s_gstart[grp[i]]];
-      }
-      if (tid < D) s_gtok[l][tid] = cum0[s_gstart[tid + 1]] - cum0[s_gstart[tid]];
-      gsync();
     } else if (tid < D) {
       s_gtok[l][tid] = 0;
     }
     if (lead && tid < D) h->group_tokens[l][tid] = s_gtok[l][tid];
-    for (int k = 0; k < SP; ++k) {
-      int64_t* cum = a.cum[l] + (int64_t)k * (N + 1);
-      int64_t* off = a.off[l] + (int64_t)k * N;
-      for (int64_t j = gtid; j < N; j += gstride)
-        a.vtmp[j] = make_chunker(a, l, perm[j], s_gtok[l]).held(k);
-      gsync();
-      const int64_t tot = scan_array(a.vtmp, cum, N, a.cta_sums, sm_scan);
-      if (lead && tid == 0) cum[N] = tot;
-      gsync();
-      for (int64_t j = gtid; j < N; j += gstride) {
-        const int i = perm[j];
-        off[i] = cum[j] - cum[s_gstart[grp[i]]];
+    stamp(a, 11 + 3 * l);
+    if (mono && SP == 1) {
+      // one chunk holding the whole sequence, in index order: the chunk scan is P itself
+      int64_t* cum = a.cum[l];
+      int64_t* off = a.off[l];
+      for (int64_t j = gtid; j <= N; j += gstride) {
+        cum[j] = a.P[j];
+        if (j < N) off[j] = a.P[j] - a.P[s_gstart[grp[j]]];
       }
       if (lead && tid < D) {
-        const int64_t st = cum[s_gstart[tid + 1]] - cum[s_gstart[tid]];
-        h->shard_tokens[l][tid * SP + k] = st;
-        if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid * SP + k);
+        const int64_t st = a.P[s_gstart[tid + 1]] - a.P[s_gstart[tid]];
+        h->shard_tokens[l][tid] = st;
+        if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid);
       }
-      // the next scan begins with a barrier-free read of lens/perm only; off and shard_tokens
-      // are consumed after later barriers
+    } else {
+      for (int k = 0; k < SP; ++k) {
+        int64_t* cum = a.cum[l] + (int64_t)k * (N + 1);
+        int64_t* off = a.off[l] + (int64_t)k * N;
+        for (int64_t j = gtid; j < N; j += gstride)
+          a.vtmp[j] = make_chunker(a, l, perm[j], s_gtok[l]).held(k);
+        gsync();
+        const int64_t tot = scan_array(a.vtmp, cum, N, a.cta_sums, sm_scan);
+        if (lead && tid == 0) cum[N] = tot;
+        gsync();
+        for (int64_t j = gtid; j < N; j += gstride) {
+          const int i = perm[j];
+          off[i] = cum[j] - cum[s_gstart[grp[i]]];
+        }
+        if (lead && tid < D) {
+          const int64_t st = cum[s_gstart[tid + 1]] - cum[s_gstart[tid]];
+          h->shard_tokens[l][tid * SP + k] = st;
+          if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid * SP + k);
+        }
+        // the next scan begins with a barrier-free read of lens/perm only; off and
+        // shard_tokens are consumed after later barriers
+      }
     }
+    stamp(a, 12 + 3 * l);
     gsync();
   }
 
