@@ -22,6 +22,14 @@ for seed in range(4):
     src = with_split(rng, random_layout(rng, world, n))
     dst = with_split(rng, random_layout(rng, world, n))
     run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage"]), seed=seed)
+# the cooperative multi-CTA planner (N = 9000: 3 CTAs) with monotone layouts (GIVEN_COUNTS ->
+# CONTIG, no phase-2 partition) and with an EXPLICIT destination; zero-copy host sources
+rng = random.Random(77)
+lensN = [rng.randint(0, 40) for _ in range(9000)]
+run_gpu_case(W.rollout_layout(9000, 4), W.layout(dp=2, tp=2, assign="contig"), lensN, fields, 4)
+run_gpu_case(W.rollout_layout(9000, 4), W.layout(dp=4, assign="explicit", group_of_seq=[i % 4 for i in range(9000)]),
+             lensN, fields, 4, mode="stage")
+run_gpu_case(W.rollout_layout(8, 2), W.layout(dp=1, tp=2, assign="contig"), lens8, fields, 2, host_src=True)
 # NEXT-2: per-sequence fields, returns (look-back across windows, zero-length sequences,
 # unaligned scalar path) and advantages, each against the oracle
 from tests.test_gpu_parity import _adv_case  # noqa: E402
