@@ -391,12 +391,24 @@ def run_single(args):
         h2d = sum(h.numel() for h in host_send) + lens_host.numel() * 4
         d2h = sum(m.numel() * 4 for m in metas.values())
 
+        # the host-to-device copies run on a copy stream, one source rank after another; each
+        # source's dispatch (earl_dispatch_exec_src) starts as soon as its bytes are resident,
+        # so the copy engines and the SMs overlap (the copies still all sit in the timed region)
+        copy_stream = torch.cuda.Stream(device=dev)
+        ready = [torch.cuda.Event() for _ in range(R)]
+
         def e2e_step():
-            for h, d in zip(host_send, send):
-                d.copy_(h, non_blocking=True)
             lens_dev.copy_(lens_host, non_blocking=True)
             splan.replan(lens_dev, stream)
-            splan.exec(send, recv, stream)
+            copy_stream.wait_stream(stream)  # the previous step's dispatch has read `send`
+            with torch.cuda.stream(copy_stream):
+                for r in range(R):
+                    for f in range(F):
+                        send[r * F + f].copy_(host_send[r * F + f], non_blocking=True)
+                    ready[r].record(copy_stream)
+            for r in range(R):
+                stream.wait_event(ready[r])
+                splan.exec_src(r, send, recv, stream)
             for r in dst_ranks:
                 splan.local_meta(r, metas[r], None, None, stream)
                 meta_host[r].copy_(metas[r], non_blocking=True)
@@ -417,7 +429,9 @@ def run_single(args):
         ems = a.elapsed_time(b) / n_e2e
         out["e2e"] = {"value": payload / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
                       "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                      "steps": n_e2e}
+                      "steps": n_e2e,
+                      "path": "pinned host -> HBM per source rank on a copy stream, overlapped "
+                              "with earl_dispatch_exec_src of the sources already resident"}
         del host_send
 
     if clocks:

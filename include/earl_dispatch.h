@@ -235,6 +235,18 @@ EARL_API earl_status_t earl_plan_destroy(earl_plan_t plan);
  * call, this rank's recv buffers are complete.  A peer missing for > 10 s latches TIMEOUT. */
 EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* send_bufs,
                                  void* const* recv_bufs, void* stream);
+/* The fused dispatch of ONE source rank's records (data leaves "from their
+ * computation origins"), to every destination replica it feeds; arguments as for
+ * earl_dispatch_exec (only src_rank's send buffers are read).  Emulated comm: lets a source's
+ * dispatch start as soon as its data is resident (e.g. overlapping the host-to-device copies of
+ * the other sources); once every source rank has been executed, in any order, the recv buffers
+ * equal those of one earl_dispatch_exec.  Multi-process comm: src_rank must be this rank (the
+ * call is earl_dispatch_exec).  Launches of one plan share its scheduling counters: issue them
+ * in one stream order, never concurrently.  Errors: INVALID_ARGUMENT for src_rank outside
+ * [0, world) (or not this rank). */
+EARL_API earl_status_t earl_dispatch_exec_src(earl_plan_t plan, int32_t src_rank,
+                                              const void* const* send_bufs,
+                                              void* const* recv_bufs, void* stream);
 /* Staged path, step a3: gather this rank's segments into one contiguous message per
  * destination shard (field-major, each field block 16-byte aligned) in stage_bufs
  * ([1] or emulated [world]; size earl_plan_stats().stage_bytes[rank]).  send_bufs as for

@@ -842,8 +842,12 @@ earl_status_t set_src(earl_plan_t p, CopyArgs& a, const void* const* bufs) {
 
 }  // namespace
 
-extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* send_bufs,
-                                            void* const* recv_bufs, void* stream) {
+namespace {
+
+// view: -1 = every record this comm executes (emulated: all source ranks; else this rank's),
+// r >= 0 = source rank r's records only (emulated comm)
+earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
+                        void* const* recv_bufs, void* stream) {
   if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
   earl_comm* c = p->comm;
   if (!c->peers_ready)
@@ -853,6 +857,7 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CopyArgs a;
   fill_copy_args(p, a, kDirect);
+  if (view >= 0) a.view_rank = view;
   earl_status_t st = set_src(p, a, send_bufs);
   if (st != EARL_OK) return st;
   const int F = p->n_fields;
@@ -898,6 +903,29 @@ extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* se
   g_launches.fetch_add(1);
   p->synced = false;
   return EARL_OK;
+}
+
+}  // namespace
+
+extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* send_bufs,
+                                            void* const* recv_bufs, void* stream) {
+  return exec_impl(p, -1, send_bufs, recv_bufs, stream);
+}
+
+extern "C" earl_status_t earl_dispatch_exec_src(earl_plan_t p, int32_t src_rank,
+                                                const void* const* send_bufs,
+                                                void* const* recv_bufs, void* stream) {
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  earl_comm* c = p->comm;
+  if (src_rank < 0 || src_rank >= c->world)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "src_rank %d outside [0, %d)", src_rank, c->world);
+  if (!c->emulated) {
+    if (src_rank != c->rank)
+      return fail(EARL_ERR_INVALID_ARGUMENT, "multi-process comm: src_rank %d is not this rank (%d)",
+                  src_rank, c->rank);
+    return exec_impl(p, -1, send_bufs, recv_bufs, stream);
+  }
+  return exec_impl(p, src_rank, send_bufs, recv_bufs, stream);
 }
 
 extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* send_bufs,

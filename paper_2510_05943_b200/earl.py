@@ -35,8 +35,8 @@ EXPORTED = [
     "earl_comm_create", "earl_comm_export_handle", "earl_comm_import_peers", "earl_comm_alloc",
     "earl_comm_reset_alloc", "earl_comm_info", "earl_comm_destroy", "earl_dispatch_plan",
     "earl_plan_replan", "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
-    "earl_plan_export", "earl_plan_groups", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_pack",
-    "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
+    "earl_plan_export", "earl_plan_groups", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_exec_src",
+    "earl_dispatch_pack", "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
     "earl_abi_version", "earl_kernel_launch_count", "earl_speedup_pct", "earl_policy_build",
     "earl_policy_table", "earl_policy_select", "earl_policy_destroy", "earl_plan_mean_length",
 ]
@@ -127,6 +127,7 @@ def lib():
         "earl_plan_destroy": [vp],
         "earl_plan_groups": [vp, vp, vp, vp],
         "earl_dispatch_exec": [vp, pvp, pvp, vp],
+        "earl_dispatch_exec_src": [vp, i32, pvp, pvp, vp],
         "earl_dispatch_pack": [vp, pvp, pvp, vp],
         "earl_dispatch_unpack": [vp, pvp, pvp, vp],
         "earl_plan_messages": [vp, i32, vp, vp, vp, vp],
@@ -340,6 +341,11 @@ class Plan:
     def exec(self, send_bufs, recv_bufs, stream=None):
         s, r = _ptr_array(send_bufs), _ptr_array(recv_bufs)
         check(lib().earl_dispatch_exec(self.h, s, r, _stream(stream)))
+
+    def exec_src(self, src_rank, send_bufs, recv_bufs, stream=None):
+        """earl_dispatch_exec_src: only source rank src_rank's records."""
+        s, r = _ptr_array(send_bufs), _ptr_array(recv_bufs)
+        check(lib().earl_dispatch_exec_src(self.h, int(src_rank), s, r, _stream(stream)))
 
     def pack(self, send_bufs, stage_bufs, stream=None):
         s, t = _ptr_array(send_bufs), _ptr_array(stage_bufs)

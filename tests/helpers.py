@@ -30,7 +30,8 @@ def run_gpu_case(src, dst, lens, fields, world, mode="exec", seed=0, check_plan=
                  guard=256, ed=None, host_src=False):
     """Dispatch on the GPU (emulated comm) and compare byte for byte with the oracle.
 
-    mode: "exec" (fused direct) or "stage" (pack + unpack).  host_src: the source arrays are
+    mode: "exec" (fused direct), "exec_src" (fused, one launch per source rank) or "stage"
+    (pack + unpack).  host_src: the source arrays are
     pinned HOST memory read by the kernels over PCIe (zero-copy).  Returns the plan stats."""
     import torch
     from paper_2510_05943_b200.dispatch import EmulatedDispatch
@@ -70,6 +71,11 @@ def run_gpu_case(src, dst, lens, fields, world, mode="exec", seed=0, check_plan=
             recv.append(buf[guard:guard + n] if n else None)
     if mode == "exec":
         plan.exec(send, recv)
+    elif mode == "exec_src":  # one launch per source rank, in a seeded random order
+        order = list(range(world))
+        random.Random(seed).shuffle(order)
+        for r in order:
+            plan.exec_src(r, send, recv)
     else:
         stage = ed.alloc_stage(plan)
         for s_ in stage:

@@ -73,6 +73,32 @@ def test_host_pinned_sources_zero_copy(seed, mode):
     run_gpu_case(src, dst, lens, fields, world, mode=mode, seed=seed, host_src=True)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_exec_per_source_rank(seed):
+    """earl_dispatch_exec_src for every source rank, in a random order, equals one exec."""
+    rng = random.Random(200 + seed)
+    world = rng.randint(1, 8)
+    n = rng.randint(0, 150)
+    lens = [rng.choice([0, 1, 17, rng.randint(0, 700)]) for _ in range(n)]
+    src = random_layout(rng, world, n)
+    dst = random_layout(rng, world, n)
+    fields = rng.sample(ODD_FIELDS, rng.randint(1, len(ODD_FIELDS)))
+    run_gpu_case(src, dst, lens, fields, world, mode="exec_src", seed=seed,
+                 host_src=seed % 2 == 1)
+
+
+def test_exec_src_rank_out_of_range():
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    ed = EmulatedDispatch(2)
+    plan = ed.plan(W.rollout_layout(8, 2), W.layout(dp=1, assign="contig"), GOLD_LENS,
+                   W.field_set("tiny3"))
+    for bad in (-1, 2):
+        with pytest.raises(EarlError):
+            plan.exec_src(bad, [None] * 6, [None] * 6)
+    plan.destroy()
+
+
 @pytest.mark.parametrize("n_gpus", [2, 4, 8])
 def test_c3_layouts_scalar6(n_gpus):
     """Config 3 shape (DPn -> DP max(1,n/4) x TP min(4,n)) on a 128-sequence slice of config 2."""
