@@ -1137,7 +1137,13 @@ extern "C" earl_status_t earl_advantages(earl_plan_t p, const double* stats, flo
   if ((st = set_per_rank<float>(p, a.adv, (const void* const*)adv, "adv", true)) != EARL_OK) return st;
   DeviceGuard g(p->comm->device);
   clear_stale_error();
-  cudaError_t e = launch_advantages(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
+  // the source ranks' tokens this launch covers, when the host knows the plan (else -1)
+  int64_t tokens = -1;
+  if (p->synced) {
+    const earl_layout_t& S = p->lay[0];
+    tokens = p->comm->emulated ? p->host_hdr.T * S.tp : (p->host_hdr.T + S.dp - 1) / S.dp;
+  }
+  cudaError_t e = launch_advantages(a, p->comm->sm_count, tokens, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "advantages launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
   return EARL_OK;

@@ -177,7 +177,7 @@ struct AggArgs {
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
 int64_t returns_windows(int64_t tokens);
-cudaError_t launch_advantages(const AggArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s);

@@ -29,6 +29,7 @@ for name, lens in (("C2 batch (512 x <=8K)", W.c2_lengths(0)),
     src = W.rollout_layout(n, 8)
     ed = EmulatedDispatch(8)
     plan = ed.plan(src, W.layout(dp=2, tp=4, assign="contig"), lens, W.field_set("tiny3"))
+    plan.sync()  # the host learns the batch's size (as any caller sizing its buffers does)
     tok = W.rollout_token_counts(lens, src["counts"])
     r = [torch.randn(max(t, 1), device="cuda") for t in tok]
     m = [(torch.rand(max(t, 1), device="cuda") < 0.8).to(torch.uint8) for t in tok]
