@@ -116,6 +116,22 @@ def test_c4_layouts_sp2(n_gpus):
                  mode="stage" if n_gpus == 4 else "exec")
 
 
+@pytest.mark.parametrize("mode", ["exec", "stage"])
+def test_alignment_every_residue_pair(mode):
+    """SURVEY.md §4 copy-core fuzz: 1-byte field pieces of 0-1100 B whose source and destination
+    offsets cover every (src mod 16, dst mod 16) pair (asserted on the oracle's table), so
+    every realignment shift, head and tail of the copy engine runs against the oracle."""
+    rng = random.Random(16)
+    n = 2500
+    lens = [rng.randint(0, 1100) for _ in range(n)]
+    src = W.layout(dp=2, assign="given_counts", counts=[n // 2, n - n // 2])
+    dst = W.layout(dp=3, assign="explicit", group_of_seq=[rng.randrange(3) for _ in range(n)])
+    segs = O.route(src, dst, lens, 3)
+    pairs = {(r[5] % 16, r[6] % 16) for r in segs if r[4] > r[3]}
+    assert len(pairs) == 256, len(pairs)
+    run_gpu_case(src, dst, lens, [("b", 1, 1, "x"), ("t", 1, 3, "x")], 3, mode=mode, seed=16)
+
+
 def test_c2_full_scalar6_exec_and_stage():
     """BASELINE.json configs[1] at full size (512 episodes) with the scalar6 fields, 8-rank
     emulation of rollout DP8 -> train DP2 x TP4, element by element against the oracle."""
