@@ -99,6 +99,24 @@ def test_exec_src_rank_out_of_range():
     plan.destroy()
 
 
+def test_spec_acceptance_500_random_layout_pairs():
+    """SPEC.md acceptance #4 (500 randomized layout pairs, bitwise equal to the oracle) scaled to
+    tokens: every byte, the metadata and the canonical plan table of each case."""
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    rng = random.Random(4)
+    eds = {}
+    for case in range(500):
+        world = rng.randint(1, 8)
+        n = rng.randint(0, 60)
+        lens = [rng.choice([0, 1, 5, rng.randint(0, 200)]) for _ in range(n)]
+        src = random_layout(rng, world, n)
+        dst = random_layout(rng, world, n)
+        fields = rng.sample(ODD_FIELDS, rng.randint(1, 3))
+        ed = eds.setdefault(world, EmulatedDispatch(world))
+        run_gpu_case(src, dst, lens, fields, world, mode=rng.choice(["exec", "stage", "exec_src"]),
+                     seed=1000 + case, ed=ed, guard=32)
+
+
 @pytest.mark.parametrize("n_gpus", [2, 4, 8])
 def test_c3_layouts_scalar6(n_gpus):
     """Config 3 shape (DPn -> DP max(1,n/4) x TP min(4,n)) on a 128-sequence slice of config 2."""
