@@ -81,6 +81,13 @@ static int gpu_part(void) {
   int32_t got[209];
   CHECK(cudaMemcpy(got, d_dst[0], sizeof(got), cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
   CHECK(memcmp(got, want, sizeof(got)) == 0, "destination bytes differ");
+  /* per-source dispatch: source ranks 1 then 0 into a cleared buffer give the same bytes */
+  CHECK(cudaMemset(d_dst[0], 0, 209 * 4) == cudaSuccess, "memset");
+  CHECK(earl_dispatch_exec_src(plan, 1, send, recv, NULL) == EARL_OK, "exec_src 1: %s", earl_last_error());
+  CHECK(earl_dispatch_exec_src(plan, 0, send, recv, NULL) == EARL_OK, "exec_src 0: %s", earl_last_error());
+  CHECK(earl_dispatch_exec_src(plan, 2, send, recv, NULL) == EARL_ERR_INVALID_ARGUMENT, "exec_src range");
+  CHECK(cudaMemcpy(got, d_dst[0], sizeof(got), cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
+  CHECK(memcmp(got, want, sizeof(got)) == 0, "per-source destination bytes differ");
   int32_t* d_cu = NULL;
   CHECK(cudaMalloc((void**)&d_cu, 9 * 4) == cudaSuccess, "malloc");
   CHECK(earl_plan_local_meta(plan, 0, d_cu, NULL, NULL, NULL) == EARL_OK, "meta");
