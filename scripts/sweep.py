@@ -126,6 +126,32 @@ def main():
     out = os.path.join(ROOT, "gpurun_out", f"{tag}_sweep.json")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     json.dump({"about": __doc__, "hbm_peak_Bps": HBM, "nvlink_Bps": NVL, "rows": rows}, open(out, "w"), indent=1)
+    write_md(rows, tag, out[:-5] + ".md")
+
+
+def write_md(rows, tag, path):
+    head = [
+        f"# C5 bandwidth sweep, {tag} (1 B200, 8-rank emulation; scripts/sweep.py)", "",
+        "a2a = plan + fused exec (DP8 -> DP8 round-robin all-to-allv); cent = centralized gather-and-dispatch "
+        "via rank 0 (two plans + two execs).",
+        "Measured times are CUDA-event medians with an L2 flush before each repetition. On one GPU every byte "
+        "moves through HBM, so the",
+        "measured centralized/a2a ratio is ~2 (two passes). The NVLink columns are the SURVEY.md §8(d) model "
+        "for a real 8-GPU box",
+        "(bottleneck link bytes / 770 GB/s): the controller serialises both phases, ratio = 2W = 16 for "
+        "uniform payloads.", "",
+        "| series | lengths | MiB/rank | N | a2a ms | a2a GB/s | HBM frac | cent ms | measured ratio | "
+        "NVLink model a2a ms | NVLink model cent ms | model ratio |",
+        "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    lines = []
+    for r in rows:
+        lines.append(
+            f"| {r['series']} ({r['fields']}) | {'uniform' if r['lengths'] == 'uniform' else 'longtail'} | "
+            f"{r['per_rank_MiB']} | {r['n_seqs']} | {r['a2a_ms']:.3f} | {r['a2a_GBps']:.0f} | "
+            f"{r['a2a_hbm_frac']:.3f} | {r['cent_ms']:.3f} | {r['measured_ratio']:.2f} | "
+            f"{r['nvlink_model_a2a_ms']:.3f} | {r['nvlink_model_cent_ms']:.3f} | "
+            f"{(r['nvlink_model_ratio'] or 0):.1f} |")
+    open(path, "w").write("\n".join(head + lines) + "\n")
 
 
 if __name__ == "__main__":
