@@ -235,6 +235,96 @@ __device__ __forceinline__ float tok_r(const Batch& B, int i) {
   return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w;
 }
 
+#ifndef EARL_AGG_TMA
+#define EARL_AGG_TMA 0
+#endif
+constexpr int kSlotBytes = kBatch * 4 + kBatch;  // a batch's rewards, then its mask bytes
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Per-warp 2-slot ring of whole batches loaded by TMA bulk copies (no LSU wavefronts on the
+// global side).  Slot uses alternate; every use completes one phase of the slot's mbarrier (a
+// batch that is not whole and 16-B aligned arrives without a copy and is read from global).
+struct BatchRing {
+  uint8_t* mem;       // this warp's 2 slots
+  uint64_t* bar;      // this warp's 2 mbarriers
+  uint32_t issued, got;
+  bool tma[2];
+
+  __device__ __forceinline__ void init(uint8_t* m, uint64_t* b, int lane) {
+    mem = m; bar = b; issued = got = 0; tma[0] = tma[1] = false;
+    if (lane == 0) {
+      for (int s = 0; s < 2; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  // start loading batch [t0, t0 + kBatch) into the next slot (its previous batch is consumed)
+  __device__ __forceinline__ void issue(const float* rw, const uint8_t* mk, int64_t t0, int64_t w1,
+                                        bool vec, int lane) {
+    const int s = issued & 1;
+    const bool whole = vec && t0 + kBatch <= w1;
+    tma[s] = whole;
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t b = smem_addr(&bar[s]);
+      if (whole) {
+        uint8_t* dst = mem + s * kSlotBytes;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                     "r"((uint32_t)kSlotBytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(dst)), "l"(rw + t0), "r"((uint32_t)(kBatch * 4)), "r"(b) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(dst + kBatch * 4)), "l"(mk + t0), "r"((uint32_t)kBatch), "r"(b)
+            : "memory");
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+      }
+    }
+    ++issued;
+  }
+  // this lane's 16 tokens of the oldest issued batch (its lane tokens start at t)
+  template <bool kLastUse>
+  __device__ __forceinline__ void get(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
+                                      int64_t w1, bool vec, int lane) {
+    const int s = got & 1;
+    const uint32_t parity = (got >> 1) & 1;
+    const uint32_t b = smem_addr(&bar[s]);
+    uint32_t done;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          " selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done) : "r"(b), "r"(parity) : "memory");
+    } while (!done);
+    ++got;
+    if (!tma[s]) {
+      load_batch<kLastUse>(B, rw, mk, t, w1, vec);
+      return;
+    }
+    // rotated chunk order: lanes 2j, 2j+1 of a quarter-warp start at chunk j, so the 8
+    // 16-B reads of a phase hit 8 distinct bank groups (a lane's 64 B span 4 of them)
+    const uint8_t* rb = mem + s * kSlotBytes + 64 * lane;
+    const int rot = (lane >> 1) & 3;
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
+    // v[k] is chunk (k + rot) & 3: rotate so that B.r[c] = v[(c - rot) & 3]
+    float4 u[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) B.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
+    B.m = *reinterpret_cast<const uint4*>(mem + s * kSlotBytes + kBatch * 4 + 16 * lane);
+  }
+};
+
 // Decoupled look-back for window w of a rank (windows w+1 .. nwin-1 lie to its right), 32
 // windows per round trip: compose their maps up to the first inclusive value or zero slope (a
 // sequence end); returns G just right of the window (0 past the buffer end).
@@ -351,6 +441,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   __shared__ double red[3][32];
   __shared__ uint32_t s_tag;
   __shared__ int s_ok;
+#if EARL_AGG_TMA
+  extern __shared__ __align__(128) uint8_t ring_mem[];  // [kWarps][2][kSlotBytes]
+  __shared__ uint64_t ring_bar[kWarps][2];
+#endif
   if (threadIdx.x == 0) {
     rank_table(a, rt, (int64_t)gridDim.x * kWarps);
     s_tag = (*(volatile uint32_t*)&a.ws->epoch + 1u) << 2;  // | 1 aggregate, | 2 inclusive
@@ -371,6 +465,10 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   float2* bmp = bmap[wid];
   float2 (*lmp)[32] = lmap[wid];
   double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
+#if EARL_AGG_TMA
+  BatchRing ring;
+  ring.init(ring_mem + (size_t)wid * 2 * kSlotBytes, ring_bar[wid], lane);
+#endif
 
   // windows are claimed in increasing order and every window only waits on smaller ones (no
   // deadlock); a warp claims its next window only when it starts it, so a window's right
@@ -395,8 +493,13 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     const bool vec = aligned(rw, 16) && aligned(G, 16) && aligned(mk, 16);
     const int64_t lt = w0 + (int64_t)kTokLane * lane;  // this lane's tokens in batch b: lt + 512 b
 
+#if EARL_AGG_TMA
+    Batch cur;
+    ring.issue(rw, mk, w0 + (int64_t)(nb - 1) * kBatch, w1, vec, lane);
+#else
     Batch cur, nxt;  // batch b, and b-1 in flight
     load_batch<false>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
+#endif
     for (int d = 3; d < 3 + EARL_AGG_PF; ++d)
       if (nb >= d) prefetch_batch(rw, mk, w0 + (int64_t)(nb - d) * kBatch, w1, lane);
 
@@ -413,7 +516,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     float wS = 0.f, wP = 1.f;
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
+#if EARL_AGG_TMA
+      if (b > 0) ring.issue(rw, mk, w0 + (int64_t)(b - 1) * kBatch, w1, vec, lane);
+      ring.get<false>(cur, rw, mk, lt + (int64_t)b * kBatch, w1, vec, lane);
+#else
       if (b > 0) load_batch<false>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
+#endif
       if (EARL_AGG_PF > 0 && b >= 1 + EARL_AGG_PF)
         prefetch_batch(rw, mk, w0 + (int64_t)(b - 1 - EARL_AGG_PF) * kBatch, w1, lane);
       const uint32_t e = ends16(b);
@@ -429,7 +537,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
       if (lane == 0) bmp[b] = make_float2(bS, bP);
       wS = bS + bP * wS;
       wP = bP * wP;
+#if !EARL_AGG_TMA
       cur = nxt;
+#endif
     }
 
     // publish the window's map, then look back (32 windows per round trip) for the carry:
@@ -454,10 +564,19 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     // pass 2: returns from the lane maps and batch carries (the window's second read hits L2),
     // float4 stores, statistics
     const bool count_stats = rt.t[ri] == 0;
+#if EARL_AGG_TMA
+    ring.issue(rw, mk, w0 + (int64_t)(nb - 1) * kBatch, w1, vec, lane);
+#else
     load_batch<true>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
+#endif
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
+#if EARL_AGG_TMA
+      if (b > 0) ring.issue(rw, mk, w0 + (int64_t)(b - 1) * kBatch, w1, vec, lane);
+      ring.get<true>(cur, rw, mk, lt + (int64_t)b * kBatch, w1, vec, lane);
+#else
       if (b > 0) load_batch<true>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
+#endif
       const uint32_t e = ends16(b);
       const float2 rm = lmp[b][lane];
       float g_next = rm.x + rm.y * bmp[b].x;
@@ -493,7 +612,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
         for (int i = 0; i < kTokLane; ++i)
           if (t + i < w1) G[t + i] = out[i];
       }
+#if !EARL_AGG_TMA
       cur = nxt;
+#endif
     }
 
     // per-sequence return G_0 of the sequences starting in the window (zero-length sequences
@@ -582,7 +703,18 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
 int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWin + 16384; }
 
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
-  returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, 0, s>>>(a);
+  size_t dyn = 0;
+  if (EARL_AGG_TMA) {
+    dyn = (size_t)kWarps * 2 * kSlotBytes;  // 40 KB of batch slots
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(returns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)dyn);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+  }
+  returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, dyn, s>>>(a);
   return cudaGetLastError();
 }
 
