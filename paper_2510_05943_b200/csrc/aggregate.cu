@@ -16,8 +16,10 @@
 // sequence, else gamma; G_t is the composition of the maps of t..end applied to 0.  The buffer
 // is cut into aligned windows of up to 4096 tokens; a warp claims windows right to left from
 // an atomic counter and streams its window twice in 512-token batches (16 contiguous tokens
-// per lane: 4 float4 + 1 uint4 loads, register double buffer): pass 1 composes the window's map and publishes it, a lane-parallel
-// look-back over the windows to its right stops at the first inclusive value or zero slope (a
+// per lane).  A batch arrives by two TMA bulk copies (rewards, mask) into a per-warp 2-slot
+// shared-memory ring, one batch ahead, and lanes read their 16 tokens in a rotated,
+// bank-conflict-free order (the kernel was L1-bound on lane-strided global loads): pass 1
+// composes the window's map and publishes it, a lane-parallel look-back over the windows to its right stops at the first inclusive value or zero slope (a
 // sequence end), pass 2 re-reads the window from L2 and writes G with float4 stores.  HBM sees
 // every token read and written once; long sequences are spread over many warps (decoupled
 // look-back).
@@ -236,8 +238,12 @@ __device__ __forceinline__ float tok_r(const Batch& B, int i) {
 }
 
 #ifndef EARL_AGG_TMA
-#define EARL_AGG_TMA 0
+#define EARL_AGG_TMA 1  // batches arrive by TMA bulk copies (0: register loads, lane-contiguous)
 #endif
+#ifndef EARL_AGG_SLOTS
+#define EARL_AGG_SLOTS 2
+#endif
+constexpr int kSlots = EARL_AGG_SLOTS;  // batches in a warp's ring (kSlots - 1 loads ahead)
 constexpr int kSlotBytes = kBatch * 4 + kBatch;  // a batch's rewards, then its mask bytes
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -248,15 +254,16 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 // global side).  Slot uses alternate; every use completes one phase of the slot's mbarrier (a
 // batch that is not whole and 16-B aligned arrives without a copy and is read from global).
 struct BatchRing {
-  uint8_t* mem;       // this warp's 2 slots
-  uint64_t* bar;      // this warp's 2 mbarriers
+  uint8_t* mem;       // this warp's kSlots slots
+  uint64_t* bar;      // this warp's kSlots mbarriers
   uint32_t issued, got;
-  bool tma[2];
+  bool tma[kSlots];
 
   __device__ __forceinline__ void init(uint8_t* m, uint64_t* b, int lane) {
-    mem = m; bar = b; issued = got = 0; tma[0] = tma[1] = false;
+    mem = m; bar = b; issued = got = 0;
+    for (int s = 0; s < kSlots; ++s) tma[s] = false;
     if (lane == 0) {
-      for (int s = 0; s < 2; ++s)
+      for (int s = 0; s < kSlots; ++s)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -265,7 +272,7 @@ struct BatchRing {
   // start loading batch [t0, t0 + kBatch) into the next slot (its previous batch is consumed)
   __device__ __forceinline__ void issue(const float* rw, const uint8_t* mk, int64_t t0, int64_t w1,
                                         bool vec, int lane) {
-    const int s = issued & 1;
+    const int s = issued % kSlots;
     const bool whole = vec && t0 + kBatch <= w1;
     tma[s] = whole;
     __syncwarp();
@@ -293,8 +300,8 @@ struct BatchRing {
   template <bool kLastUse>
   __device__ __forceinline__ void get(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
                                       int64_t w1, bool vec, int lane) {
-    const int s = got & 1;
-    const uint32_t parity = (got >> 1) & 1;
+    const int s = got % kSlots;
+    const uint32_t parity = (got / kSlots) & 1;
     const uint32_t b = smem_addr(&bar[s]);
     uint32_t done;
     do {
@@ -442,8 +449,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   __shared__ uint32_t s_tag;
   __shared__ int s_ok;
 #if EARL_AGG_TMA
-  extern __shared__ __align__(128) uint8_t ring_mem[];  // [kWarps][2][kSlotBytes]
-  __shared__ uint64_t ring_bar[kWarps][2];
+  extern __shared__ __align__(128) uint8_t ring_mem[];  // [kWarps][kSlots][kSlotBytes]
+  __shared__ uint64_t ring_bar[kWarps][kSlots];
 #endif
   if (threadIdx.x == 0) {
     rank_table(a, rt, (int64_t)gridDim.x * kWarps);
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
 #if EARL_AGG_TMA
   BatchRing ring;
-  ring.init(ring_mem + (size_t)wid * 2 * kSlotBytes, ring_bar[wid], lane);
+  ring.init(ring_mem + (size_t)wid * kSlots * kSlotBytes, ring_bar[wid], lane);
 #endif
 
   // windows are claimed in increasing order and every window only waits on smaller ones (no
@@ -495,7 +502,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
 
 #if EARL_AGG_TMA
     Batch cur;
-    ring.issue(rw, mk, w0 + (int64_t)(nb - 1) * kBatch, w1, vec, lane);
+    for (int d = 1; d < kSlots && nb - d >= 0; ++d)
+      ring.issue(rw, mk, w0 + (int64_t)(nb - d) * kBatch, w1, vec, lane);
 #else
     Batch cur, nxt;  // batch b, and b-1 in flight
     load_batch<false>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
@@ -517,7 +525,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
 #if EARL_AGG_TMA
-      if (b > 0) ring.issue(rw, mk, w0 + (int64_t)(b - 1) * kBatch, w1, vec, lane);
+      if (b - (kSlots - 1) >= 0)
+        ring.issue(rw, mk, w0 + (int64_t)(b - (kSlots - 1)) * kBatch, w1, vec, lane);
       ring.get<false>(cur, rw, mk, lt + (int64_t)b * kBatch, w1, vec, lane);
 #else
       if (b > 0) load_batch<false>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
@@ -565,14 +574,16 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     // float4 stores, statistics
     const bool count_stats = rt.t[ri] == 0;
 #if EARL_AGG_TMA
-    ring.issue(rw, mk, w0 + (int64_t)(nb - 1) * kBatch, w1, vec, lane);
+    for (int d = 1; d < kSlots && nb - d >= 0; ++d)
+      ring.issue(rw, mk, w0 + (int64_t)(nb - d) * kBatch, w1, vec, lane);
 #else
     load_batch<true>(cur, rw, mk, lt + (int64_t)(nb - 1) * kBatch, w1, vec);
 #endif
 #pragma unroll 1
     for (int b = nb - 1; b >= 0; --b) {
 #if EARL_AGG_TMA
-      if (b > 0) ring.issue(rw, mk, w0 + (int64_t)(b - 1) * kBatch, w1, vec, lane);
+      if (b - (kSlots - 1) >= 0)
+        ring.issue(rw, mk, w0 + (int64_t)(b - (kSlots - 1)) * kBatch, w1, vec, lane);
       ring.get<true>(cur, rw, mk, lt + (int64_t)b * kBatch, w1, vec, lane);
 #else
       if (b > 0) load_batch<true>(nxt, rw, mk, lt + (int64_t)(b - 1) * kBatch, w1, vec);
@@ -705,7 +716,7 @@ int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWi
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
   size_t dyn = 0;
   if (EARL_AGG_TMA) {
-    dyn = (size_t)kWarps * 2 * kSlotBytes;  // 40 KB of batch slots
+    dyn = (size_t)kWarps * kSlots * kSlotBytes;  // kSlots x 20 KB of batch slots
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(returns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
