@@ -232,7 +232,10 @@ EARL_API earl_status_t earl_plan_destroy(earl_plan_t plan);
  * Protocol (multi-process): entry barrier (every peer's stream reached exec, so its recv
  * buffers may be overwritten), stores, system-scope fence, release of an epoch flag into
  * each peer's signal pad, acquire-wait for every peer's flag.  When the stream passes the
- * call, this rank's recv buffers are complete.  A peer missing for > 10 s latches TIMEOUT. */
+ * call, this rank's recv buffers are complete.  A peer missing for > 10 s (or the
+ * EARL_TIMEOUT_MS read at earl_comm_create) latches TIMEOUT with the bit mask of the missing
+ * peers, reported by the next synchronising call (a barrier timeout names the
+ * missing workers). */
 EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* send_bufs,
                                  void* const* recv_bufs, void* stream);
 /* The fused dispatch of ONE source rank's records (data leaves "from their

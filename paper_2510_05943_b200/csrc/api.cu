@@ -167,6 +167,10 @@ extern "C" earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t c
   c->device = cuda_device;
   c->emulated = (rank == EARL_ALL_RANKS);
   c->window_bytes = ((window_bytes + 255) & ~255ull) + kPadBytes;
+  if (const char* t = getenv("EARL_TIMEOUT_MS")) {  // peer waits (SPEC.md:316 barrier timeout)
+    const long long ms = atoll(t);
+    if (ms > 0) c->timeout_ns = (uint64_t)ms * 1000000ull;
+  }
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
   // keep freed plan memory cached in the pool: steady-state planning never calls the driver
   cudaMemPool_t pool;

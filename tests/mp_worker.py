@@ -200,3 +200,46 @@ def gpu_roles_main(rank, world, port, q, case):
         q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_timeout_main(rank, world, port, q, case):
+    """Failure detection: every rank but the last calls the fused exec; the last
+    never does.  The others' entry barrier times out (EARL_TIMEOUT_MS) and the plan reports
+    EARL_ERR_TIMEOUT naming the missing peer."""
+    try:
+        import os
+        os.environ["EARL_TIMEOUT_MS"] = "300"
+        import numpy as np
+        import torch
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        import torch.distributed as dist
+        lens = case
+        fields = W.field_set("tiny3")
+        src = W.rollout_layout(len(lens), world)
+        dst = W.layout(dp=1, tp=world, assign="contig")
+        D = Dispatcher(window_bytes=sum(lens) * W.bytes_per_token(fields) + (1 << 16), device=0)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        plan = D.plan(src, dst, glens, fields)
+        ptrs, views = D.alloc_recv(plan, fields)
+        tok = W.rollout_token_counts(np.asarray(lens), src["counts"])[rank]
+        mine = [torch.zeros(max(16, tok * b), dtype=torch.uint8, device="cuda") for b in (4, 4, 4)]
+        missing = world - 1
+        msg = "ok"
+        if rank != missing:
+            plan.exec(mine, ptrs)
+            try:
+                plan.sync()
+                msg = f"rank {rank}: no timeout reported"
+            except EarlError as e:
+                want = f"mask 0x{1 << missing:x}"
+                if "TIMEOUT" not in str(e) or want not in str(e):
+                    msg = f"rank {rank}: unexpected error {e}"
+        dist.barrier()  # the missing rank keeps its window mapped until the others are done
+        dist.destroy_process_group()
+        q.put((rank, msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

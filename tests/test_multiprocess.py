@@ -116,3 +116,14 @@ def test_role_plans_processes(world, flag):
     src = W.rollout_layout(len(lens), world)
     dst = W.layout(dp=max(1, world // 2), tp=2 if world >= 2 else 1, assign="lpt")
     run_procs(mp_worker.gpu_roles_main, world, extra=((lens, src, dst, flag, world - 1),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_missing_peer_times_out(world):
+    """A rank that never joins the exchange: the others report EARL_ERR_TIMEOUT with its bit."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    run_procs(mp_worker.gpu_timeout_main, world, extra=(W.TINY_LENGTHS.tolist(),), timeout=300)
