@@ -140,6 +140,18 @@ def c4_lengths(seed: int = 0) -> np.ndarray:
 # include/earl_dispatch.h and implemented separately by each side)
 # ---------------------------------------------------------------------------
 
+# The paper's dispatch experiment (Fig. 4): log-prob tensors of the reference
+# model's workers, "46 MiB, 93 MiB, and 187 MiB per independent worker" at context
+# 8K / 16K / 32K.  Reading: each worker holds FIG4_RESPONSES responses padded to the
+# context length, one fp32 log-prob per token (1500 x L x 4 B = 46.875 / 93.75 / 187.5 MiB).
+FIG4_RESPONSES = 1500
+FIG4_CONTEXTS = (8192, 16384, 32768)
+
+
+def fig4_lengths(context: int, workers: int = 8) -> np.ndarray:
+    return np.full(workers * FIG4_RESPONSES, int(context), dtype=np.int64)
+
+
 def layout(rank0=0, dp=1, sp=1, tp=1, assign="contig", counts=None, group_of_seq=None,
            sp_split="block", sp_min_len=0):
     return {

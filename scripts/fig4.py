@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 from paper_2510_05943_b200 import workloads as W  # noqa: E402
 from paper_2510_05943_b200.dispatch import EmulatedDispatch  # noqa: E402
 
-R, PER_WORKER, NVL = 8, 1500, 770e9
+R, NVL = 8, 770e9
 dev = torch.device("cuda", 0)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 fields = [("old_logprobs", 4, 1, "logprob")]
@@ -43,9 +43,9 @@ def timed(fn, reps=10):
 
 
 ed = EmulatedDispatch(R)
-for L in (8192, 16384, 32768):
-    n = R * PER_WORKER
-    lens = np.full(n, L, dtype=np.int64)
+for L in W.FIG4_CONTEXTS:
+    lens = W.fig4_lengths(L, R)
+    n = len(lens)
     src = W.rollout_layout(n, R)
     dst = W.layout(dp=2, tp=4, assign="contig")
     mid = W.layout(dp=1, assign="given_counts", counts=[n])

@@ -410,3 +410,25 @@ def test_distinct_src_replicas_feed_td_mod_tps():
         for td in range(tpd):
             for f in range(len(fields)):
                 assert np.array_equal(out[td][f], src_arrays[td % tps][f])
+
+
+def test_fig4_workload_matches_the_papers_payloads():
+    """tests/golden/paper_numbers.json: the Fig. 4 replay's per-worker log-prob
+    payload is the paper's 46 / 93 / 187 MiB (printed rounded down) at 8K / 16K / 32K."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_numbers.json")))["fig4"]
+    for L, mib in zip(g["contexts"], g["per_worker_MiB"]):
+        lens = W.fig4_lengths(L, 8)
+        counts = W.near_equal_counts(len(lens), 8)
+        per_worker = W.rollout_token_counts(lens, counts)
+        assert len(set(per_worker)) == 1
+        assert int(per_worker[0] * 4 / (1 << 20)) == mib
+
+
+def test_table1_is_linear_in_context():
+    """Table 1: the estimated batch grows linearly with the context length,
+    15,625 MiB per 1K tokens on a 1K-GPU cluster (kappa of SPEC.md:59)."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_numbers.json")))["table1"]
+    for L, mib in zip(g["contexts"], g["MiB"]):
+        assert mib * 1024 == 15625 * L
