@@ -714,18 +714,22 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
 int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWin + 16384; }
 
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
-  size_t dyn = 0;
-  if (EARL_AGG_TMA) {
-    dyn = (size_t)kWarps * kSlots * kSlotBytes;  // kSlots x 20 KB of batch slots
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(returns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)dyn);
+  // the batch ring: kSlots x 2.5 KB per warp of dynamic shared memory; with the static arrays
+  // it exceeds the 48 KB a launch gets without opting in (once per device)
+  constexpr size_t kRingBytes = EARL_AGG_TMA ? (size_t)kWarps * kSlots * kSlotBytes : 0;
+  if (kRingBytes > 0) {
+    static bool opted[64] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64 || !opted[dev]) {
+      e = cudaFuncSetAttribute(returns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kRingBytes);
       if (e != cudaSuccess) return e;
-      attr = true;
+      if (dev >= 0 && dev < 64) opted[dev] = true;
     }
   }
-  returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, dyn, s>>>(a);
+  returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
   return cudaGetLastError();
 }
 
