@@ -715,19 +715,12 @@ int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWi
 
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
   // the batch ring: kSlots x 2.5 KB per warp of dynamic shared memory; with the static arrays
-  // it exceeds the 48 KB a launch gets without opting in (once per device)
+  // it exceeds the 48 KB a launch gets without opting in
   constexpr size_t kRingBytes = EARL_AGG_TMA ? (size_t)kWarps * kSlots * kSlotBytes : 0;
   if (kRingBytes > 0) {
     static bool opted[64] = {};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
+    cudaError_t e = opt_in_dynamic_smem(returns_kernel, (int)kRingBytes, opted);
     if (e != cudaSuccess) return e;
-    if (dev < 0 || dev >= 64 || !opted[dev]) {
-      e = cudaFuncSetAttribute(returns_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kRingBytes);
-      if (e != cudaSuccess) return e;
-      if (dev >= 0 && dev < 64) opted[dev] = true;
-    }
   }
   returns_kernel<<<sm_count * kCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
   return cudaGetLastError();

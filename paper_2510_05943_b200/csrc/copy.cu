@@ -638,13 +638,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
 template <int WARPS, int STAGES, int CHUNK>
 cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
   constexpr size_t smem = copy_smem_bytes<WARPS, STAGES, CHUNK>();
-  static bool configured = false;
+  static bool configured[64] = {};
   auto kern = copy_kernel<WARPS, STAGES, CHUNK>;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = opt_in_dynamic_smem(kern, (int)smem, configured);
+  if (e != cudaSuccess) return e;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
   if (per_sm < 1) per_sm = 1;

@@ -174,6 +174,20 @@ struct AggArgs {
   const double* stats;               // [3] the same over the whole batch (after the all-reduce)
 };
 
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device.  The attribute is
+// per device, so a process driving several GPUs opts in once on each (done[] per device id).
+template <class F>
+inline cudaError_t opt_in_dynamic_smem(F* func, int bytes, bool (&done)[64]) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const bool tracked = dev >= 0 && dev < 64;
+  if (tracked && done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && tracked) done[dev] = true;
+  return e;
+}
+
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
 int64_t returns_windows(int64_t tokens);

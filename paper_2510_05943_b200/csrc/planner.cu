@@ -795,8 +795,9 @@ __global__ void local_meta_kernel(const __grid_constant__ PlanArgs a, int g, int
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem) {
   static int per_sm = -1;
   static int forced = -2;
+  static bool opted[64] = {};
+  opt_in_dynamic_smem(planner_kernel, 64 * 1024, opted);
   if (per_sm < 0) {
-    cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, planner_kernel, NT, 64 * 1024) !=
         cudaSuccess)
       per_sm = 1;
@@ -816,13 +817,9 @@ int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_sm
 }
 
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(planner_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         64 * 1024);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static bool configured[64] = {};
+  cudaError_t e = opt_in_dynamic_smem(planner_kernel, 64 * 1024, configured);
+  if (e != cudaSuccess) return e;
   if (grid == 1) {
     planner_kernel<<<1, NT, lpt_smem, s>>>(a);
     return cudaGetLastError();
