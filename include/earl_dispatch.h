@@ -207,6 +207,11 @@ EARL_API earl_status_t earl_plan_groups(earl_plan_t plan, int32_t* src_groups, i
                                         void* stream);
 /* Byte accounting of SPEC.md:239-247 (host; synchronises). */
 EARL_API earl_status_t earl_plan_stats(earl_plan_t plan, earl_plan_stats_t* stats);
+/* Debug check of replicated planning (every rank computes a byte-identical plan
+ * with no metadata exchange): a 64-bit FNV-1a hash of the plan's tables and its record arrays
+ * (host; synchronises; copies the records to the host, so O(records) time).  Equal inputs give
+ * equal hashes on every rank; the binding all-gathers them and reports EARL_ERR_MISMATCH. */
+EARL_API earl_status_t earl_plan_hash(earl_plan_t plan, uint64_t* hash);
 /* Debug: the canonical, uncoalesced segment table in (s, d, i, x) order (reading c19),
  * one record per (sequence i, token overlap [x,y), destination replica): source rank s,
  * destination rank d, source local token offset, destination local token offset.

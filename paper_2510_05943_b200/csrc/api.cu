@@ -615,6 +615,49 @@ extern "C" earl_status_t earl_plan_mean_length(earl_plan_t p, double* avg) {
   return EARL_OK;
 }
 
+namespace {
+// FNV-1a, 64-bit
+inline uint64_t fnv1a(uint64_t h, const void* data, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(data);
+  for (size_t k = 0; k < n; ++k) { h ^= b[k]; h *= 0x100000001b3ull; }
+  return h;
+}
+
+template <class T>
+earl_status_t hash_device(uint64_t& h, const T* dev, int64_t n) {
+  if (n <= 0) return EARL_OK;
+  std::vector<T> buf((size_t)n);
+  CUDA_TRY(cudaMemcpy(buf.data(), dev, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost));
+  h = fnv1a(h, buf.data(), sizeof(T) * (size_t)n);
+  return EARL_OK;
+}
+}  // namespace
+
+extern "C" earl_status_t earl_plan_hash(earl_plan_t p, uint64_t* out) {
+  if (!p || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  DeviceGuard g(p->comm->device);
+  const PlanHeader& h = p->host_hdr;
+  uint64_t x = 0xcbf29ce484222325ull;
+  // every planned table of the header (not the error latch or the copy kernels' counters)
+  const char* lo = reinterpret_cast<const char*>(&h.T);
+  const char* hi = reinterpret_cast<const char*>(&h.work_ctr);
+  x = fnv1a(x, lo, (size_t)(hi - lo));
+  const Records& r = p->args.rec;
+  const int64_t n = h.n_records;
+  if ((st = hash_device(x, r.seq, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.x, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.n, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.code, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.src_tok, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.dst_tok, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.msg_tok, n)) != EARL_OK) return st;
+  if ((st = hash_device(x, r.tok_prefix, n + 1)) != EARL_OK) return st;
+  *out = x;
+  return EARL_OK;
+}
+
 extern "C" earl_status_t earl_plan_stats(earl_plan_t p, earl_plan_stats_t* out) {
   if (!p || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   earl_status_t st = plan_check(p);

@@ -12,6 +12,8 @@ tensors and passes pointers.
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -148,7 +150,22 @@ class Dispatcher:
     def plan(self, src, dst, seq_lens: torch.Tensor, fields, stream=None):
         self._src = layout_for_device(src, self.device)
         self._dst = layout_for_device(dst, self.device)
-        return self.comm.plan(self._src, self._dst, seq_lens, fields, stream)
+        plan = self.comm.plan(self._src, self._dst, seq_lens, fields, stream)
+        if os.environ.get("EARL_CHECK_PLAN") == "1":
+            self.check_plan(plan)
+        return plan
+
+    def check_plan(self, plan):
+        """Debug check of replicated planning: every rank's plan hash, all-gathered
+        over the process group, must be equal; otherwise EARL_ERR_MISMATCH naming the ranks."""
+        mine = plan.hash()
+        hashes = [None] * self.world
+        self.dist.all_gather_object(hashes, mine, group=self.group)
+        if len(set(hashes)) != 1:
+            bad = [r for r, h in enumerate(hashes) if h != hashes[0]]
+            raise earl.EarlError(7, f"plan hash differs across ranks: rank 0 {hashes[0]:#x}, "
+                                    f"ranks {bad} differ")
+        return mine
 
     def alloc_recv(self, plan, fields, reset=True):
         """Receive tensors inside the symmetric window: same offsets on every rank, sized for

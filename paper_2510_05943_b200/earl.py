@@ -35,6 +35,7 @@ EXPORTED = [
     "earl_comm_create", "earl_comm_export_handle", "earl_comm_import_peers", "earl_comm_alloc",
     "earl_comm_reset_alloc", "earl_comm_info", "earl_comm_destroy", "earl_dispatch_plan",
     "earl_plan_replan", "earl_plan_sync", "earl_plan_local_sizes", "earl_plan_local_meta", "earl_plan_stats",
+    "earl_plan_hash",
     "earl_plan_export", "earl_plan_groups", "earl_plan_destroy", "earl_dispatch_exec", "earl_dispatch_exec_src",
     "earl_dispatch_pack", "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
     "earl_abi_version", "earl_kernel_launch_count", "earl_speedup_pct", "earl_policy_build",
@@ -123,6 +124,7 @@ def lib():
         "earl_plan_local_sizes": [vp, i32, C.POINTER(i64), C.POINTER(i64)],
         "earl_plan_local_meta": [vp, i32, vp, vp, vp, vp],
         "earl_plan_stats": [vp, C.POINTER(PlanStats)],
+        "earl_plan_hash": [vp, C.POINTER(C.c_uint64)],
         "earl_plan_export": [vp, i64, C.POINTER(i64), vp, vp, vp, vp, vp, vp, vp],
         "earl_plan_destroy": [vp],
         "earl_plan_groups": [vp, vp, vp, vp],
@@ -308,6 +310,12 @@ class Plan:
         v = C.c_double()
         check(lib().earl_plan_mean_length(self.h, C.byref(v)))
         return v.value
+
+    def hash(self) -> int:
+        """earl_plan_hash: 64-bit hash of the plan's tables and records (debug; synchronises)."""
+        h = C.c_uint64()
+        check(lib().earl_plan_hash(self.h, C.byref(h)))
+        return h.value
 
     def stats(self) -> dict:
         st = PlanStats()

@@ -243,3 +243,43 @@ def gpu_timeout_main(rank, world, port, q, case):
         q.put((rank, msg))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_hash_main(rank, world, port, q, case):
+    """Replicated planning across processes: equal plans pass Dispatcher.check_plan; when one
+    rank plans from different lengths, every rank gets EARL_ERR_MISMATCH."""
+    try:
+        import numpy as np
+        import torch
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        import torch.distributed as dist
+        lens = list(case)
+        fields = W.field_set("tiny3")
+        src, dst = W.config_layouts("c3", world, len(lens))
+        D = Dispatcher(window_bytes=1 << 20, device=0)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        plan = D.plan(src, dst, glens, fields)
+        D.check_plan(plan)
+        bad = list(lens)
+        if rank == world - 1:
+            bad[0] += 3
+        plan2 = D.plan(src, dst, torch.as_tensor(np.asarray(bad, dtype=np.int32)).cuda(), fields)
+        msg = f"rank {rank}: mismatch not detected"
+        try:
+            D.check_plan(plan2)
+        except EarlError as e:
+            if "MISMATCH" in str(e) or "differs" in str(e):
+                msg = "ok"
+            else:
+                msg = f"rank {rank}: {e}"
+        plan.destroy()
+        plan2.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

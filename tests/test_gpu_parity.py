@@ -87,6 +87,32 @@ def test_exec_per_source_rank(seed):
                  host_src=seed % 2 == 1)
 
 
+def test_plan_hash_is_a_function_of_the_inputs():
+    """earl_plan_hash (the replicated-planning check): equal inputs, equal hashes -- also after a
+    replan to other lengths and back; other lengths or layouts, other hashes."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    lens = W.c2_lengths(0)[:200].tolist()
+    src, dst = W.config_layouts("c3", 8, len(lens))
+    ed = EmulatedDispatch(8)
+    f = W.field_set("scalar6-fp32")
+    a, b = ed.plan(src, dst, lens, f), ed.plan(src, dst, lens, f)
+    h = a.hash()
+    assert h == b.hash()
+    other = list(lens)
+    other[7] += 1
+    c = ed.plan(src, dst, other, f)
+    assert c.hash() != h
+    d = ed.plan(src, W.layout(dp=4, tp=2, assign="contig"), lens, f)
+    assert d.hash() != h
+    a.replan(torch.as_tensor(np.asarray(other, dtype=np.int32)).cuda())
+    assert a.hash() == c.hash()
+    a.replan(torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda())
+    assert a.hash() == h
+    for p in (a, b, c, d):
+        p.destroy()
+
+
 def test_exec_src_rank_out_of_range():
     from paper_2510_05943_b200.dispatch import EmulatedDispatch
     from paper_2510_05943_b200.earl import EarlError

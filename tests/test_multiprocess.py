@@ -127,3 +127,15 @@ def test_missing_peer_times_out(world):
     from paper_2510_05943_b200 import build
     build.build()
     run_procs(mp_worker.gpu_timeout_main, world, extra=(W.TINY_LENGTHS.tolist(),), timeout=300)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_plan_hash_mismatch_detected(world):
+    """Every rank plans the same batch: Dispatcher.check_plan passes; one rank with other lengths:
+    every rank raises EARL_ERR_MISMATCH (SURVEY.md §7 replicated deterministic planning)."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    run_procs(mp_worker.gpu_hash_main, world, extra=(W.c2_lengths(0)[:48].tolist(),), timeout=300)
