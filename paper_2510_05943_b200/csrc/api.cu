@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "earl_internal.cuh"
 
 using namespace earl;
@@ -19,6 +21,14 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
+
+// NVTX range around a C-ABI call that enqueues device work (SURVEY.md §5 tracing): tools (nsys,
+// ncu --nvtx --nvtx-include "earl_dispatch_exec/") attribute the kernels to the call; without a
+// tool attached the header-only NVTX3 calls are a null-pointer check.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 earl_status_t fail(earl_status_t st, const char* fmt, ...) {
   char buf[512];
@@ -416,6 +426,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
                                             const earl_layout_t* dst, const int32_t* seq_lens,
                                             int64_t n_seqs, const earl_field_t* fields,
                                             int32_t n_fields, void* stream, earl_plan_t* out) {
+  NvtxRange nvtx("earl_dispatch_plan");
   if (!c || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm or plan out-pointer");
   *out = nullptr;
   if (n_seqs < 0 || n_seqs > 0x7fffffffLL)
@@ -549,6 +560,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
 }
 
 extern "C" earl_status_t earl_plan_replan(earl_plan_t p, const int32_t* seq_lens, void* stream) {
+  NvtxRange nvtx("earl_plan_replan");
   if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
   if (p->N > 0 && !seq_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens is NULL");
   DeviceGuard g(p->comm->device);
@@ -956,12 +968,14 @@ earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
 
 extern "C" earl_status_t earl_dispatch_exec(earl_plan_t p, const void* const* send_bufs,
                                             void* const* recv_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_exec");
   return exec_impl(p, -1, send_bufs, recv_bufs, stream);
 }
 
 extern "C" earl_status_t earl_dispatch_exec_src(earl_plan_t p, int32_t src_rank,
                                                 const void* const* send_bufs,
                                                 void* const* recv_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_exec_src");
   if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
   earl_comm* c = p->comm;
   if (src_rank < 0 || src_rank >= c->world)
@@ -977,6 +991,7 @@ extern "C" earl_status_t earl_dispatch_exec_src(earl_plan_t p, int32_t src_rank,
 
 extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* send_bufs,
                                             void* const* stage_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_pack");
   if (!p || !stage_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   earl_comm* c = p->comm;
   DeviceGuard g(c->device);
@@ -999,6 +1014,7 @@ extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* se
 
 extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* stage_bufs,
                                               void* const* recv_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_unpack");
   if (!p || !stage_bufs || !recv_bufs) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   earl_comm* c = p->comm;
   DeviceGuard g(c->device);
@@ -1145,6 +1161,7 @@ earl_status_t set_per_rank(earl_plan_t p, T** dst, const void* const* src, const
 extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* const* rewards,
                                       const void* const* mask, void* const* returns,
                                       void* const* seq_return, double* partial, void* stream) {
+  NvtxRange nvtx("earl_returns");
   if (!p || !partial) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   AggArgs a;
   earl_status_t st = agg_args(p, a);
@@ -1173,6 +1190,7 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
 extern "C" earl_status_t earl_advantages(earl_plan_t p, const double* stats, float eps,
                                          const void* const* returns, const void* const* mask,
                                          void* const* adv, void* stream) {
+  NvtxRange nvtx("earl_advantages");
   if (!p || !stats) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
   AggArgs a;
   earl_status_t st = agg_args(p, a);
