@@ -554,10 +554,12 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
     // publish the window's map, then look back (32 windows per round trip) for the carry:
     // compose the maps of windows w+1, w+2, ... up to the first inclusive value or zero slope
     AggWindow* W = a.win + rt.wbeg[ri];
+    delay_inject(4 + (uint32_t)w);
     if (lane == 0 && w + 1 < nwin) {
       st_word(&W[w].S, tag | 1u, wS);
       st_word(&W[w].P, tag | 1u, wP);
     }
+    delay_inject(5 + (uint32_t)w);
     const float carry = look_back(W, w, nwin, tag, lane);  // past the buffer end: G = 0
     if (lane == 0) {
       st_word(&W[w].inc, tag | 2u, wS + wP * carry);

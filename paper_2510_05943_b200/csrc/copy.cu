@@ -82,6 +82,7 @@ __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world,
     my_pad[kEpochSlot] = epoch;
   }
   epoch = __shfl_sync(kFull, epoch, 0);
+  delay_inject(1);
   const unsigned miss = signal_and_wait(my_pad, pads.p, world, me, kReadySlot, epoch, timeout_ns);
   if (threadIdx.x == 0 && miss) {
     if (atomicCAS(err, 0, EARL_ERR_TIMEOUT) == 0) *err_detail = (int32_t)miss;
@@ -550,6 +551,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     fence_mbar_init();
   }
   __syncwarp();
+  delay_inject(2);
   const PlanHeader* h = a.hdr;
   if (h->err == 0) {
     const uint64_t c0 = CHUNK / 4;
@@ -614,6 +616,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
   }
   // completion (multi-process comm): last CTA releases this epoch to every peer and waits
   if (a.protocol) {
+    delay_inject(3);
     asm volatile("fence.proxy.async.global;" ::: "memory");
     __threadfence_system();
     __syncthreads();

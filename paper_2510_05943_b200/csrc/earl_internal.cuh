@@ -174,6 +174,22 @@ struct AggArgs {
   const double* stats;               // [3] the same over the whole batch (after the all-reduce)
 };
 
+// Delay injection (SURVEY.md §5 race detection; build with EARL_NVCC_DEFINES=EARL_DELAY_INJECT=1):
+// a pseudo-random spin of up to ~20 us per (CTA, warp, site) at the points where flag ordering
+// or look-back correctness depends on timing, so tests shake out missing fences and waits.
+#ifndef EARL_DELAY_INJECT
+#define EARL_DELAY_INJECT 0
+#endif
+__device__ __forceinline__ void delay_inject(uint32_t site) {
+  if (EARL_DELAY_INJECT) {
+    uint32_t x = blockIdx.x * 2654435761u ^ (threadIdx.x >> 5) * 40503u ^ site * 2246822519u;
+    x ^= x >> 15; x *= 0x2c1b3c6du; x ^= x >> 12; x *= 0x297a2d39u; x ^= x >> 15;
+    const long long cycles = (long long)(x % 40000u);  // up to ~20 us at 1.9 GHz
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles) {}
+  }
+}
+
 // Opt a kernel in to `bytes` of dynamic shared memory on the current device.  The attribute is
 // per device, so a process driving several GPUs opts in once on each (done[] per device id).
 template <class F>

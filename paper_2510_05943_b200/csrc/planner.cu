@@ -48,6 +48,7 @@ __device__ __forceinline__ void stamp(const PlanArgs& a, int k) {
 }
 
 __device__ __forceinline__ void gsync() {
+  delay_inject(6);
   if (gridDim.x == 1) __syncthreads();
   else cg::this_grid().sync();
 }
