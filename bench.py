@@ -601,6 +601,12 @@ def run_multi(args):
                               "moved": st["moved"], "records": st["records"]}}
         if e2e:
             out["e2e"] = e2e
+        try:
+            nccl_ver = ".".join(str(x) for x in torch.cuda.nccl.version())
+        except Exception:
+            nccl_ver = None
+        out["comm"] = {"backend": dist.get_backend(), "nccl": nccl_ver,
+                       "env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("NCCL_")}}
         if clocks:
             clocks.mark(t0, t1)
             out["clocks"] = clocks.stop()
