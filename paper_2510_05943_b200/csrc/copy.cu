@@ -657,8 +657,9 @@ cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
 // Copy-engine shape (warps per CTA, ring stages, chunk bytes), chosen per launch from the field
 // widths (measured): when nearly all bytes sit in fields whose width is a
 // multiple of 16 B (hidden vectors: source and destination always congruent, bytes leave by TMA
-// bulk stores) 4 warps x 4 stages write fewer concurrent streams and win on TP-replicated
-// stores (0.934 vs 0.915 of peak on c3); otherwise the realign path needs the issue slots of 8
+// bulk stores) few warps with large stages win on TP-replicated stores: 2 warps x 2 stages x
+// 16 KB (3 CTAs per SM) 0.933-0.940 of peak on c3 against 0.920 for 4 warps x 4 x 8 KB (1 CTA)
+// on the same box, c4 1.00, c2-lpt 0.99; otherwise the realign path needs the issue slots of 8
 // warps (0.93 vs 0.63 on the long-tail scalar sweep).  EARL_COPY_CFG forces a shape for tuning.
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s) {
   static int forced = -2;
@@ -666,7 +667,7 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cu
     const char* e = getenv("EARL_COPY_CFG");
     forced = e ? atoi(e) : -1;
   }
-  const int cfg = forced >= 0 ? forced : (congruent_heavy ? 2 : 3);
+  const int cfg = forced >= 0 ? forced : (congruent_heavy ? 14 : 3);
   switch (cfg) {
     case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
     case 2: return launch_cfg<4, 4, 8192>(a, sm_count, s);
@@ -675,6 +676,8 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cu
     case 6: return launch_cfg<8, 4, 6144>(a, sm_count, s);
     case 7: return launch_cfg<4, 3, 16384>(a, sm_count, s);
     case 8: return launch_cfg<2, 6, 16384>(a, sm_count, s);
+    case 11: return launch_cfg<2, 4, 8192>(a, sm_count, s);
+    case 14: return launch_cfg<2, 2, 16384>(a, sm_count, s);
     default: return launch_cfg<8, 3, 8192>(a, sm_count, s);
   }
 }
