@@ -30,6 +30,13 @@ run_gpu_case(W.rollout_layout(9000, 4), W.layout(dp=2, tp=2, assign="contig"), l
 run_gpu_case(W.rollout_layout(9000, 4), W.layout(dp=4, assign="explicit", group_of_seq=[i % 4 for i in range(9000)]),
              lensN, fields, 4, mode="stage")
 run_gpu_case(W.rollout_layout(8, 2), W.layout(dp=1, tp=2, assign="contig"), lens8, fields, 2, host_src=True)
+# the congruent-heavy copy-engine shape (>= 90% of the bytes in 16-B-multiple fields: 2 warps x
+# 2 stages x 16 KB, TMA bulk stores to every TP replica)
+hid = [("h", 2, 64, "x"), ("a", 4, 1, "x")]
+run_gpu_case(W.rollout_layout(60, 4), W.layout(dp=1, tp=4, assign="contig"),
+             [rng.randint(0, 300) for _ in range(60)], hid, 4)
+run_gpu_case(W.rollout_layout(60, 4), W.layout(dp=2, sp=2, assign="contig"),
+             [rng.randint(0, 300) for _ in range(60)], hid, 4, mode="stage")
 # NEXT-2: per-sequence fields, returns (look-back across windows, zero-length sequences,
 # unaligned scalar path) and advantages, each against the oracle
 from tests.test_gpu_parity import _adv_case  # noqa: E402
