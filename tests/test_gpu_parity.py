@@ -275,6 +275,49 @@ def test_device_latched_errors():
     assert e.value.name == "EARL_ERR_LAYOUT"
 
 
+EDGE = 2**31 - 1
+CAPACITY_CASES = [
+    (dict(dp=1, assign="contig"), [2**30, 2**30 - 1]),           # exactly INT32_MAX: fits
+    (dict(dp=1, assign="contig"), [2**30, 2**30]),               # one token over
+    (dict(dp=1, assign="contig"), [2**20] * 2049),               # 2^31 + 2^20
+    (dict(dp=1, sp=2, assign="contig"), [EDGE, EDGE - 2]),       # SP rank 0 at the edge
+    (dict(dp=1, sp=2, assign="contig"), [EDGE, EDGE]),           # SP rank 0 over
+    (dict(dp=2, assign="explicit", group_of_seq=[0, 0, 1]), [2**30, 2**30, 5]),  # partitioned path
+    (dict(dp=2, assign="explicit", group_of_seq=[0, 1, 1]), [2**30, 2**30, 5]),
+    (dict(dp=2, tp=2, assign="contig"), [2**30, 2**30]),         # two groups of 2^30: fit
+]
+
+
+@pytest.mark.parametrize("k", range(len(CAPACITY_CASES)))
+def test_planner_capacity_latch_matches_oracle(k):
+    """Reading c12 (int32 cu_seqlens): the planner's device latch fires exactly when the oracle's
+    check_capacity does -- lengths only, no payload (a plan of > 2^31 tokens moves nothing)."""
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    dst_d, lens = CAPACITY_CASES[k]
+    dst = W.layout(**dst_d)
+    src = W.rollout_layout(len(lens), 2)
+    try:
+        O.check_capacity(dst, lens, O.assign_groups(dst, lens))
+        want_err = False
+    except O.OracleError as e:
+        assert e.code == O.ERR_CAPACITY
+        want_err = True
+    ed = EmulatedDispatch(4)
+    plan = ed.plan(src, dst, lens, W.field_set("tiny3"))
+    if want_err:
+        with pytest.raises(EarlError) as e:
+            plan.sync()
+        assert e.value.name == "EARL_ERR_CAPACITY"
+        assert "INT32_MAX" in str(e.value)
+    else:
+        plan.sync()
+        hd = O.holdings(dst, lens, O.assign_groups(dst, lens))
+        for r, h in hd.items():
+            assert plan.local_sizes(r)[1] == h["n_tokens"]
+    plan.destroy()
+
+
 @pytest.mark.parametrize("bad,name", [
     (dict(dp=3), "EARL_ERR_LAYOUT"),
     (dict(dp=2, assign="given_counts", counts=[1, 1]), "EARL_ERR_LAYOUT"),

@@ -104,6 +104,8 @@ def test_golden_c1(case):
         assert sum(st["self"]) == c["self_bytes"]
     if "total_bytes" in c:
         assert st["total"] == c["total_bytes"]
+    if "runs" in c:  # hand-counted coalesced runs (reading c19)
+        assert st["runs"] == c["runs"], (case, st["runs"])
 
 
 def test_block_split_spot_values():
@@ -386,6 +388,59 @@ def test_other_errors():
     with pytest.raises(O.OracleError) as e:
         O.route(W.layout(dp=1), W.layout(dp=1), [1], 9)
     assert e.value.code == O.ERR_UNSUPPORTED
+
+
+def test_capacity_boundary_int32_cu_seqlens():
+    """Reading c12: cu_seqlens is int32, so a destination shard may hold at most INT32_MAX =
+    2^31 - 1 tokens (a number fixed by the int32 type, not by the oracle).  Exactly at the
+    boundary passes; one token more raises CAPACITY.  Lengths only: holdings are counts."""
+    edge = 2**31 - 1
+    dp1 = W.layout(dp=1, assign="contig")
+    O.check_capacity(dp1, [2**30, 2**30 - 1], [0, 0])          # 2^31 - 1 tokens: fits
+    with pytest.raises(O.OracleError) as e:
+        O.check_capacity(dp1, [2**30, 2**30], [0, 0])          # 2^31: one too many
+    assert e.value.code == O.ERR_CAPACITY
+    with pytest.raises(O.OracleError) as e:
+        O.check_capacity(dp1, [2**20] * 2049, [0] * 2049)      # 2049 x 2^20 = 2^31 + 2^20
+    assert e.value.code == O.ERR_CAPACITY
+    # SP2 splits every sequence, the earlier chunk taking the odd token (reading c7):
+    # SP rank 0 holds 2^30 of 2^31 - 1 plus 2^30 - 1 of 2^31 - 3 = 2^31 - 1 tokens
+    sp2 = W.layout(dp=1, sp=2, assign="contig")
+    O.check_capacity(sp2, [edge, edge - 2], [0, 0])
+    with pytest.raises(O.OracleError):
+        O.check_capacity(sp2, [edge, edge], [0, 0])           # SP rank 0: 2^30 + 2^30
+    # DP2: the same 2^31 tokens split over two groups fit
+    dp2 = W.layout(dp=2, assign="contig")
+    lens = [2**30, 2**30]
+    O.check_capacity(dp2, lens, O.assign_groups(dp2, lens))
+    # TP replicas each hold the whole group: replication does not change the per-rank count
+    tp4 = W.layout(dp=1, tp=4, assign="contig")
+    O.check_capacity(tp4, [edge], [0])
+    with pytest.raises(O.OracleError):
+        O.check_capacity(tp4, [edge, 1], [0, 0])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_contig_without_sp_is_one_run_per_pair(seed):
+    """Reading c19 + SPEC.md:262: under monotone layouts without SP (rollout GIVEN_COUNTS ->
+    CONTIG, TP replicas allowed) every (s, d) pair's segments are one contiguous run on both sides,
+    so the coalesced run count equals the number of (s, d) pairs with bytes, and it never exceeds
+    SPEC's coalescing bound |src ranges| + |dst ranges| per replica pair."""
+    rng = random.Random(seed)
+    world = rng.randint(1, 8)
+    n = rng.randint(1, 40)
+    lens = [rng.randint(0, 50) for _ in range(n)]
+    sdp = rng.randint(1, world)
+    stp = rng.randint(1, world // sdp)
+    ddp = rng.randint(1, world)
+    dtp = rng.randint(1, world // ddp)
+    src = W.layout(dp=sdp, tp=stp, assign="given_counts", counts=O.count_blocks(n, sdp))
+    dst = W.layout(dp=ddp, tp=dtp, assign="contig")
+    segs = O.route(src, dst, lens, world)
+    st = O.stats(segs, [("a", 4, 1, "x")], world)
+    pairs = {(s, d) for (s, d, _, x, y, _, _) in segs}
+    assert st["runs"] == len(pairs)
+    assert st["runs"] <= (sdp + ddp) * dtp
 
 
 def test_golden_tp_replica_rule():
