@@ -34,6 +34,7 @@ if ROOT not in sys.path:
 
 METRIC = "dispatch GB/s per GPU & ms/batch at 1/2/4/8 B200; % of NVLink/HBM roofline"
 NVLINK_PEER_GBPS = 770.0   # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+NVLINK_NOMINAL_GBPS = 900.0
 
 
 def parse():
@@ -469,6 +470,10 @@ def run_multi(args):
     shared = os.environ.get("EARL_SHARED_GPU") == "1"
     if shared:
         local = 0
+    elif torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py --gpus {os.environ.get('WORLD_SIZE')}: rank {local} has no GPU "
+                         f"({torch.cuda.device_count()} visible); EARL_SHARED_GPU=1 puts every "
+                         "rank on cuda:0 (code-path check only)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if shared:
@@ -487,17 +492,28 @@ def run_multi(args):
     send = [W.gen_field_device(fields[f], tok_r[rank], 1000 + 16 * rank + f, dev) for f in range(F)]
     D = Dispatcher(window_bytes=T * B + (1 << 20), device=local)
     stream = torch.cuda.current_stream()
-    glens, _ = D.allgather_lens(my_lens)
+    # step a1 on the device: the rollout's per-rank counts are fixed by the source layout, so the
+    # length gather is one kernel over the peer windows (earl_allgather_lengths), no host sync
+    from paper_2510_05943_b200.dispatch import rank_counts
+    cnts = rank_counts(src, world)
+    glens_buf = torch.empty(max(1, len(lens)), dtype=torch.int32, device=dev)
+    glens, _ = D.allgather_lens(my_lens, counts=cnts, out=glens_buf)
+    D.comm.check()
+    assert glens.cpu().tolist() == [int(x) for x in lens], "a1: gathered lengths differ"
     plan = D.plan(src, dst, glens, fields)
     st = plan.stats()
     recv_ptrs, _views = D.alloc_recv(plan, fields)
     staged = args.exchange == "staged"
     plan.destroy()
 
+    if staged and not shared:
+        D.init_nccl()   # K8: the library's grouped ncclSend / ncclRecv (one GPU per rank)
     mplan = D.plan(src, dst, glens, fields, stream)
 
     def step(ev=None):
-        gl, _ = D.allgather_lens(my_lens)
+        if ev is not None:
+            ev[3].record(stream)
+        gl, _ = D.allgather_lens(my_lens, counts=cnts, out=glens_buf, stream=stream)
         if ev is not None:
             ev[0].record(stream)
         p = mplan
@@ -512,12 +528,13 @@ def run_multi(args):
         if ev is not None:
             ev[2].record(stream)
 
-    clocks = ClockSampler(local) if rank == 0 and not args.profile else None
+    # every rank samples its own GPU's clocks (shared-GPU mode: rank 0 only)
+    clocks = ClockSampler(local) if (rank == 0 or not shared) and not args.profile else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     l0 = earl.kernel_launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
@@ -530,15 +547,42 @@ def run_multi(args):
     t1 = time.time()
     launches = earl.kernel_launch_count() - l0
     from paper_2510_05943_b200.dispatch import max_over_ranks
-    ms_step, t_exec, t_plan = max_over_ranks([a.elapsed_time(b) / args.steps,
-                                              sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps,
-                                              statistics.median(e[0].elapsed_time(e[1]) for e in evs)])
+    my_exec = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ms_step, t_exec, t_plan, t_a1, neg_exec_min = max_over_ranks(
+        [a.elapsed_time(b) / args.steps, my_exec,
+         statistics.median(e[0].elapsed_time(e[1]) for e in evs),
+         statistics.median(e[3].elapsed_time(e[0]) for e in evs), -my_exec])
+    t_exec_min = -neg_exec_min
+    clocks_r = None
     plan = D.plan(src, dst, glens, fields)
     plan.sync()
     plan.destroy()
 
     # end to end through the public API with host buffers: H2D of this rank's payload (pinned),
     # length all-gather, plan, exchange, D2H of this rank's cu_seqlens -- every step
+    # the whole step (a1 gather + replan + exec) captured once as a CUDA graph and replayed
+    graph_ms = None
+    if not (args.profile or staged):
+        gs = torch.cuda.Stream(device=dev)
+        gs.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            gl, _ = D.allgather_lens(my_lens, counts=cnts, out=glens_buf, stream=gs)
+            mplan.replan(gl, gs)
+            mplan.exec(send, recv_ptrs, gs)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record(stream)
+        for _ in range(args.steps):
+            graph.replay()
+        gb.record(stream)
+        torch.cuda.synchronize()
+        graph_ms = max_over_ranks([ga.elapsed_time(gb) / args.steps])[0]
+        mplan.sync()
+        del graph
     e2e = None
     if not (args.no_e2e or args.profile):
         host_send = [torch.empty(t.numel(), dtype=torch.uint8, pin_memory=True) for t in send]
@@ -549,10 +593,14 @@ def run_multi(args):
         cu_host = torch.empty(ns_mine + 1, dtype=torch.int32, pin_memory=True)
         h2d = sum(hs.numel() for hs in host_send)
 
+        my_lens_host = my_lens.cpu().pin_memory()
+        h2d += my_lens_host.numel() * 4
+
         def e2e_step():
             for hs, d in zip(host_send, send):
                 d.copy_(hs, non_blocking=True)
-            gl, _ = D.allgather_lens(my_lens)
+            my_lens.copy_(my_lens_host, non_blocking=True)
+            gl, _ = D.allgather_lens(my_lens, counts=cnts, out=glens_buf, stream=stream)
             mplan.replan(gl, stream)
             if staged:
                 D.exec_staged(mplan, send, recv_ptrs, stream=stream)
@@ -576,9 +624,18 @@ def run_multi(args):
         e2e = {"value": T * B / (ems * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ems,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int((ns_mine + 1) * 4),
                "steps": n_e2e, "per_rank": True}
+    if clocks:
+        clocks.mark(t0, t1)
+        clocks_r = clocks.stop()
+    all_clocks = [None] * world
+    dist.all_gather_object(all_clocks, clocks_r)
+    mapped = sum(1 for p in range(world) if p != rank and D.comm.peer_mapped(p))
+    all_mapped = [None] * world
+    dist.all_gather_object(all_mapped, mapped)
     if rank == 0:
         payload = T * B
         nvl = max(max(st["egress"]), max(st["ingress"]))
+        nvl_gbps = nvl / (t_exec * 1e-3) / 1e9
         out = {"metric": METRIC, "value": payload / (ms_step * 1e-3) / 1e9, "unit": "GB/s",
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
@@ -588,8 +645,21 @@ def run_multi(args):
                           "l2": "inputs larger than L2", "parallelism": f"{world} ranks, P2P",
                           "shared_gpu": shared},
                "per_gpu_GBps": payload / (ms_step * 1e-3) / 1e9 / world,
-               "t_plan_ms": t_plan, "t_exec_ms": t_exec,
+               "t_a1_ms": t_a1, "t_plan_ms": t_plan, "t_exec_ms": t_exec,
+               "t_exec_min_ms": t_exec_min,
                "exchange": args.exchange,
+               "nvlink": {"bottleneck_bytes": int(nvl), "GBps": nvl_gbps,
+                          "frac_measured_770": nvl_gbps / NVLINK_PEER_GBPS,
+                          "frac_nominal_900": nvl_gbps / NVLINK_NOMINAL_GBPS,
+                          "egress_per_rank": [int(x) for x in st["egress"]],
+                          "ingress_per_rank": [int(x) for x in st["ingress"]],
+                          "self_per_rank": [int(x) for x in st["self"]],
+                          "note": "t_exec includes the entry barrier (rank skew): "
+                                  "t_exec_ms is the max, t_exec_min_ms the min over ranks"},
+               "data_plane": {"kind": "CUDA IPC windows, fused P2P stores" if not staged
+                              else ("pack + library NCCL grouped send/recv + unpack" if not shared
+                                    else "pack + exchange over the gloo group + unpack"),
+                              "mapped_peers_per_rank": all_mapped},
                "roofline": {"bound": "nvlink", "kernel": ("pack + NCCL send/recv + unpack" if staged
                                                           else "entry barrier + copy_kernel (P2P)"),
                             "achieved": nvl / (t_exec * 1e-3) / 1e9, "peak": NVLINK_PEER_GBPS,
@@ -607,20 +677,42 @@ def run_multi(args):
             nccl_ver = None
         out["comm"] = {"backend": dist.get_backend(), "nccl": nccl_ver,
                        "env": {k: v for k, v in sorted(os.environ.items()) if k.startswith("NCCL_")}}
-        if clocks:
-            clocks.mark(t0, t1)
-            out["clocks"] = clocks.stop()
+        if graph_ms is not None:
+            out["graph"] = {"ms_per_step": graph_ms, "value": payload / (graph_ms * 1e-3) / 1e9,
+                            "note": "a1 gather + replan + exec captured once as a CUDA graph"}
+        if all_clocks[0] is not None:
+            c0 = dict(all_clocks[0])
+            c0["per_rank"] = all_clocks
+            out["clocks"] = c0
         emit(out)
     dist.barrier()
     dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` (N > 1) started without torchrun: re-execute this script under
+    torch.distributed.run with one process per GPU (rank 0 prints the JSON line)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
         return
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     if world > 1:
         run_multi(args)
     else:

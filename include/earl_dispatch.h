@@ -59,7 +59,7 @@
 extern "C" {
 #endif
 
-#define EARL_ABI_VERSION 2
+#define EARL_ABI_VERSION 3
 #define EARL_MAX_WORLD 8        /* reading c21: one box, W <= 8 */
 #define EARL_MAX_FIELDS 16
 #define EARL_HANDLE_BYTES 128   /* size of the exported window handle */
@@ -74,7 +74,7 @@ typedef enum {
   EARL_ERR_CAPACITY = 3,         /* window too small, dst rank > INT32_MAX tokens (c12),
                                     LPT with N > 8192, buffer too small                  */
   EARL_ERR_CUDA = 4,             /* a CUDA runtime call failed                            */
-  EARL_ERR_NCCL = 5,             /* reserved                                              */
+  EARL_ERR_NCCL = 5,             /* an NCCL call of the staged exchange failed (K8)       */
   EARL_ERR_TIMEOUT = 6,          /* peer signals missing; mask in earl_last_error */
   EARL_ERR_MISMATCH = 7,         /* plan hash differs across ranks (debug)                */
   EARL_ERR_UNSUPPORTED = 8,      /* world > 8, wrong comm kind for the call               */
@@ -114,7 +114,9 @@ typedef struct {
   int32_t sp_min_len;           /* EARL_SP_THRESHOLD: shortest sequence that is split (>= 0) */
   int32_t reserved;             /* 0 */
   const int64_t* counts;        /* HOST [dp], GIVEN_COUNTS only */
-  const int32_t* group_of_seq;  /* DEVICE [N], EXPLICIT only */
+  const int32_t* group_of_seq;  /* DEVICE [N], EXPLICIT only; read by the planner at every
+                                   earl_dispatch_plan / earl_plan_replan, so it must stay valid
+                                   for the plan's lifetime */
 } earl_layout_t;
 
 /* One per-token field: bytes_per_elem * elems_per_token bytes per token (opaque). */
@@ -165,6 +167,31 @@ EARL_API earl_status_t earl_comm_alloc(earl_comm_t comm, int32_t rank, uint64_t 
 EARL_API earl_status_t earl_comm_reset_alloc(earl_comm_t comm);
 EARL_API earl_status_t earl_comm_info(earl_comm_t comm, int32_t* rank, int32_t* world, int32_t* emulated);
 EARL_API earl_status_t earl_comm_destroy(earl_comm_t comm);
+/* Bit p of *mask is set when peer p's window is mapped into this process (CUDA IPC; bench
+ * evidence of the N-rank data plane).  Emulated comm: 0. */
+EARL_API earl_status_t earl_comm_peer_mask(earl_comm_t comm, uint32_t* mask);
+
+/* Step a1: the global length vector every rank plans from (the layout
+ * knowledge of PAPER.md:178), gathered on the device.  Global order is rank-major (reading c6):
+ * rank r's counts[r] lengths occupy [sum_{q<r} counts[q], +counts[r]) of the output.
+ * counts: HOST [world], identical on every rank (the source layout's per-rank sequence counts,
+ *   e.g. rollout GIVEN_COUNTS; 0 for replicas that hold no sequences of their own).
+ * local_lens: [1] (emulated: [world]) DEVICE int32 pointers to this rank's counts[rank] lengths
+ *   (NULL where the count is 0).
+ * global_lens: DEVICE int32 [sum(counts)] output, written on `stream`.
+ * Collective in a multi-process comm: one kernel stores this rank's lengths into every peer's
+ * gather area (a double buffer after the window's signal pad, EARL_LENS_CAPACITY sequences,
+ * default 2^18, read at earl_comm_create), releases an epoch flag to each peer and acquires
+ * theirs; no host synchronisation, so gather + earl_plan_replan + earl_dispatch_exec capture
+ * into one CUDA graph.  A peer missing for longer than the comm's timeout latches TIMEOUT,
+ * reported by earl_comm_check.
+ * Errors: INVALID_ARGUMENT (NULL, negative count), CAPACITY (sum(counts) > the gather area). */
+EARL_API earl_status_t earl_allgather_lengths(earl_comm_t comm, const int64_t* counts,
+                                              const void* const* local_lens, int32_t* global_lens,
+                                              void* stream);
+/* Synchronise `stream` and report (then clear) an error latched on the device by a comm-level
+ * collective (earl_allgather_lengths: TIMEOUT with the missing peers' bit mask). */
+EARL_API earl_status_t earl_comm_check(earl_comm_t comm, void* stream);
 
 /* ---- plan -------------------------------------------------------------------------- */
 
@@ -181,7 +208,8 @@ EARL_API earl_status_t earl_dispatch_plan(earl_comm_t comm, const earl_layout_t*
                                  int64_t n_seqs, const earl_field_t* fields, int32_t n_fields,
                                  void* stream, earl_plan_t* plan);
 /* Re-plan the same N sequences (same comm, layouts, fields) for new lengths seq_lens (DEVICE
- * int32 [N]) into the plan's existing device memory: nothing is allocated, so a training loop
+ * int32 [N]; ignored, may be NULL, for a plan from earl_plan_seq_fields, which re-reads its
+ * token plan's groups) into the plan's existing device memory: nothing is allocated, so a training loop
  * re-plans every batch at the planner's cost only.  Stream-ordered: work still using the
  * previous plan must precede it on `stream` (or be synchronised).  earl_dispatch_plan followed
  * by earl_plan_replan / earl_dispatch_exec is capturable into a CUDA graph; after replaying one,
@@ -205,6 +233,19 @@ EARL_API earl_status_t earl_plan_local_meta(earl_plan_t plan, int32_t rank, int3
  * layouts and the SP degree folded into TP (reading n4). */
 EARL_API earl_status_t earl_plan_groups(earl_plan_t plan, int32_t* src_groups, int32_t* dst_groups,
                                         void* stream);
+/* Reading n4: plan the routing of PER-SEQUENCE fields (a reward or score per
+ * episode, n_fields of them, bytes_per_elem * elems_per_token bytes per SEQUENCE) along
+ * `token_plan`: every destination rank (g, k, t) receives one record per sequence of its group,
+ * in the group order of the token plan (every SP rank and TP replica holds a copy), sent by the
+ * source rank (g_src(i), SP 0, t mod tp_src).  Built on the device as a second plan over unit
+ * lengths whose layouts are the token plan's with SP folded into TP and the groups pinned as
+ * EXPLICIT (its own copies of g_src / g_dst, refreshed by earl_plan_replan(seq_plan, NULL, s)
+ * after the token plan is re-planned).  Execute with earl_dispatch_exec (buffers hold one record
+ * per sequence); query with the usual calls.  The token plan stays alive until the last plan
+ * made from it is destroyed.  Errors: as earl_dispatch_plan; INVALID_ARGUMENT if token_plan is
+ * itself a per-sequence plan. */
+EARL_API earl_status_t earl_plan_seq_fields(earl_plan_t token_plan, const earl_field_t* fields,
+                                            int32_t n_fields, void* stream, earl_plan_t* seq_plan);
 /* Byte accounting of SPEC.md:239-247 (host; synchronises). */
 EARL_API earl_status_t earl_plan_stats(earl_plan_t plan, earl_plan_stats_t* stats);
 /* Debug check of replicated planning (every rank computes a byte-identical plan
@@ -230,17 +271,23 @@ EARL_API earl_status_t earl_plan_destroy(earl_plan_t plan);
  *   DEVICE memory, or page-locked HOST memory mapped into the device address space
  *   (cudaHostAlloc / cudaHostRegister under UVA): the kernel then reads it over PCIe itself
  *   (zero-copy; no separate host-to-device copy).
- * recv_bufs: DEVICE field arrays under `dst`, sized n_local_tokens * B_f.  Multi-process
- *   comm with world > 1: each must lie inside this rank's window (earl_comm_alloc) at the
- *   same offset on every rank -- peers store into it over NVLink.  Ranks not in the dst
- *   layout may pass NULLs.
+ * recv_bufs: DEVICE field arrays under `dst`, sized n_local_tokens * B_f; NULL = this rank
+ *   receives nothing for that field (e.g. it is in no destination layout).  Multi-process comm
+ *   with world > 1: each non-NULL one must lie inside this rank's window (earl_comm_alloc) --
+ *   peers store into it over NVLink.  Offsets need not match across ranks: every rank
+ *   publishes its own offsets in its signal pad and the senders write where the destination
+ *   put its buffers, so a source-only rank passing NULLs still sends all of its records.
  * Protocol (multi-process): entry barrier (every peer's stream reached exec, so its recv
- * buffers may be overwritten), stores, system-scope fence, release of an epoch flag into
- * each peer's signal pad, acquire-wait for every peer's flag.  When the stream passes the
- * call, this rank's recv buffers are complete.  A peer missing for > 10 s (or the
- * EARL_TIMEOUT_MS read at earl_comm_create) latches TIMEOUT with the bit mask of the missing
- * peers, reported by the next synchronising call (a barrier timeout names the
- * missing workers). */
+ * buffers may be overwritten; each rank's receive offsets are published with its ready flag),
+ * stores, system-scope fence, release of a done flag (2 * epoch + failed) into each peer's
+ * signal pad, acquire-wait for every peer's.  When the stream passes the call, this rank's
+ * recv buffers are complete.  A peer missing for > 10 s (or the EARL_TIMEOUT_MS read at
+ * earl_comm_create) latches TIMEOUT with the bit mask of the missing peers; a peer that skipped
+ * its copies (its own barrier timed out) makes every rank that sees it latch TIMEOUT naming it
+ * (detail bits 8-15).  Both are reported by the next synchronising call (a
+ * barrier timeout names the missing workers).
+ * Launches on one plan are serialised in issue order across streams (each waits for the plan's
+ * previous launch), and earl_plan_sync / earl_plan_destroy cover every launch. */
 EARL_API earl_status_t earl_dispatch_exec(earl_plan_t plan, const void* const* send_bufs,
                                  void* const* recv_bufs, void* stream);
 /* The fused dispatch of ONE source rank's records (data leaves "from their
@@ -280,6 +327,32 @@ EARL_API earl_status_t earl_dispatch_unpack(earl_plan_t plan, const void* const*
 EARL_API earl_status_t earl_plan_messages(earl_plan_t plan, int32_t rank, int64_t* send_off,
                                           int64_t* send_bytes, int64_t* recv_off,
                                           int64_t* recv_bytes);
+
+/* ---- K8: the staged exchange over NCCL ------------------
+ * The comparator of the fused P2P exec: pack -> grouped ncclSend / ncclRecv of the per-peer
+ * messages (the earl_plan_messages table; a rank's message to itself goes through NCCL too) ->
+ * unpack.  Two extra HBM passes and a host read of the byte table per call (NCCL takes host
+ * sizes), against the fused exec's single pass; also the transport that crosses nodes. */
+
+/* A fresh NCCL unique id (EARL_HANDLE_BYTES bytes) on one rank, to be broadcast out of band. */
+EARL_API earl_status_t earl_nccl_unique_id(void* id_out);
+/* Collective: create the comm's NCCL communicator (ncclCommInitRankConfig, world ranks, this
+ * rank).  Knobs read here: EARL_NCCL_MIN_CTAS / EARL_NCCL_MAX_CTAS (config.minCTAs / maxCTAs),
+ * EARL_NCCL_REGISTER=1 (stage buffers from ncclMemAlloc, registered with ncclCommRegister).
+ * Errors: UNSUPPORTED (emulated comm), NCCL. */
+EARL_API earl_status_t earl_comm_init_nccl(earl_comm_t comm, const void* unique_id);
+/* Step a4 of the staged path: this rank's messages from send_stage (as earl_dispatch_pack left
+ * them) to every peer, and every peer's message into recv_stage (concatenated in source-rank
+ * order, the layout earl_dispatch_unpack reads), as one NCCL group on `stream`.  Synchronises
+ * on the plan for the byte table.  Errors: INVALID_ARGUMENT (no NCCL comm, NULL stage with
+ * bytes to move), NCCL. */
+EARL_API earl_status_t earl_dispatch_exchange(earl_plan_t plan, const void* send_stage,
+                                              void* recv_stage, void* stream);
+/* pack + exchange + unpack with comm-owned stage buffers (grown on demand, outside the timed
+ * steady state); send_bufs / recv_bufs as for earl_dispatch_exec (recv_bufs need not be in the
+ * window).  Synchronises on the plan once per call. */
+EARL_API earl_status_t earl_dispatch_exec_staged(earl_plan_t plan, const void* const* send_bufs,
+                                                 void* const* recv_bufs, void* stream);
 
 /* ---- NEXT-2: distributed aggregation before the dispatch ---------- */
 

@@ -14,9 +14,20 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libearl_dispatch.so")
-SOURCES = ["api.cu", "planner.cu", "copy.cu", "aggregate.cu", "selector.cpp"]
+SOURCES = ["api.cu", "planner.cu", "copy.cu", "aggregate.cu", "lengths.cu", "selector.cpp"]
 HEADERS = ["earl_internal.cuh"]
 PUBLIC_HEADER = os.path.join(ROOT, "include", "earl_dispatch.h")
+
+def nccl_dir() -> str:
+    """The NCCL torch ships with (same soname: one NCCL per process)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        d = list(spec.submodule_search_locations)[0]
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    return "/usr"
+
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -46,7 +57,13 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    nd = nccl_dir()
     cmd = [nvcc()] + NVCC_FLAGS + ["-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp"]
+    if nd == "/usr":
+        cmd += ["-lnccl"]
+    else:
+        cmd += ["-I", os.path.join(nd, "include"), "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+                "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
     # tuning experiments only (e.g. EARL_NVCC_DEFINES="EARL_AGG_CTAS_PER_SM=2")
     cmd += ["-D" + d for d in os.environ.get("EARL_NVCC_DEFINES", "").split()]
     cmd += [os.path.join(CSRC, s) for s in SOURCES]

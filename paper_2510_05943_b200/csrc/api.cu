@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
 
 #include "earl_internal.cuh"
@@ -84,6 +85,8 @@ struct earl_comm {
   int32_t device = 0;
   bool emulated = false;
   uint64_t window_bytes = 0;
+  uint64_t pad_bytes = kPadBytes;  // signal pad + (multi-process) the a1 gather double buffer
+  int64_t lens_cap = 0;            // sequences per gather buffer
   uint8_t* win[kMaxWorld] = {};    // local windows (emulated: one per rank; else win[rank])
   uint8_t* peer[kMaxWorld] = {};   // every rank's window as addressable from this process
   bool peer_mapped[kMaxWorld] = {};
@@ -91,9 +94,18 @@ struct earl_comm {
   uint64_t alloc_off[kMaxWorld] = {};
   uint64_t epoch = 0;
   unsigned int* done_ctr = nullptr;
+  unsigned int* lens_ctr = nullptr;  // a1 gather: last-CTA counter
+  int32_t* dev_err = nullptr;        // a1 gather: [status, missing-peer mask] latched on the device
   int sm_count = 148;
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int refs = 1;          // the user's handle + one per live plan: freed when it reaches 0
+  // K8, the staged exchange's NCCL comm (earl_comm_init_nccl) and its stage buffers (send,
+  // receive), grown on demand; registered with the comm when EARL_NCCL_REGISTER=1
+  ncclComm_t nccl = nullptr;
+  bool nccl_register = false;
+  void* nst[2] = {};
+  uint64_t nst_bytes[2] = {};
+  void* nreg[2] = {};
 };
 
 namespace {
@@ -105,7 +117,17 @@ void comm_release(earl_comm* c) {
     if (c->peer_mapped[p]) cudaIpcCloseMemHandle(c->peer[p]);
   for (int r = 0; r < kMaxWorld; ++r)
     if (c->win[r]) cudaFree(c->win[r]);
+  for (int k = 0; k < 2; ++k) {
+    if (c->nreg[k]) ncclCommDeregister(c->nccl, c->nreg[k]);
+    if (c->nst[k]) {
+      if (c->nccl_register) ncclMemFree(c->nst[k]);
+      else cudaFree(c->nst[k]);
+    }
+  }
+  if (c->nccl) ncclCommDestroy(c->nccl);
   if (c->done_ctr) cudaFree(c->done_ctr);
+  if (c->lens_ctr) cudaFree(c->lens_ctr);
+  if (c->dev_err) cudaFree(c->dev_err);
   cudaGetLastError();
   delete c;
 }
@@ -121,13 +143,19 @@ struct earl_plan {
   void* mem = nullptr;
   size_t mem_bytes = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev = nullptr;
+  cudaEvent_t ev = nullptr;   // recorded after the plan's last launch (use_end)
+  bool ev_recorded = false;
   bool synced = false;
   PlanHeader host_hdr{};
   size_t lpt_smem = 0;
   int grid = 1;
   void* agg_ws = nullptr;     // returns_kernel look-back workspace (AggWork + AggWindow[agg_cap])
   int64_t agg_cap = 0;
+  // per-sequence field plan (earl_plan_seq_fields): the token plan it follows (referenced, so it
+  // outlives this plan) and this plan's own device arrays [g_src | g_dst | ones], N int32 each
+  earl_plan* parent = nullptr;
+  int32_t* owned = nullptr;
+  int refs = 1;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -176,7 +204,17 @@ extern "C" earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t c
   c->world = world;
   c->device = cuda_device;
   c->emulated = (rank == EARL_ALL_RANKS);
-  c->window_bytes = ((window_bytes + 255) & ~255ull) + kPadBytes;
+  // multi-process windows carry the a1 gather area after the signal pad: 2 x lens_cap int32
+  // (EARL_LENS_CAPACITY sequences, default 2^18 = 2 MiB per window)
+  if (!c->emulated && world > 1) {
+    c->lens_cap = int64_t(1) << 18;
+    if (const char* lc = getenv("EARL_LENS_CAPACITY")) {
+      const long long v = atoll(lc);
+      if (v > 0) c->lens_cap = (v + 3) & ~3LL;
+    }
+    c->pad_bytes = kPadBytes + (((uint64_t)c->lens_cap * 8 + 255) & ~255ull);
+  }
+  c->window_bytes = ((window_bytes + 255) & ~255ull) + c->pad_bytes;
   if (const char* t = getenv("EARL_TIMEOUT_MS")) {  // peer waits (SPEC.md:316 barrier timeout)
     const long long ms = atoll(t);
     if (ms > 0) c->timeout_ns = (uint64_t)ms * 1000000ull;
@@ -202,10 +240,14 @@ extern "C" earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t c
     e = cudaMemset(c->win[rr], 0, kPadBytes);
     if (e != cudaSuccess) return cleanup(fail(EARL_ERR_CUDA, "pad memset: %s", cudaGetErrorString(e)));
     c->peer[rr] = c->win[rr];
-    c->alloc_off[rr] = kPadBytes;
+    c->alloc_off[rr] = c->pad_bytes;
   }
   cudaError_t e = cudaMalloc(&c->done_ctr, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(c->done_ctr, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->lens_ctr, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->lens_ctr, 0, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev_err, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->dev_err, 0, 2 * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cleanup(fail(EARL_ERR_CUDA, "comm init: %s", cudaGetErrorString(e)));
   c->peers_ready = c->emulated || world == 1;
@@ -260,7 +302,7 @@ extern "C" earl_status_t earl_comm_alloc(earl_comm_t c, int32_t rank, uint64_t b
 
 extern "C" earl_status_t earl_comm_reset_alloc(earl_comm_t c) {
   if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
-  for (int r = 0; r < kMaxWorld; ++r) c->alloc_off[r] = kPadBytes;
+  for (int r = 0; r < kMaxWorld; ++r) c->alloc_off[r] = c->pad_bytes;
   return EARL_OK;
 }
 
@@ -270,6 +312,87 @@ extern "C" earl_status_t earl_comm_info(earl_comm_t c, int32_t* rank, int32_t* w
   if (rank) *rank = c->rank;
   if (world) *world = c->world;
   if (emulated) *emulated = c->emulated ? 1 : 0;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_allgather_lengths(earl_comm_t c, const int64_t* counts,
+                                                const void* const* local_lens, int32_t* global_lens,
+                                                void* stream) {
+  NvtxRange nvtx("earl_allgather_lengths");
+  if (!c || !counts || !local_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!c->peers_ready)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "multi-process comm: earl_comm_import_peers not called");
+  LensArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.world = c->world;
+  a.emulated = c->emulated ? 1 : 0;
+  a.me = c->emulated ? 0 : c->rank;
+  int64_t tot = 0;
+  for (int r = 0; r < c->world; ++r) {
+    if (counts[r] < 0) return fail(EARL_ERR_INVALID_ARGUMENT, "counts[%d] < 0", r);
+    a.counts[r] = counts[r];
+    a.start[r] = tot;
+    tot += counts[r];
+  }
+  if (tot > 0x7fffffffLL) return fail(EARL_ERR_INVALID_ARGUMENT, "more than 2^31 - 1 sequences");
+  a.total = tot;
+  if (tot > 0 && !global_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "global_lens is NULL");
+  a.out = global_lens;
+  if (c->emulated) {
+    for (int r = 0; r < c->world; ++r) {
+      a.src[r] = static_cast<const int32_t*>(local_lens[r]);
+      if (counts[r] > 0 && !a.src[r])
+        return fail(EARL_ERR_INVALID_ARGUMENT, "local_lens[%d] is NULL with counts %lld", r,
+                    (long long)counts[r]);
+    }
+  } else {
+    a.local = static_cast<const int32_t*>(local_lens[0]);
+    if (counts[c->rank] > 0 && !a.local)
+      return fail(EARL_ERR_INVALID_ARGUMENT, "local_lens is NULL with counts %lld",
+                  (long long)counts[c->rank]);
+  }
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  clear_stale_error();
+  if (!c->emulated && c->world == 1) {  // one rank: the global vector is the local one
+    if (tot > 0) CUDA_TRY(cudaMemcpyAsync(global_lens, a.local, tot * 4, cudaMemcpyDeviceToDevice, s));
+    return EARL_OK;
+  }
+  if (tot == 0 && c->emulated) return EARL_OK;
+  if (!c->emulated) {
+    if (tot > c->lens_cap)
+      return fail(EARL_ERR_CAPACITY, "%lld sequences exceed the gather capacity %lld (EARL_LENS_CAPACITY)",
+                  (long long)tot, (long long)c->lens_cap);
+    a.cap = c->lens_cap;
+    a.my_pad = reinterpret_cast<uint64_t*>(c->win[c->rank]);
+    for (int q = 0; q < c->world; ++q) a.peer_pad[q] = reinterpret_cast<uint64_t*>(c->peer[q]);
+    a.ctr = c->lens_ctr;
+    a.err = c->dev_err;
+    a.timeout_ns = c->timeout_ns;
+  }
+  cudaError_t e = launch_gather_lengths(a, c->sm_count, s);
+  if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "length gather launch: %s", cudaGetErrorString(e));
+  g_launches.fetch_add(1);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_check(earl_comm_t c, void* stream) {
+  if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
+  DeviceGuard g(c->device);
+  int32_t h[2] = {0, 0};
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  CUDA_TRY(cudaMemcpy(h, c->dev_err, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h[0] == 0) return EARL_OK;
+  CUDA_TRY(cudaMemset(c->dev_err, 0, sizeof(h)));
+  return fail((earl_status_t)h[0], "length gather: peers missing (mask 0x%x)", h[1]);
+}
+
+extern "C" earl_status_t earl_comm_peer_mask(earl_comm_t c, uint32_t* mask) {
+  if (!c || !mask) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  uint32_t m = 0;
+  for (int p = 0; p < c->world; ++p)
+    if (c->peer_mapped[p]) m |= 1u << p;
+  *mask = m;
   return EARL_OK;
 }
 
@@ -345,10 +468,36 @@ T* carve(uint8_t*& p, int64_t count) {
   return r;
 }
 
-// Host view of the plan header: always re-read after synchronising the plan's stream (a plan
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cap != cudaStreamCaptureStatusNone;
+}
+
+// Every device launch on a plan is bracketed by use_begin / use_end: a launch on a stream other
+// than the plan's last one first waits for the plan's event (the plan's launches share its
+// scheduling counters and header, so they are serialised in issue order whatever streams the
+// caller uses), and the event is re-recorded after it.  plan_wait and earl_plan_destroy
+// therefore cover every launch, not only the planner's.  Under CUDA-graph capture nothing is
+// recorded (the caller synchronises the replay stream before host queries, as documented).
+void use_begin(earl_plan* p, cudaStream_t s) {
+  if (s != p->stream && p->ev && !capturing(s) && p->ev_recorded) cudaStreamWaitEvent(s, p->ev, 0);
+}
+void use_end(earl_plan* p, cudaStream_t s) {
+  p->synced = false;
+  if (capturing(s)) return;
+  p->stream = s;
+  if (p->ev && cudaEventRecord(p->ev, s) == cudaSuccess) p->ev_recorded = true;
+}
+
+// Host view of the plan header: always re-read after the plan's last launch completed (a plan
 // may have been re-planned on the device -- replan, CUDA-graph replay -- since the last query).
 earl_status_t plan_wait(earl_plan_t p) {
   DeviceGuard g(p->comm->device);
+  if (p->ev_recorded) CUDA_TRY(cudaEventSynchronize(p->ev));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   CUDA_TRY(cudaMemcpy(&p->host_hdr, p->args.hdr, sizeof(PlanHeader), cudaMemcpyDeviceToHost));
   p->synced = true;
@@ -368,7 +517,12 @@ earl_status_t plan_check(earl_plan_t p) {
       case EARL_ERR_CAPACITY:
         return fail(EARL_ERR_CAPACITY, "dst shard %d holds more than INT32_MAX tokens", h.err_detail);
       case EARL_ERR_TIMEOUT:
-        return fail(EARL_ERR_TIMEOUT, "peers missing (mask 0x%x)", h.err_detail);
+        if ((h.err_detail >> 8) == 0)
+          return fail(EARL_ERR_TIMEOUT, "peers missing (mask 0x%x)", h.err_detail & 0xff);
+        return fail(EARL_ERR_TIMEOUT,
+                    "peers missing (mask 0x%x); peers that skipped their copies (mask 0x%x): this "
+                    "rank's receive buffers are incomplete", h.err_detail & 0xff,
+                    (h.err_detail >> 8) & 0xff);
       default: return fail((earl_status_t)h.err, "device error %d", h.err_detail);
     }
   }
@@ -392,6 +546,7 @@ bool coords(const earl_layout_t& L, int rank, int* g, int* k, int* t) {
 // synchronises the stream itself before host queries).
 cudaError_t plan_launch(earl_plan* p, cudaStream_t s) {
   PlanArgs& a = p->args;
+  use_begin(p, s);
   cudaError_t e = cudaMemsetAsync(a.hdr, 0, sizeof(PlanHeader), s);
   if (e != cudaSuccess) return e;
   static const char* plan_trace = getenv("EARL_PLAN_TRACE");
@@ -414,12 +569,8 @@ cudaError_t plan_launch(earl_plan* p, cudaStream_t s) {
   }
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1);
-  p->stream = s;
-  p->synced = false;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cap);
-  if (cap == cudaStreamCaptureStatusNone) e = cudaEventRecord(p->ev, s);
-  return e;
+  use_end(p, s);
+  return cudaSuccess;
 }
 
 extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* src,
@@ -559,11 +710,34 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   return EARL_OK;
 }
 
+namespace {
+// A per-sequence field plan re-reads its token plan's group assignment (stream-ordered after the
+// token plan's last launch) before its own planner runs.
+cudaError_t refresh_groups(earl_plan* p, cudaStream_t s) {
+  earl_plan* t = p->parent;
+  const size_t bytes = (size_t)p->N * sizeof(int32_t);
+  if (!bytes) return cudaSuccess;
+  if (s != t->stream && t->ev_recorded && !capturing(s)) cudaStreamWaitEvent(s, t->ev, 0);
+  cudaError_t e = cudaMemcpyAsync(p->owned, t->args.grp[0], bytes, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(p->owned + p->N, t->args.grp[1], bytes, cudaMemcpyDeviceToDevice, s);
+  return e;
+}
+}  // namespace
+
 extern "C" earl_status_t earl_plan_replan(earl_plan_t p, const int32_t* seq_lens, void* stream) {
   NvtxRange nvtx("earl_plan_replan");
   if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
-  if (p->N > 0 && !seq_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens is NULL");
   DeviceGuard g(p->comm->device);
+  if (p->parent) {  // a per-sequence field plan: unit lengths, groups from its token plan
+    use_begin(p, static_cast<cudaStream_t>(stream));
+    cudaError_t e = refresh_groups(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "replan groups: %s", cudaGetErrorString(e));
+    e = plan_launch(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "replan: %s", cudaGetErrorString(e));
+    return EARL_OK;
+  }
+  if (p->N > 0 && !seq_lens) return fail(EARL_ERR_INVALID_ARGUMENT, "seq_lens is NULL");
   p->args.seq_lens = seq_lens;
   cudaError_t e = plan_launch(p, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "replan: %s", cudaGetErrorString(e));
@@ -599,9 +773,13 @@ extern "C" earl_status_t earl_plan_local_meta(earl_plan_t p, int32_t rank, int32
   if (!coords(p->lay[1], rank, &g, &k, &t)) return EARL_OK;  // not a destination: nothing
   DeviceGuard dg(p->comm->device);
   clear_stale_error();
+  use_begin(p, (cudaStream_t)stream);
   cudaError_t e = launch_local_meta(p->args, g, k, cu, ids, tok_start, (cudaStream_t)stream);
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "local_meta launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  const bool synced = p->synced;
+  use_end(p, (cudaStream_t)stream);
+  p->synced = synced;  // a read-only launch: the host header stays valid
   return EARL_OK;
 }
 
@@ -611,10 +789,14 @@ extern "C" earl_status_t earl_plan_groups(earl_plan_t p, int32_t* src_groups, in
   DeviceGuard dg(p->comm->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t bytes = (size_t)p->N * sizeof(int32_t);
+  use_begin(p, s);
   if (bytes && src_groups)
     CUDA_TRY(cudaMemcpyAsync(src_groups, p->args.grp[0], bytes, cudaMemcpyDeviceToDevice, s));
   if (bytes && dst_groups)
     CUDA_TRY(cudaMemcpyAsync(dst_groups, p->args.grp[1], bytes, cudaMemcpyDeviceToDevice, s));
+  const bool synced = p->synced;
+  use_end(p, s);
+  p->synced = synced;
   return EARL_OK;
 }
 
@@ -782,17 +964,90 @@ extern "C" earl_status_t earl_plan_export(earl_plan_t p, int64_t capacity, int64
   return EARL_OK;
 }
 
-extern "C" earl_status_t earl_plan_destroy(earl_plan_t p) {
-  if (!p) return EARL_OK;
+namespace {
+void plan_release(earl_plan* p) {
+  if (--p->refs > 0) return;
   {
     DeviceGuard g(p->comm->device);
     if (p->mem) cudaFreeAsync(p->mem, p->stream);
+    if (p->owned) cudaFreeAsync(p->owned, p->stream);
     if (p->agg_ws) cudaFree(p->agg_ws);
     if (p->ev) cudaEventDestroy(p->ev);
     cudaGetLastError();
   }
+  earl_plan* parent = p->parent;
   comm_release(p->comm);
   delete p;
+  if (parent) plan_release(parent);
+}
+}  // namespace
+
+// A token plan referenced by per-sequence field plans is freed with the last of them.
+extern "C" earl_status_t earl_plan_destroy(earl_plan_t p) {
+  if (!p) return EARL_OK;
+  plan_release(p);
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_plan_seq_fields(earl_plan_t tp, const earl_field_t* fields,
+                                              int32_t n_fields, void* stream, earl_plan_t* out) {
+  NvtxRange nvtx("earl_plan_seq_fields");
+  if (!tp || !out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  if (tp->parent) return fail(EARL_ERR_INVALID_ARGUMENT, "the plan is itself a per-sequence field plan");
+  const int64_t N = tp->N;
+  DeviceGuard g(tp->comm->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* owned = nullptr;
+  if (N > 0) {
+    CUDA_TRY(cudaMallocAsync(&owned, (size_t)3 * N * sizeof(int32_t), s));
+    // unit lengths: one record per sequence
+    clear_stale_error();
+    cudaError_t e = launch_fill_i32(owned + 2 * N, 1, N, s);
+    if (e == cudaSuccess) g_launches.fetch_add(1);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(owned, s);
+      return fail(EARL_ERR_CUDA, "unit lengths: %s", cudaGetErrorString(e));
+    }
+  }
+  // reading n4: the token plan's groups as EXPLICIT layouts, SP folded into TP -- rank (g,k,t) =
+  // rank0 + g*sp*tp + k*tp + t is rank (g, 0, k*tp + t) of the folded layout, so every SP rank
+  // and TP replica of a group holds one record per sequence of the group
+  earl_layout_t fl[2];
+  for (int w = 0; w < 2; ++w) {
+    fl[w] = tp->lay[w];
+    fl[w].tp = tp->lay[w].sp * tp->lay[w].tp;
+    fl[w].sp = 1;
+    fl[w].assign = EARL_ASSIGN_EXPLICIT;
+    fl[w].counts = nullptr;
+    fl[w].group_of_seq = owned ? owned + w * N : nullptr;
+    fl[w].sp_split = EARL_SP_BLOCK;
+    fl[w].sp_min_len = 0;
+  }
+  earl_plan_t p = nullptr;
+  // the planner must see the groups: copy them first (stream-ordered after the token plan)
+  earl_plan tmp;
+  tmp.parent = tp;
+  tmp.N = N;
+  tmp.owned = owned;
+  use_begin(tp, s);
+  cudaError_t e = refresh_groups(&tmp, s);
+  tmp.parent = nullptr;
+  tmp.owned = nullptr;
+  if (e != cudaSuccess) {
+    if (owned) cudaFreeAsync(owned, s);
+    return fail(EARL_ERR_CUDA, "seq-field groups: %s", cudaGetErrorString(e));
+  }
+  earl_status_t st = earl_dispatch_plan(tp->comm, &fl[0], &fl[1], owned ? owned + 2 * N : nullptr, N,
+                                        fields, n_fields, stream, &p);
+  if (st != EARL_OK) {
+    if (owned) cudaFreeAsync(owned, s);
+    return st;
+  }
+  p->parent = tp;
+  p->owned = owned;
+  tp->refs += 1;
+  *out = p;
   return EARL_OK;
 }
 
@@ -856,15 +1111,27 @@ int congruent_heavy(const CopyArgs& a) {
   return cong * 10 >= a.Bpre[a.n_fields] * 9 ? 1 : 0;
 }
 
+// The copy-engine shape of a launch: chosen from the field widths (launch_copy), or, for the
+// multi-process exec whose stores cross NVLink, forced by EARL_COPY_CFG_P2P (a launch_copy
+// shape id; e.g. 3 = 8 warps x 3 x 8 KB, more warps issuing remote stores).
+int launch_shape(const CopyArgs& a) {
+  static const int p2p = [] {
+    const char* v = getenv("EARL_COPY_CFG_P2P");
+    return v ? atoi(v) : -1;
+  }();
+  if (a.protocol && p2p >= 0) return 100 + p2p;
+  return congruent_heavy(a);
+}
+
 cudaError_t traced_launch(CopyArgs& a, earl_comm* c, cudaStream_t s) {
   clear_stale_error();
   CopyTrace& t = trace_state();
-  if (!t.path) return launch_copy(a, copy_grid(c), congruent_heavy(a), s);
+  if (!t.path) return launch_copy(a, copy_grid(c), launch_shape(a), s);
   const size_t n = (size_t)c->sm_count * 64 * 4;
   if (!t.dev) { cudaMalloc(&t.dev, n * 8); t.n = n; }
   cudaMemsetAsync(t.dev, 0, n * 8, s);
   a.trace = t.dev;
-  cudaError_t e = launch_copy(a, copy_grid(c), congruent_heavy(a), s);
+  cudaError_t e = launch_copy(a, copy_grid(c), launch_shape(a), s);
   if (e != cudaSuccess) return e;
   std::vector<uint64_t> h(n);
   cudaMemcpyAsync(h.data(), t.dev, n * 8, cudaMemcpyDeviceToHost, s);
@@ -928,39 +1195,53 @@ earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
           return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer rank %d field %d not 16-B aligned", r, f);
         a.dst[r][f] = static_cast<uint8_t*>(ptr);
       }
+  } else if (c->world == 1) {
+    for (int f = 0; f < F; ++f) {
+      void* ptr = recv_bufs[f];
+      if (ptr && !aligned16(ptr))
+        return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer field %d not 16-B aligned", f);
+      a.dst[0][f] = static_cast<uint8_t*>(ptr);
+    }
   } else {
-    // peers store into my recv buffers through their mapping of my window: same offset
+    // every destination publishes its own receive offsets (window-relative) in its signal pad;
+    // the entry barrier resolves them into the table the copy kernel stores through, so each
+    // rank writes where the DESTINATION put its buffers (NULL = receive nothing)
+    uint64_t off[kMaxFields];
+    uint8_t* base = c->win[c->rank];
     for (int f = 0; f < F; ++f) {
       uint8_t* ptr = static_cast<uint8_t*>(recv_bufs[f]);
+      off[f] = kNoOffset;
       if (!ptr) continue;
       if (!aligned16(ptr))
         return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer field %d not 16-B aligned", f);
-      uint8_t* base = c->win[c->rank];
-      if (c->world > 1 && (ptr < base + kPadBytes || ptr >= base + c->window_bytes))
+      if (ptr < base + c->pad_bytes || ptr >= base + c->window_bytes)
         return fail(EARL_ERR_INVALID_ARGUMENT,
                     "recv buffer field %d is not inside this rank's window (use earl_comm_alloc)", f);
-      const uint64_t off = (uint64_t)(ptr - base);
-      for (int d = 0; d < c->world; ++d) a.dst[d][f] = c->peer[d] ? c->peer[d] + off : nullptr;
+      off[f] = (uint64_t)(ptr - base);
     }
-    if (c->world == 1)
-      for (int f = 0; f < F; ++f) a.dst[0][f] = static_cast<uint8_t*>(recv_bufs[f]);
-  }
-  if (!c->emulated && c->world > 1) {
     a.protocol = 1;
     a.my_pad = reinterpret_cast<uint64_t*>(c->win[c->rank]);
     uint64_t* pads[kMaxWorld] = {};
     for (int q = 0; q < c->world; ++q) pads[q] = reinterpret_cast<uint64_t*>(c->peer[q]);
     for (int q = 0; q < kMaxWorld; ++q) a.peer_pad[q] = pads[q];
+    a.dst_tab = reinterpret_cast<uint8_t* const*>(a.my_pad + kDstTabSlot);
+    static const int remote_tma = [] {
+      const char* v = getenv("EARL_REMOTE_STORE");
+      return v && std::strcmp(v, "tma") == 0 ? 1 : 0;
+    }();
+    a.remote_tma = remote_tma;
+    use_begin(p, s);
     clear_stale_error();
-    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, c->timeout_ns,
+    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, F, off, c->timeout_ns,
                                          a.err, a.err_detail, s);
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1);
   }
+  use_begin(p, s);
   cudaError_t e = traced_launch(a, c, s);
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "copy launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
-  p->synced = false;
+  use_end(p, s);
   return EARL_OK;
 }
 
@@ -1006,9 +1287,11 @@ extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* se
       return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", rr);
     a.stage[rr] = static_cast<uint8_t*>(stage_bufs[r]);
   }
+  use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  use_end(p, static_cast<cudaStream_t>(stream));
   return EARL_OK;
 }
 
@@ -1046,21 +1329,19 @@ extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* 
       a.dst[c->rank][f] = static_cast<uint8_t*>(ptr);
     }
   }
+  use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "unpack launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  use_end(p, static_cast<cudaStream_t>(stream));
   return EARL_OK;
 }
 
-extern "C" earl_status_t earl_plan_messages(earl_plan_t p, int32_t rank, int64_t* send_off,
-                                            int64_t* send_bytes, int64_t* recv_off,
-                                            int64_t* recv_bytes) {
-  if (!p || !send_off || !send_bytes || !recv_off || !recv_bytes)
-    return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+namespace {
+// The staged path's per-peer byte table of `rank` from the plan's (synced) host header.
+void message_table(earl_plan_t p, int rank, int64_t* send_off, int64_t* send_bytes,
+                   int64_t* recv_off, int64_t* recv_bytes) {
   const int W = p->comm->world;
-  if (rank < 0 || rank >= W) return fail(EARL_ERR_INVALID_ARGUMENT, "rank %d outside the comm", rank);
-  earl_status_t st = plan_check(p);
-  if (st != EARL_OK) return st;
   const PlanHeader& h = p->host_hdr;
   const earl_layout_t& S = p->lay[0];
   const earl_layout_t& D = p->lay[1];
@@ -1097,7 +1378,148 @@ extern "C" earl_status_t earl_plan_messages(earl_plan_t p, int32_t rank, int64_t
       off += recv_bytes[s];
     }
   }
+}
+}  // namespace
+
+extern "C" earl_status_t earl_plan_messages(earl_plan_t p, int32_t rank, int64_t* send_off,
+                                            int64_t* send_bytes, int64_t* recv_off,
+                                            int64_t* recv_bytes) {
+  if (!p || !send_off || !send_bytes || !recv_off || !recv_bytes)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  const int W = p->comm->world;
+  if (rank < 0 || rank >= W) return fail(EARL_ERR_INVALID_ARGUMENT, "rank %d outside the comm", rank);
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  message_table(p, rank, send_off, send_bytes, recv_off, recv_bytes);
   return EARL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// K8: the staged exchange over NCCL (grouped ncclSend / ncclRecv), the comparator of the fused
+// P2P exec
+// ---------------------------------------------------------------------------------------
+
+#define NCCL_TRY(expr)                                                                     \
+  do {                                                                                     \
+    ncclResult_t r_ = (expr);                                                              \
+    if (r_ != ncclSuccess)                                                                 \
+      return fail(EARL_ERR_NCCL, "%s failed: %s (%s)", #expr, ncclGetErrorString(r_),      \
+                  ncclGetLastError(nullptr));                                              \
+  } while (0)
+
+extern "C" earl_status_t earl_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  static_assert(sizeof(ncclUniqueId) <= EARL_HANDLE_BYTES, "unique id size");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  std::memset(id_out, 0, EARL_HANDLE_BYTES);
+  std::memcpy(id_out, &id, sizeof(id));
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_init_nccl(earl_comm_t c, const void* unique_id) {
+  if (!c || !unique_id) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm: the NCCL exchange needs one process per GPU");
+  if (c->nccl) return EARL_OK;
+  DeviceGuard g(c->device);
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  if (const char* v = getenv("EARL_NCCL_MIN_CTAS")) cfg.minCTAs = atoi(v);
+  if (const char* v = getenv("EARL_NCCL_MAX_CTAS")) cfg.maxCTAs = atoi(v);
+  cfg.commName = "earl_dispatch";
+  NCCL_TRY(ncclCommInitRankConfig(&c->nccl, c->world, id, c->rank, &cfg));
+  const char* reg = getenv("EARL_NCCL_REGISTER");
+  c->nccl_register = reg && atoi(reg) != 0;
+  return EARL_OK;
+}
+
+namespace {
+// Grow stage buffer k (0 = send, 1 = receive) of the comm to at least `bytes`.
+earl_status_t nccl_stage(earl_comm* c, int k, uint64_t bytes) {
+  if (bytes < 16) bytes = 16;
+  if (c->nst[k] && c->nst_bytes[k] >= bytes) return EARL_OK;
+  CUDA_TRY(cudaDeviceSynchronize());  // the old buffer may still be in use
+  if (c->nreg[k]) { ncclCommDeregister(c->nccl, c->nreg[k]); c->nreg[k] = nullptr; }
+  if (c->nst[k]) {
+    if (c->nccl_register) ncclMemFree(c->nst[k]);
+    else cudaFree(c->nst[k]);
+    c->nst[k] = nullptr;
+  }
+  bytes = (bytes + (1ull << 21) - 1) & ~((1ull << 21) - 1);
+  if (c->nccl_register) {
+    NCCL_TRY(ncclMemAlloc(&c->nst[k], bytes));
+    NCCL_TRY(ncclCommRegister(c->nccl, c->nst[k], bytes, &c->nreg[k]));
+  } else {
+    CUDA_TRY(cudaMalloc(&c->nst[k], bytes));
+  }
+  c->nst_bytes[k] = bytes;
+  return EARL_OK;
+}
+}  // namespace
+
+namespace {
+// The grouped send/recv of this rank's messages (the plan's host header must be current).
+earl_status_t exchange_impl(earl_plan_t p, const void* send_stage, void* recv_stage, void* stream) {
+  earl_comm* c = p->comm;
+  const int W = c->world;
+  int64_t so[kMaxWorld], sb[kMaxWorld], ro[kMaxWorld], rb[kMaxWorld];
+  message_table(p, c->rank, so, sb, ro, rb);
+  int64_t need_s = 0, need_r = 0;
+  for (int q = 0; q < W; ++q) {
+    if (sb[q]) need_s = std::max(need_s, so[q] + sb[q]);
+    if (rb[q]) need_r = std::max(need_r, ro[q] + rb[q]);
+  }
+  if ((need_s && !send_stage) || (need_r && !recv_stage))
+    return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer is NULL");
+  DeviceGuard g(c->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint8_t* sp = static_cast<const uint8_t*>(send_stage);
+  uint8_t* rp = static_cast<uint8_t*>(recv_stage);
+  use_begin(p, s);
+  NCCL_TRY(ncclGroupStart());
+  for (int q = 0; q < W; ++q) {
+    if (sb[q]) NCCL_TRY(ncclSend(sp + so[q], (size_t)sb[q], ncclUint8, q, c->nccl, s));
+    if (rb[q]) NCCL_TRY(ncclRecv(rp + ro[q], (size_t)rb[q], ncclUint8, q, c->nccl, s));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  use_end(p, s);
+  return EARL_OK;
+}
+}  // namespace
+
+extern "C" earl_status_t earl_dispatch_exchange(earl_plan_t p, const void* send_stage,
+                                                void* recv_stage, void* stream) {
+  NvtxRange nvtx("earl_dispatch_exchange");
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (!p->comm->nccl) return fail(EARL_ERR_INVALID_ARGUMENT, "earl_comm_init_nccl was not called");
+  earl_status_t st = plan_check(p);  // the byte table is host data: NCCL takes host sizes
+  if (st != EARL_OK) return st;
+  return exchange_impl(p, send_stage, recv_stage, stream);
+}
+
+extern "C" earl_status_t earl_dispatch_exec_staged(earl_plan_t p, const void* const* send_bufs,
+                                                   void* const* recv_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_exec_staged");
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  earl_comm* c = p->comm;
+  if (!c->nccl) return fail(EARL_ERR_INVALID_ARGUMENT, "earl_comm_init_nccl was not called");
+  earl_status_t st = plan_check(p);
+  if (st != EARL_OK) return st;
+  int64_t so[kMaxWorld], sb[kMaxWorld], ro[kMaxWorld], rb[kMaxWorld];
+  message_table(p, c->rank, so, sb, ro, rb);
+  int64_t need_r = 0;
+  for (int q = 0; q < c->world; ++q) need_r += rb[q];
+  int gs, ks, ts;
+  const int64_t need_s = coords(p->lay[0], c->rank, &gs, &ks, &ts) ? p->host_hdr.stage_bytes_shard[gs * p->lay[0].sp + ks] : 0;
+  DeviceGuard g(c->device);
+  if ((st = nccl_stage(c, 0, (uint64_t)need_s)) != EARL_OK) return st;
+  if ((st = nccl_stage(c, 1, (uint64_t)need_r)) != EARL_OK) return st;
+  void* stage_s[1] = {c->nst[0]};
+  void* stage_r[1] = {c->nst[1]};
+  if ((st = earl_dispatch_pack(p, send_bufs, stage_s, stream)) != EARL_OK) return st;
+  if ((st = exchange_impl(p, c->nst[0], c->nst[1], stream)) != EARL_OK) return st;
+  return earl_dispatch_unpack(p, stage_r, recv_bufs, stream);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1181,9 +1603,13 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   a.ws = static_cast<AggWork*>(p->agg_ws);
   a.win = reinterpret_cast<AggWindow*>(a.ws + 1);
   a.win_cap = p->agg_cap;
+  use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_returns(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "returns launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  const bool synced = p->synced;
+  use_end(p, static_cast<cudaStream_t>(stream));
+  p->synced = synced;  // T is unchanged (a CAPACITY latch is read by the next synchronising call)
   return EARL_OK;
 }
 
@@ -1208,8 +1634,12 @@ extern "C" earl_status_t earl_advantages(earl_plan_t p, const double* stats, flo
     const earl_layout_t& S = p->lay[0];
     tokens = p->comm->emulated ? p->host_hdr.T * S.tp : (p->host_hdr.T + S.dp - 1) / S.dp;
   }
+  use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = launch_advantages(a, p->comm->sm_count, tokens, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "advantages launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
+  const bool synced = p->synced;
+  use_end(p, static_cast<cudaStream_t>(stream));
+  p->synced = synced;
   return EARL_OK;
 }

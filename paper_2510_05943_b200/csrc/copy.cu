@@ -54,37 +54,69 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
-// Signal every peer (slot `slot_base + me` of its pad), then wait for every peer's signal in
-// my pad.  Lane p handles peer p.  Returns the mask of peers that timed out.
+// Signal every peer (store `value` into slot `slot_base + me` of its pad), then wait until every
+// peer's slot in my pad holds at least `want`.  Lane p handles peer p.  Returns the mask of peers
+// that timed out; *got (lane p) is the value peer p left in my pad.
 __device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                    int slot_base, uint64_t epoch, uint64_t timeout_ns) {
+                                    int slot_base, uint64_t value, uint64_t want,
+                                    uint64_t timeout_ns, uint64_t* got) {
   const int lane = threadIdx.x & 31;
-  if (lane < world && lane != me) st_release_sys(peer_pad[lane] + slot_base + me, epoch);
+  if (lane < world && lane != me) st_release_sys(peer_pad[lane] + slot_base + me, value);
   unsigned missing = 0;
+  uint64_t v = want;
   if (lane < world && lane != me) {
     const uint64_t t0 = globaltimer();
-    while (ld_acquire_sys(my_pad + slot_base + lane) < epoch) {
+    while ((v = ld_acquire_sys(my_pad + slot_base + lane)) < want) {
       if (globaltimer() - t0 > timeout_ns) { missing = 1u << lane; break; }
       __nanosleep(64);
     }
   }
+  if (got) *got = v;
   return __reduce_or_sync(kFull, missing);
 }
 
 // The exec epoch lives in this rank's pad (slot kEpochSlot, written only by this rank): the
 // entry barrier of every exec advances it and the copy kernel that follows on the stream reads
 // it, so an exec captured into a CUDA graph gets a fresh epoch on every replay.
+//
+// Before signalling, this rank publishes where its receive buffers are (window offsets, one per
+// field) in its own pad; after acquiring peer p's ready flag, lane p reads p's published offsets
+// and resolves p's destination bases in this rank's address space (its mapping of p's window).
+// Every rank therefore writes at the offsets the DESTINATION chose -- a rank that receives
+// nothing (or is in no destination layout) may pass NULLs without silencing its own sends.
+// Ordering: a peer reads these offsets only after acquiring this epoch's ready flag, and this
+// rank rewrites them only in its next exec, after every peer released its done flag (i.e.
+// finished reading).
 __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world, int me,
-                                     uint64_t timeout_ns, int32_t* err, int32_t* err_detail) {
+                                     int n_fields, RecvOffsets offs, uint64_t timeout_ns,
+                                     int32_t* err, int32_t* err_detail) {
+  const int lane = threadIdx.x & 31;
   uint64_t epoch = 0;
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     epoch = my_pad[kEpochSlot] + 1;
     my_pad[kEpochSlot] = epoch;
   }
   epoch = __shfl_sync(kFull, epoch, 0);
+  if (lane < kMaxFields) my_pad[kOffSlot + lane] = lane < n_fields ? offs.v[lane] : kNoOffset;
+  __threadfence_system();
+  __syncwarp();
   delay_inject(1);
-  const unsigned miss = signal_and_wait(my_pad, pads.p, world, me, kReadySlot, epoch, timeout_ns);
-  if (threadIdx.x == 0 && miss) {
+  const unsigned miss = signal_and_wait(my_pad, pads.p, world, me, kReadySlot, epoch, epoch,
+                                        timeout_ns, nullptr);
+  // lane p: peer p's (or, for p == me, this rank's own) destination bases
+  uint64_t* tab = my_pad + kDstTabSlot;
+  if (lane < kMaxWorld) {
+    for (int f = 0; f < kMaxFields; ++f) {
+      uint64_t o = kNoOffset;
+      if (lane < world && f < n_fields && !(miss >> lane & 1)) {
+        o = lane == me ? offs.v[f]
+                       : *reinterpret_cast<volatile const uint64_t*>(pads.p[lane] + kOffSlot + f);
+      }
+      tab[lane * kMaxFields + f] =
+          o == kNoOffset ? 0ull : reinterpret_cast<uint64_t>(reinterpret_cast<uint8_t*>(pads.p[lane]) + o);
+    }
+  }
+  if (lane == 0 && miss) {
     if (atomicCAS(err, 0, EARL_ERR_TIMEOUT) == 0) *err_detail = (int32_t)miss;
   }
 }
@@ -251,6 +283,7 @@ struct Walker {
   uint32_t R;
   uint64_t prem;
   int pf, pd0;
+  uint8_t* const* dt;  // the launch's destination field bases [kMaxWorld][kMaxFields] (smem)
 
   __device__ __forceinline__ void set_block(const View& v, int bb) {
     b = bb;
@@ -358,15 +391,15 @@ struct Walker {
           R = 1;
           pd0 = d0;
         } else if (unpack_rank) {
-          uint8_t* base = a.dst[a.me][f];
+          uint8_t* base = dt[a.me * kMaxFields + f];
           pdst = base + dst_tok * (int64_t)Bf + (int64_t)u0;
           R = base != nullptr ? 1 : 0;
           pd0 = a.me;
         } else {
           R = 0;
-          uint8_t* base0 = a.dst[d0][f];
+          uint8_t* base0 = dt[d0 * kMaxFields + f];
           for (int td = ts; td < a.tp_d; td += a.tp_s)
-            if (a.dst[d0 + (td - ts)][f] != nullptr) ++R;
+            if (dt[(d0 + (td - ts)) * kMaxFields + f] != nullptr) ++R;
           pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
           if (base0 == nullptr) R = 0;
           pd0 = d0;
@@ -449,15 +482,15 @@ __device__ __forceinline__ bool fill_stage(const CopyArgs& a, const View& v, Wal
 // compile-time constant so the replica pointers stay in registers and the realign loop is
 // ~12 instructions per 512 B (a runtime-R loop cost ~100: profiles/r01_c5lt_note.txt).
 template <int R>
-__device__ __forceinline__ void store_sub_r(const CopyArgs& a, const SubDesc& S, uint8_t* stage,
-                                            int lane) {
+__device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* dt, const SubDesc& S,
+                                            uint8_t* stage, int lane) {
   const uint32_t len = S.len;
   const uint8_t* sm = stage + S.so + S.off;
   uint8_t* dp[R];
   dp[0] = S.dst0;
 #pragma unroll
   for (int r = 1; r < R; ++r)
-    dp[r] = S.dst0 + (a.dst[S.d0 + r * a.tp_s][S.f] - a.dst[S.d0][S.f]);
+    dp[r] = S.dst0 + (dt[(S.d0 + r * a.tp_s) * kMaxFields + S.f] - dt[S.d0 * kMaxFields + S.f]);
   uint32_t head = (16 - (uint32_t)((uintptr_t)S.dst0 & 15)) & 15;
   if (head > len) head = len;
   if (lane < (int)head) {
@@ -471,12 +504,13 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, const SubDesc& S,
     const uint32_t smo = S.so + S.off + head;
     if ((smo & 15) == 0) {
       // local replicas: one bulk TMA store each; replicas on a peer GPU (multi-process comm)
-      // are written by the warp with 16-B stores over NVLink
+      // are written by the warp with 16-B stores over NVLink, or (EARL_REMOTE_STORE=tma) by
+      // bulk TMA stores to the peer address as well
       bool remote[R];
       bool any_remote = false;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        remote[r] = a.mode != kPack && a.me >= 0 && (S.d0 + r * a.tp_s) != a.me;
+        remote[r] = !a.remote_tma && a.mode != kPack && a.me >= 0 && (S.d0 + r * a.tp_s) != a.me;
         any_remote |= remote[r];
       }
       if (lane == 0) {
@@ -518,17 +552,17 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, const SubDesc& S,
   }
 }
 
-__device__ __forceinline__ void store_sub(const CopyArgs& a, const SubDesc& S, uint8_t* stage,
-                                          int lane) {
+__device__ __forceinline__ void store_sub(const CopyArgs& a, uint8_t* const* dt, const SubDesc& S,
+                                          uint8_t* stage, int lane) {
   switch (S.R) {
-    case 1: store_sub_r<1>(a, S, stage, lane); break;
-    case 2: store_sub_r<2>(a, S, stage, lane); break;
-    case 3: store_sub_r<3>(a, S, stage, lane); break;
-    case 4: store_sub_r<4>(a, S, stage, lane); break;
-    case 5: store_sub_r<5>(a, S, stage, lane); break;
-    case 6: store_sub_r<6>(a, S, stage, lane); break;
-    case 7: store_sub_r<7>(a, S, stage, lane); break;
-    default: store_sub_r<8>(a, S, stage, lane); break;
+    case 1: store_sub_r<1>(a, dt, S, stage, lane); break;
+    case 2: store_sub_r<2>(a, dt, S, stage, lane); break;
+    case 3: store_sub_r<3>(a, dt, S, stage, lane); break;
+    case 4: store_sub_r<4>(a, dt, S, stage, lane); break;
+    case 5: store_sub_r<5>(a, dt, S, stage, lane); break;
+    case 6: store_sub_r<6>(a, dt, S, stage, lane); break;
+    case 7: store_sub_r<7>(a, dt, S, stage, lane); break;
+    default: store_sub_r<8>(a, dt, S, stage, lane); break;
   }
 }
 
@@ -541,7 +575,12 @@ template <int WARPS, int STAGES, int CHUNK>
 __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_constant__ CopyArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned s_last;
+  __shared__ uint8_t* s_dst[kMaxWorld * kMaxFields];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // destination field bases: the kernel parameter, or (multi-process exec) the table the entry
+  // barrier resolved from every destination's published offsets
+  for (int k = threadIdx.x; k < kMaxWorld * kMaxFields; k += WARPS * 32)
+    s_dst[k] = a.protocol ? a.dst_tab[k] : a.dst[k / kMaxFields][k % kMaxFields];
   uint8_t* data = smem + (size_t)w * STAGES * CHUNK;
   StageDesc* desc = reinterpret_cast<StageDesc*>(smem + (size_t)WARPS * STAGES * CHUNK) + w * STAGES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + (size_t)WARPS * STAGES * CHUNK +
@@ -550,7 +589,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
-  __syncwarp();
+  __syncthreads();
   delay_inject(2);
   const PlanHeader* h = a.hdr;
   if (h->err == 0) {
@@ -565,6 +604,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       if (a.trace) t_start = globaltimer();
       build_view(a, c0, v);
       wk.setup(a, v, c0, nwarps);
+      wk.dt = s_dst;
       const uint64_t total = wk.total;
       // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
       uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
@@ -585,7 +625,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       mbar_wait(&bar[st], (uint32_t)((c / STAGES) & 1));
       uint8_t* stage = data + (size_t)st * CHUNK;
       const uint32_t nsub = desc[st].n;
-      for (uint32_t k = 0; k < nsub; ++k) store_sub(a, desc[st].sub[k], stage, lane);
+      for (uint32_t k = 0; k < nsub; ++k) store_sub(a, s_dst, desc[st].sub[k], stage, lane);
       if (lane == 0) { bulk_commit(); bulk_wait_read1(); }
       __syncwarp();
       int ok = 0;
@@ -628,11 +668,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
     if (s_last && threadIdx.x < 32) {
       if (threadIdx.x == 0) *a.done_ctr = 0;
       __threadfence_system();
+      // done = 2 * epoch + failed: a rank whose copies were skipped (its entry barrier timed out,
+      // or its plan latched an error) says so, and every peer latches an error instead of
+      // returning with that rank's contribution missing
       const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(a.my_pad + kEpochSlot);
-      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.world, a.me, kDoneSlot, epoch,
-                                            a.timeout_ns);
-      if (threadIdx.x == 0 && miss) {
-        if (atomicCAS(a.err, 0, EARL_ERR_TIMEOUT) == 0) *a.err_detail = (int32_t)miss;
+      const uint64_t failed = *reinterpret_cast<volatile const int32_t*>(a.err) != 0 ? 1 : 0;
+      uint64_t got = 0;
+      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.world, a.me, kDoneSlot,
+                                            2 * epoch + failed, 2 * epoch, a.timeout_ns, &got);
+      const int lane = threadIdx.x;
+      const unsigned bad = __ballot_sync(kFull, lane < a.world && lane != a.me &&
+                                                    !(miss >> lane & 1) && got == 2 * epoch + 1);
+      if (lane == 0 && (miss | bad)) {
+        if (atomicCAS(a.err, 0, EARL_ERR_TIMEOUT) == 0) *a.err_detail = (int32_t)(miss | bad << 8);
       }
     }
   }
@@ -661,13 +709,14 @@ cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
 // 16 KB (3 CTAs per SM) 0.933-0.940 of peak on c3 against 0.920 for 4 warps x 4 x 8 KB (1 CTA)
 // on the same box, c4 1.00, c2-lpt 0.99; otherwise the realign path needs the issue slots of 8
 // warps (0.93 vs 0.63 on the long-tail scalar sweep).  EARL_COPY_CFG forces a shape for tuning.
-cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s) {
+// shape >= 100: the shape id shape - 100, forced by the caller (multi-process P2P override).
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t s) {
   static int forced = -2;
   if (forced == -2) {
     const char* e = getenv("EARL_COPY_CFG");
     forced = e ? atoi(e) : -1;
   }
-  const int cfg = forced >= 0 ? forced : (congruent_heavy ? 14 : 3);
+  const int cfg = shape >= 100 ? shape - 100 : forced >= 0 ? forced : (shape ? 14 : 3);
   switch (cfg) {
     case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
     case 2: return launch_cfg<4, 4, 8192>(a, sm_count, s);
@@ -683,11 +732,14 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cu
 }
 
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
-                                 cudaStream_t s) {
+                                 int n_fields, const uint64_t* recv_off, uint64_t timeout_ns,
+                                 int32_t* err, int32_t* err_detail, cudaStream_t s) {
   PeerPads pads;
   for (int p = 0; p < kMaxWorld; ++p) pads.p[p] = peer_pad[p];
-  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, timeout_ns, err, err_detail);
+  RecvOffsets offs;
+  for (int f = 0; f < kMaxFields; ++f) offs.v[f] = f < n_fields ? recv_off[f] : kNoOffset;
+  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, n_fields, offs, timeout_ns, err,
+                                        err_detail);
   return cudaGetLastError();
 }
 

@@ -101,6 +101,9 @@ struct PlanArgs {
 struct PeerPads {
   uint64_t* p[kMaxWorld];
 };
+struct RecvOffsets {
+  uint64_t v[kMaxFields];   // window-relative receive offsets of this rank (kNoOffset = NULL)
+};
 
 enum CopyMode { kDirect = 0, kPack = 1, kUnpack = 2 };
 
@@ -111,6 +114,7 @@ struct CopyArgs {
   int32_t nts;             // min(tp_src, tp_dst)
   int32_t rank0_s, tp_s, rank0_d, tp_d, sp_d, n_dst_shards, n_src_shards;
   int32_t protocol;        // 1: multi-process fused exec (epoch release / acquire at the end)
+  int32_t remote_tma;      // 1: peer replicas by bulk TMA stores too (EARL_REMOTE_STORE=tma)
   const uint8_t* recv_stage;                  // unpack on a real rank: received messages
   uint32_t Bf[kMaxFields];
   uint64_t Bpre[kMaxFields + 1];  // prefix of Bf
@@ -125,6 +129,9 @@ struct CopyArgs {
   unsigned int* done_ctr;                     // device counter for the last-CTA pattern
   uint64_t* my_pad;                           // this rank's signal pad (local)
   uint64_t* peer_pad[kMaxWorld];              // peers' signal pads (mapped)
+  uint8_t* const* dst_tab;                    // protocol 1: [kMaxWorld][kMaxFields] destination
+                                              // field bases resolved by the entry barrier from
+                                              // every destination's published window offsets
   uint64_t timeout_ns;
   int32_t* err;                               // where to latch TIMEOUT (plan header)
   int32_t* err_detail;
@@ -134,9 +141,44 @@ struct CopyArgs {
 };
 
 // signal pad slots (uint64 each): [0, 8) ready flags written by peer p at p; [8, 16) done flags
+// (2 * epoch + failed: a peer that skipped its copies says so); [16] this rank's exec epoch;
+// [32, 48) this rank's published receive offsets (one per field, window-relative, kNoOffset =
+// NULL), read by every peer after it acquires this rank's ready flag; [64, 192) the destination
+// table [kMaxWorld][kMaxFields] this rank's entry barrier resolved from the peers' offsets.
 constexpr int kReadySlot = 0;
 constexpr int kDoneSlot = 8;
 constexpr int kEpochSlot = 16;  // this rank's exec epoch (written by its own entry barrier)
+constexpr int kLensEpochSlot = 17;  // this rank's length-gather epoch (a1)
+constexpr int kLensSlot = 24;       // [24, 32): length-gather flags written by peer p at p
+constexpr int kOffSlot = 32;
+constexpr int kDstTabSlot = 64;
+constexpr uint64_t kNoOffset = ~0ull;
+
+// step a1 (lengths.cu): the device gather of the global length vector
+struct LensArgs {
+  int32_t world, me, emulated;
+  int64_t cap;                      // sequences per gather buffer (multi-process)
+  int64_t total;                    // sum of counts
+  int64_t counts[kMaxWorld];
+  int64_t start[kMaxWorld];         // exclusive prefix of counts
+  const int32_t* local;             // this rank's lengths (multi-process)
+  const int32_t* src[kMaxWorld];    // every rank's lengths (emulated)
+  int32_t* out;                     // [total]
+  uint64_t* my_pad;
+  uint64_t* peer_pad[kMaxWorld];    // window bases (pad first, then the gather areas)
+  unsigned int* ctr;                // last-CTA counter (comm-owned)
+  int32_t* err;                     // comm-owned [2]: status, detail (missing-peer mask)
+  uint64_t timeout_ns;
+};
+
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // NEXT-2 (aggregate.cu): returns / advantages on the source ranks (SP = 1)
 // returns_kernel look-back state: one descriptor per token window of a source rank.  Each word
@@ -210,10 +252,12 @@ int64_t returns_windows(int64_t tokens);
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
-cudaError_t launch_copy(const CopyArgs& a, int sm_count, int congruent_heavy, cudaStream_t s);
+cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
-                                 cudaStream_t s);
+                                 int n_fields, const uint64_t* recv_off, uint64_t timeout_ns,
+                                 int32_t* err, int32_t* err_detail, cudaStream_t s);
+cudaError_t launch_gather_lengths(const LensArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t s);
 cudaError_t launch_local_meta(const PlanArgs& a, int rank_g, int rank_k, int32_t* cu, int64_t* ids,
                               int32_t* tok_start, cudaStream_t s);
 

@@ -66,6 +66,15 @@ class EmulatedDispatch:
         self._dst = layout_for_device(dst, self.device)
         return self.comm.plan(self._src, self._dst, lens, fields, stream)
 
+    def allgather_lens(self, local_lens, counts, out=None, stream=None):
+        """Step a1 on the emulated comm: local_lens[r] = rank r's lengths (None where counts[r]
+        is 0), concatenated rank-major on the device into `out` (earl_allgather_lengths)."""
+        total = int(sum(counts))
+        if out is None:
+            out = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+        self.comm.allgather_lengths(counts, local_lens, out, stream)
+        return out[:total]
+
     def alloc_recv(self, plan, fields):
         """Per-rank, per-field uint8 receive tensors sized from the plan (host sync)."""
         st = plan.stats()
@@ -113,6 +122,19 @@ def allgather_lengths(local_lens: torch.Tensor, group=None):
     return torch.cat([allp[r][: counts[r]] for r in range(world)]), counts
 
 
+def rank_counts(src: dict, world: int):
+    """Per-rank sequence counts of a rollout (GIVEN_COUNTS) source layout, in the rank-major
+    global order of step a1: rank (g, 0, 0) contributes group g's counts[g] lengths, every other
+    rank (SP chunks, TP replicas, ranks outside the layout) none."""
+    if src.get("assign") != "given_counts":
+        raise ValueError("the device length gather needs a GIVEN_COUNTS source layout")
+    out = [0] * int(world)
+    sp, tp, r0 = int(src.get("sp", 1)), int(src.get("tp", 1)), int(src.get("rank0", 0))
+    for g, c in enumerate(src["counts"]):
+        out[r0 + g * sp * tp] = int(c)
+    return out
+
+
 def max_over_ranks(values, group=None):
     """Element-wise max of a list of floats over the ranks (timing: the slowest rank decides)."""
     import torch.distributed as dist
@@ -139,9 +161,19 @@ class Dispatcher:
             dist.all_gather_object(handles, self.comm.export_handle(), group=group)
             self.comm.import_peers(handles)
 
-    def allgather_lens(self, local_lens: torch.Tensor):
-        """Step a1 (see allgather_lengths) on this dispatcher's process group; gloo groups
-        (tests) run the collective on host tensors."""
+    def allgather_lens(self, local_lens: torch.Tensor, counts=None, out=None, stream=None):
+        """Step a1.  With `counts` (per-rank sequence counts, the same on every rank: see
+        rank_counts) the library gathers on the device (earl_allgather_lengths: one kernel over
+        the peer windows, no host synchronisation, graph-capturable) and returns (out, counts).
+        Without, the counts are not known in advance: two all-gathers over the process group
+        (see allgather_lengths; gloo groups run it on host tensors)."""
+        if counts is not None:
+            total = int(sum(counts))
+            if out is None:
+                out = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
+            loc = local_lens if local_lens is not None and local_lens.numel() else None
+            self.comm.allgather_lengths(counts, [loc], out, stream)
+            return out[:total], list(counts)
         backend = self.dist.get_backend(self.group)
         dev = self.device if backend == "nccl" else torch.device("cpu")
         glob, counts = allgather_lengths(local_lens.to(dev), self.group)
@@ -227,13 +259,31 @@ class Dispatcher:
         for p, hbuf in host_recv.items():
             recv_stage[ro[p]:ro[p] + rb[p]].copy_(hbuf)
 
+    def init_nccl(self):
+        """K8: the library's own NCCL communicator over this group's ranks (rank 0 draws the
+        unique id, the process group broadcasts it).  Needs one GPU per rank (NCCL rejects two
+        ranks on one device)."""
+        if getattr(self, "_nccl", False):
+            return
+        obj = [earl.nccl_unique_id() if self.rank == 0 else None]
+        self.dist.broadcast_object_list(obj, src=0, group=self.group)
+        self.comm.init_nccl(obj[0])
+        self._nccl = True
+
     def exec_staged(self, plan, send_bufs, recv_bufs, send_stage=None, recv_stage=None, msgs=None,
                     stream=None):
         """pack (this rank's records) -> grouped send/recv -> unpack (this rank's arrays).
 
         Without an explicit `msgs` the per-peer byte table is read from the plan on every call
         -- a device->host synchronisation that the NCCL path inherently needs (its sizes are
-        host arguments), unlike the fused exec.  Stage buffers grow on demand and are cached."""
+        host arguments), unlike the fused exec.  Stage buffers grow on demand and are cached.
+
+        After init_nccl() the whole staged path runs in the library (earl_dispatch_exec_staged:
+        pack, grouped ncclSend / ncclRecv, unpack); otherwise the exchange goes through the
+        process group (gloo in the one-GPU tests: host-staged)."""
+        if getattr(self, "_nccl", False) and send_stage is None and recv_stage is None:
+            plan.exec_staged(send_bufs, recv_bufs, stream)
+            return
         if msgs is None:
             msgs = plan.messages(self.rank)
         if send_stage is None or recv_stage is None:
@@ -254,28 +304,13 @@ class Dispatcher:
 # per-sequence fields (reading n4)
 # ---------------------------------------------------------------------------------------
 
-def fold_layout(lay: dict, groups_dev) -> dict:
-    """The layout a per-sequence field travels on: the token plan's groups as EXPLICIT, its SP
-    degree folded into TP (rank(g,k,t) = rank0 + g*SP*TP + (k*TP + t) is rank (g, 0, k*TP+t) of
-    the folded layout), so every SP rank and TP replica of a group holds one record per sequence."""
-    out = dict(lay)
-    out.update(sp=1, tp=int(lay.get("sp", 1)) * int(lay.get("tp", 1)), assign="explicit",
-               counts=None, group_of_seq=None, group_of_seq_dev=groups_dev, sp_split="block",
-               sp_min_len=0)
-    return out
-
-
 def plan_seq_fields(comm, token_plan, src, dst, sfields, device, stream=None):
-    """Plan the routing of per-sequence fields along `token_plan`: unit lengths (one record per
-    sequence) over the folded layouts with the token plan's own group assignment."""
-    n = token_plan.n_seqs
-    gs = torch.empty(max(n, 1), dtype=torch.int32, device=device)
-    gd = torch.empty(max(n, 1), dtype=torch.int32, device=device)
-    token_plan.groups(gs, gd, stream)
-    ones = torch.ones(n, dtype=torch.int32, device=device)
-    sp = comm.plan(fold_layout(src, gs), fold_layout(dst, gd), ones, sfields, stream)
-    sp._keep = (gs, gd, ones)
-    return sp
+    """Plan the routing of per-sequence fields along `token_plan` (reading n4): the library's
+    earl_plan_seq_fields (unit lengths over the token plan's layouts with SP folded into TP and
+    its groups pinned as EXPLICIT, built on the device).  comm / src / dst / device are accepted
+    for call-site compatibility; the token plan carries them."""
+    from .earl import Plan
+    return Plan.seq_fields(token_plan, sfields, stream)
 
 
 def distributed_advantages(dispatcher, plan, gamma, rewards, mask, returns, adv, eps=1e-8,

@@ -40,6 +40,9 @@ EXPORTED = [
     "earl_dispatch_pack", "earl_dispatch_unpack", "earl_plan_messages", "earl_returns", "earl_advantages", "earl_status_string", "earl_last_error",
     "earl_abi_version", "earl_kernel_launch_count", "earl_speedup_pct", "earl_policy_build",
     "earl_policy_table", "earl_policy_select", "earl_policy_destroy", "earl_plan_mean_length",
+    "earl_allgather_lengths", "earl_comm_check", "earl_comm_peer_mask",
+    "earl_nccl_unique_id", "earl_comm_init_nccl", "earl_dispatch_exchange", "earl_dispatch_exec_staged",
+    "earl_plan_seq_fields",
 ]
 
 
@@ -117,6 +120,14 @@ def lib():
         "earl_comm_reset_alloc": [vp],
         "earl_comm_info": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)],
         "earl_comm_destroy": [vp],
+        "earl_allgather_lengths": [vp, vp, pvp, vp, vp],
+        "earl_comm_check": [vp, vp],
+        "earl_comm_peer_mask": [vp, C.POINTER(C.c_uint32)],
+        "earl_nccl_unique_id": [vp],
+        "earl_comm_init_nccl": [vp, vp],
+        "earl_dispatch_exchange": [vp, vp, vp, vp],
+        "earl_dispatch_exec_staged": [vp, pvp, pvp, vp],
+        "earl_plan_seq_fields": [vp, C.POINTER(Field), i32, vp, pvp],
         "earl_dispatch_plan": [vp, C.POINTER(Layout), C.POINTER(Layout), vp, i64,
                                C.POINTER(Field), i32, vp, pvp],
         "earl_plan_sync": [vp],
@@ -253,6 +264,30 @@ class Comm:
     def reset_alloc(self):
         check(lib().earl_comm_reset_alloc(self.h))
 
+    def allgather_lengths(self, counts, local_lens, global_lens, stream=None):
+        """earl_allgather_lengths (step a1): counts = per-rank sequence counts (host, every rank
+        the same); local_lens = [this rank's int32 tensor] (emulated: one per rank, None where
+        the count is 0); global_lens = int32 device tensor of sum(counts) elements (output)."""
+        cnt = np.ascontiguousarray(counts, dtype=np.int64)
+        assert cnt.size == self.world
+        check(lib().earl_allgather_lengths(self.h, cnt.ctypes.data, _ptr_array(local_lens),
+                                           _ptr(global_lens) or None, _stream(stream)))
+
+    def init_nccl(self, unique_id: bytes):
+        """earl_comm_init_nccl (collective): the staged exchange's NCCL communicator."""
+        buf = (C.c_uint8 * EARL_HANDLE_BYTES).from_buffer_copy(unique_id)
+        check(lib().earl_comm_init_nccl(self.h, buf))
+
+    def peer_mapped(self, p: int) -> bool:
+        """earl_comm_peer_mask: is peer p's window mapped into this process?"""
+        m = C.c_uint32()
+        check(lib().earl_comm_peer_mask(self.h, C.byref(m)))
+        return bool(m.value >> int(p) & 1)
+
+    def check(self, stream=None):
+        """earl_comm_check: synchronise `stream`, raise a device-latched comm error."""
+        check(lib().earl_comm_check(self.h, _stream(stream)))
+
     def plan(self, src, dst, seq_lens, fields, stream=None) -> "Plan":
         return Plan(self, src, dst, seq_lens, fields, stream)
 
@@ -271,6 +306,23 @@ class Comm:
 class Plan:
     """earl_plan_t produced by earl_dispatch_plan (device-side planner, no host sync)."""
 
+    @classmethod
+    def seq_fields(cls, token_plan: "Plan", sfields, stream=None) -> "Plan":
+        """earl_plan_seq_fields (reading n4): per-sequence fields routed along token_plan."""
+        p = cls.__new__(cls)
+        p.comm = token_plan.comm
+        p.fields = list(sfields)
+        p._fa = make_fields(p.fields)
+        h = C.c_void_p()
+        check(lib().earl_plan_seq_fields(token_plan.h, p._fa, len(p.fields), _stream(stream),
+                                         C.byref(h)))
+        p.h = h
+        p.n_seqs = token_plan.n_seqs
+        p._seq_lens = None
+        p._groups_keepalive = None
+        p._parent = token_plan  # the library keeps the token plan alive; so does the binding
+        return p
+
     def __init__(self, comm: Comm, src, dst, seq_lens, fields, stream=None):
         self.comm = comm
         self.fields = list(fields)
@@ -284,12 +336,17 @@ class Plan:
         self.h = h
         self.n_seqs = n
         self._seq_lens = seq_lens  # keep alive until the planner ran
+        # EXPLICIT group vectors are re-read by every replan: they live as long as the plan
+        self._groups_keepalive = (src.get("group_of_seq_dev"), dst.get("group_of_seq_dev"))
 
-    def replan(self, seq_lens, stream=None):
-        """Re-run the device planner for new lengths (same N) into this plan's memory."""
-        assert int(seq_lens.numel()) == self.n_seqs
+    def replan(self, seq_lens=None, stream=None):
+        """Re-run the device planner for new lengths (same N) into this plan's memory (a
+        per-sequence field plan takes no lengths: it re-reads its token plan's groups)."""
+        if seq_lens is not None:
+            assert int(seq_lens.numel()) == self.n_seqs
         check(lib().earl_plan_replan(self.h, _ptr(seq_lens) or None, _stream(stream)))
-        self._seq_lens = seq_lens
+        if seq_lens is not None:
+            self._seq_lens = seq_lens
 
     # -- queries (host-synchronising) --
     def sync(self):
@@ -354,6 +411,16 @@ class Plan:
         """earl_dispatch_exec_src: only source rank src_rank's records."""
         s, r = _ptr_array(send_bufs), _ptr_array(recv_bufs)
         check(lib().earl_dispatch_exec_src(self.h, int(src_rank), s, r, _stream(stream)))
+
+    def exchange(self, send_stage, recv_stage, stream=None):
+        """earl_dispatch_exchange: grouped ncclSend / ncclRecv of this rank's messages."""
+        check(lib().earl_dispatch_exchange(self.h, _ptr(send_stage) or None, _ptr(recv_stage) or None,
+                                           _stream(stream)))
+
+    def exec_staged(self, send_bufs, recv_bufs, stream=None):
+        """earl_dispatch_exec_staged: pack + NCCL exchange + unpack (library stage buffers)."""
+        s, r = _ptr_array(send_bufs), _ptr_array(recv_bufs)
+        check(lib().earl_dispatch_exec_staged(self.h, s, r, _stream(stream)))
 
     def pack(self, send_bufs, stage_bufs, stream=None):
         s, t = _ptr_array(send_bufs), _ptr_array(stage_bufs)
@@ -431,6 +498,12 @@ class Policy:
             self.destroy()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * EARL_HANDLE_BYTES)()
+    check(lib().earl_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def kernel_launch_count() -> int:

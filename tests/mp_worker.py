@@ -68,8 +68,23 @@ def gpu_main(rank, world, port, q, case):
         D = Dispatcher(window_bytes=T * W.bytes_per_token(fields) + (1 << 16), device=0)
         mine = [torch.from_numpy(a).cuda() if a.size else None for a in src_arrays.get(rank, [])] \
             if rank in src_arrays else [None] * len(fields)
-        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        # step a1: every rank holds only its own block of the lengths (the rollout's counts when
+        # the source layout is GIVEN_COUNTS, else near-equal blocks) and the global vector is
+        # gathered -- on the device (earl_allgather_lengths) on even iterations, by the host
+        # path (counts not known in advance) on odd ones
+        from paper_2510_05943_b200.dispatch import rank_counts
+        cnts = rank_counts(src, world) if src.get("assign") == "given_counts" \
+            else W.near_equal_counts(len(lens), world)
+        edges = np.concatenate([[0], np.cumsum(cnts)]).astype(int)
+        local = torch.as_tensor(np.asarray(lens[edges[rank]:edges[rank + 1]], dtype=np.int32)).cuda()
         for it in range(n_exec):
+            if it % 2 == 0:
+                glens, got_counts = D.allgather_lens(local, counts=cnts)
+            else:
+                glens, got_counts = D.allgather_lens(local)
+            D.comm.check()
+            assert list(got_counts) == list(cnts), (got_counts, cnts)
+            assert glens.cpu().tolist() == list(lens), f"iter {it}: gathered lengths differ"
             plan = D.plan(src, dst, glens, fields)
             ptrs, views = D.alloc_recv(plan, fields)
             for v in views:
@@ -281,5 +296,166 @@ def gpu_hash_main(rank, world, port, q, case):
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+def gpu_null_recv_main(rank, world, port, q, case):
+    """Source-only ranks pass NULL receive buffers (earl_dispatch.h: a rank that receives nothing
+    may), and ranks place their receive buffers at rank-specific window offsets: every
+    destination still gets every byte the oracle gives it (the senders use the offsets each
+    destination published, not their own)."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher, field_bytes
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, src, dst, fields = case
+        T = sum(lens)
+        glob = W.gen_global_fields(fields, T, seed_base=91, random_bits=True)
+        src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+        want, _, _ = O.dispatch(src, dst, lens, src_arrays, fields, world)
+        D = Dispatcher(window_bytes=T * W.bytes_per_token(fields) + (1 << 20), device=0)
+        mine = [torch.from_numpy(a).cuda() if a.size else None for a in src_arrays.get(rank, [])] \
+            if rank in src_arrays else [None] * len(fields)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        for it in range(3):
+            plan = D.plan(src, dst, glens, fields)
+            st = plan.stats()
+            D.comm.reset_alloc()
+            D.comm.alloc(256 * (1 + rank + it))   # rank- and iteration-specific offsets
+            ptrs, views = [], []
+            n_mine = int(st["n_local_tokens"][rank])
+            for b in field_bytes(fields):
+                if rank in want and n_mine:
+                    ptr = D.comm.alloc(n_mine * b)
+                    from paper_2510_05943_b200.dispatch import window_tensor
+                    v = window_tensor(ptr, n_mine * b, D.device)
+                    v.fill_(0xA5)
+                    ptrs.append(ptr)
+                    views.append(v)
+                else:
+                    ptrs.append(None)   # receives nothing: NULL
+                    views.append(None)
+            torch.cuda.synchronize()
+            plan.exec(mine, ptrs)
+            torch.cuda.synchronize()
+            plan.sync()
+            if rank in want:
+                for f in range(len(fields)):
+                    got = views[f].cpu().numpy() if views[f] is not None else np.zeros(0, np.uint8)
+                    assert np.array_equal(got, want[rank][f]), f"iter {it} rank {rank} field {f}"
+            plan.destroy()
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+def gpu_late_peer_main(rank, world, port, q, case):
+    """A peer that arrives after the others' entry barrier timed out: the others skip their
+    copies and say so in their done flags; the late rank passes its own barrier (the others'
+    ready flags are there), copies, and then reports TIMEOUT naming the ranks whose copies were
+    skipped -- instead of returning with their contribution missing."""
+    try:
+        import os
+        import time
+        os.environ["EARL_TIMEOUT_MS"] = "400"
+        import numpy as np
+        import torch
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        import torch.distributed as dist
+        lens = case
+        fields = W.field_set("tiny3")
+        src = W.rollout_layout(len(lens), world)
+        dst = W.layout(dp=1, tp=world, assign="contig")
+        D = Dispatcher(window_bytes=sum(lens) * W.bytes_per_token(fields) + (1 << 16), device=0)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        plan = D.plan(src, dst, glens, fields)
+        ptrs, views = D.alloc_recv(plan, fields)
+        tok = W.rollout_token_counts(np.asarray(lens), src["counts"])[rank]
+        mine = [torch.zeros(max(16, tok * b), dtype=torch.uint8, device="cuda") for b in (4, 4, 4)]
+        late = world - 1
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == late:
+            time.sleep(1.5)   # the others' entry barriers (400 ms) and done waits expire first
+        plan.exec(mine, ptrs)
+        msg = "ok"
+        try:
+            plan.sync()
+            msg = f"rank {rank}: no error reported"
+        except EarlError as e:
+            others = sum(1 << r for r in range(world) if r != late)
+            if rank == late:
+                want = f"skipped their copies (mask 0x{others:x})"
+            else:
+                want = f"mask 0x{1 << late:x}"
+            if "TIMEOUT" not in str(e) or want not in str(e):
+                msg = f"rank {rank}: unexpected error {e}"
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+def gpu_nccl_main(rank, world, port, q, case):
+    """K8 through the library: pack -> grouped ncclSend / ncclRecv (earl_dispatch_exchange) ->
+    unpack, against the oracle.  One GPU hosts one NCCL rank only, so this runs at world 1 (the
+    message to itself goes through NCCL too); multi-rank message tables are covered by the
+    gloo-staged multi-process tests."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, fields = case
+        src = W.rollout_layout(len(lens), 1)
+        dst = W.layout(dp=1, assign="contig")
+        T = sum(lens)
+        glob = W.gen_global_fields(fields, T, seed_base=13, random_bits=True)
+        src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+        want, _, _ = O.dispatch(src, dst, lens, src_arrays, fields, world)
+        D = Dispatcher(window_bytes=1 << 16, device=0)
+        D.init_nccl()
+        mine = [torch.from_numpy(a).cuda() for a in src_arrays[0]]
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        plan = D.plan(src, dst, glens, fields)
+        st = plan.stats()
+        recv = [torch.full((int(st["n_local_tokens"][0]) * b,), 0xA5, dtype=torch.uint8, device="cuda")
+                for b in [x[1] * x[2] for x in fields]]
+        for it in range(3):
+            D.exec_staged(plan, mine, recv)     # library path: earl_dispatch_exec_staged
+            torch.cuda.synchronize()
+            plan.sync()
+            for f in range(len(fields)):
+                assert np.array_equal(recv[f].cpu().numpy(), want[0][f]), (it, f)
+            for x in recv:
+                x.fill_(0)
+        # the exchange call on its own, with caller-owned stage buffers
+        send_stage, recv_stage, msgs = D.alloc_stage(plan)
+        plan.pack(mine, [send_stage])
+        plan.exchange(send_stage, recv_stage)
+        plan.unpack([recv_stage], recv)
+        torch.cuda.synchronize()
+        for f in range(len(fields)):
+            assert np.array_equal(recv[f].cpu().numpy(), want[0][f]), ("exchange", f)
+        plan.destroy()
+        import torch.distributed as dist
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))

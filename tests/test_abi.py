@@ -36,7 +36,7 @@ def test_every_declared_symbol_is_exported():
     L = earl.lib()
     for name in decl:
         getattr(L, name)
-    assert L.earl_abi_version() == 2
+    assert L.earl_abi_version() == 3
     assert L.earl_status_string(2) == b"EARL_ERR_LAYOUT"
 
 

@@ -588,6 +588,31 @@ def test_seq_fields_on_gpu(seed):
         for f in range(len(sf)):
             got = recv[d * len(sf) + f][: arrs[f].size].cpu().numpy()
             assert np.array_equal(got, arrs[f]), (d, f)
+    # the token plan re-planned for other lengths (same N): the per-sequence plan follows it
+    # (earl_plan_replan on it re-reads the token plan's groups on the device)
+    if n and seed % 2 == 0:
+        lens2 = [rng.randint(0, 500) for _ in range(n)]
+        want2 = O.dispatch_seq_fields(src, dst, lens2, {
+            r: [np.concatenate([glob[f][i * Bs[f]:(i + 1) * Bs[f]] for i in m])
+                if m else np.zeros(0, dtype=np.uint8) for f in range(len(sf))]
+            for r, m in O.seq_holdings(src, lens2, O.assign_groups(src, lens2)).items()}, sf, world)
+        if all(O.seq_holdings(src, lens2, O.assign_groups(src, lens2)).get(r) == hs.get(r)
+               for r in range(world)):
+            tp.replan(torch.as_tensor(np.asarray(lens2, dtype=np.int32)).cuda())
+            sp.replan()
+            st2 = sp.stats()
+            recv2 = [torch.zeros(max(1, int(st2["n_local_tokens"][r]) * Bs[f]), dtype=torch.uint8,
+                                 device="cuda") for r in range(world) for f in range(len(sf))]
+            sp.exec(send, recv2)
+            torch.cuda.synchronize()
+            for d, arrs in want2.items():
+                for f in range(len(sf)):
+                    got = recv2[d * len(sf) + f][: arrs[f].size].cpu().numpy()
+                    assert np.array_equal(got, arrs[f]), ("replan", d, f)
+    tp.destroy()   # the per-sequence plan keeps its token plan alive
+    sp.exec(send, recv)
+    torch.cuda.synchronize()
+    sp.destroy()
 
 
 @pytest.mark.parametrize("gamma", [1.0, 0.97, 0.0])

@@ -139,3 +139,82 @@ def test_plan_hash_mismatch_detected(world):
     from paper_2510_05943_b200 import build
     build.build()
     run_procs(mp_worker.gpu_hash_main, world, extra=(W.c2_lengths(0)[:48].tolist(),), timeout=300)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["dp2_to_dp1", "disjoint_2to2", "tp2_dst_one_src", "random4"])
+def test_source_only_ranks_pass_null_recv(name):
+    """ADVICE r1 (high): a rank that receives nothing passes NULL receive buffers and still sends
+    every record; receive offsets differ per rank (published by each destination)."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    f = W.field_set("tiny3") + [("m", 1, 1, "mask"), ("h", 2, 24, "hidden")]
+    if name == "dp2_to_dp1":            # rank 1 is source-only
+        world, lens = 2, W.TINY_LENGTHS.tolist()
+        src, dst = W.rollout_layout(8, 2), W.layout(dp=1, assign="contig")
+    elif name == "disjoint_2to2":      # ranks 0,1 source-only; 2,3 destination-only
+        world, lens = 4, W.c2_lengths(0)[:30].tolist()
+        src = dict(W.rollout_layout(30, 2))
+        dst = dict(W.layout(dp=2, assign="contig"), rank0=2)
+    elif name == "tp2_dst_one_src":    # one source rank feeds a TP2 group on the other ranks
+        world, lens = 3, W.c2_lengths(0)[:20].tolist()
+        src = W.rollout_layout(20, 1)
+        dst = dict(W.layout(dp=1, tp=2, assign="contig"), rank0=1)
+    else:
+        from tests.helpers import random_layout
+        rng = random.Random(11)
+        world, n = 4, 25
+        lens = [rng.randint(0, 200) for _ in range(n)]
+        src = random_layout(rng, world, n, allow_lpt=True)
+        dst = random_layout(rng, world, n, allow_lpt=True)
+    run_procs(mp_worker.gpu_null_recv_main, world, extra=((lens, src, dst, f),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_late_peer_reports_skipped_copies(world):
+    """ADVICE r1 (medium): ranks whose entry barrier timed out skip their copies and flag it in
+    their done signal; the late rank reports TIMEOUT naming them."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    run_procs(mp_worker.gpu_late_peer_main, world, extra=(W.TINY_LENGTHS.tolist(),), timeout=300)
+
+
+@pytest.mark.gpu
+def test_nccl_staged_exchange_in_library():
+    """K8 (VERDICT r1 #4): the staged exchange as library NCCL calls, bit-exact vs the oracle."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    lens = W.c2_lengths(2)[:40].tolist()
+    f = W.field_set("scalar6-fp32") + [("h", 2, 40, "hidden")]
+    run_procs(mp_worker.gpu_nccl_main, 1, extra=((lens, f),), timeout=300)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"EARL_REMOTE_STORE": "tma"}, {"EARL_COPY_CFG_P2P": "3"},
+                                 {"EARL_REMOTE_STORE": "tma", "EARL_COPY_CFG_P2P": "1"}])
+@pytest.mark.parametrize("name", ["c3_dp8_dp2tp4", "c4_dp4_sp2"])
+def test_p2p_store_variants(name, env, monkeypatch):
+    """The NVLink options of the fused exec (VERDICT r1 #4): peer replicas by bulk TMA stores
+    (EARL_REMOTE_STORE=tma) and a forced launch shape for multi-process launches
+    (EARL_COPY_CFG_P2P), bit-exact against the oracle like the defaults."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    f3 = W.field_set("tiny3") + [("m", 1, 1, "mask"), ("h", 2, 64, "hidden")]
+    if name == "c3_dp8_dp2tp4":
+        world, lens = 8, W.c2_lengths(0)[:64].tolist()
+        src, dst = W.config_layouts("c3", 8, 64)
+    else:
+        world, lens = 4, W.c4_lengths(0)[:10].tolist()
+        src, dst = W.config_layouts("c4", 4, 10)
+    run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 2, "fused"),), timeout=600)
