@@ -405,7 +405,8 @@ EARL_API earl_status_t earl_policy_build(int32_t n_configs, const int32_t* confi
 EARL_API earl_status_t earl_policy_table(earl_policy_t policy, int32_t* config_of_bucket);
 /* The configuration for the next rollout given the observed average length (s3 hysteresis: keep
  * `current` while avg_len stays within hysteresis_tokens of a boundary shared with a range of
- * `current`).  *next = the configuration, *switched = (next != current).
+ * `current`, unless `current` is an OOM entry of the new range: the selection is never an OOM
+ * configuration).  *next = the configuration, *switched = (next != current).
  * Errors: INVALID_ARGUMENT (current outside [0, n_configs), NULL), POLICY (avg_len outside
  * [bounds[0], bounds[n_buckets])). */
 EARL_API earl_status_t earl_policy_select(earl_policy_t policy, double avg_len, int32_t current,

@@ -14,6 +14,7 @@ earl_status_t set_error(earl_status_t st, const char* msg);  // api.cu
 struct earl_policy {
   std::vector<int32_t> table;   // configuration per context range
   std::vector<int64_t> bounds;  // n_buckets + 1
+  std::vector<uint8_t> oom;     // [n_configs][n_buckets] (empty: no OOM probe)
   int32_t n_configs = 0;
   int64_t hysteresis = 0;
 };
@@ -76,6 +77,7 @@ extern "C" earl_status_t earl_policy_build(int32_t n_configs, const int32_t* con
   p->bounds.assign(bounds, bounds + n_buckets + 1);
   p->n_configs = n_configs;
   p->hysteresis = hysteresis_tokens;
+  if (oom) p->oom.assign(oom, oom + (size_t)n_configs * n_buckets);
   *out = p;
   return EARL_OK;
 }
@@ -100,9 +102,10 @@ extern "C" earl_status_t earl_policy_select(earl_policy_t p, double avg_len, int
                 (long long)p->bounds[0], (long long)p->bounds[nb]);
   int32_t want = p->table[b];
   const double h = (double)p->hysteresis;
-  if (want != current) {
+  const bool current_oom = !p->oom.empty() && p->oom[(size_t)current * nb + b];
+  if (want != current && !current_oom) {
     // hysteresis: a range of the current configuration borders this one and avg_len sits
-    // within h tokens of the shared boundary
+    // within h tokens of the shared boundary (never onto a configuration that OOMs here)
     if (b > 0 && p->table[b - 1] == current && avg_len - (double)p->bounds[b] < h) want = current;
     if (b + 1 < nb && p->table[b + 1] == current && (double)p->bounds[b + 1] - avg_len < h) want = current;
   }

@@ -97,9 +97,31 @@ int main() {
   CK(cuMulticastGetGranularity(&mgran, &mp, CU_MULTICAST_GRANULARITY_MINIMUM));
   CK(cuMulticastGetGranularity(&mrec, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
   printf("multicast granularity min=%zu recommended=%zu\n", mgran, mrec);
-  mp.size = ((size + mrec - 1) / mrec) * mrec;
   CUmemGenericAllocationHandle mch;
-  CK(cuMulticastCreate(&mch, &mp));
+  // which properties does this box accept? (size: min vs recommended granularity; handle
+  // types: POSIX FD, fabric, none)
+  CUresult cr = CUDA_ERROR_INVALID_VALUE;
+  const unsigned long long htypes[3] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                        CU_MEM_HANDLE_TYPE_FABRIC, 0};
+  const size_t sizes[2] = {((size + mgran - 1) / mgran) * mgran, ((size + mrec - 1) / mrec) * mrec};
+  for (int hi = 0; hi < 3 && cr != CUDA_SUCCESS; ++hi)
+    for (int si = 0; si < 2 && cr != CUDA_SUCCESS; ++si) {
+      mp.handleTypes = htypes[hi];
+      mp.size = sizes[si];
+      cr = cuMulticastCreate(&mch, &mp);
+      const char* es = nullptr;
+      cuGetErrorString(cr, &es);
+      printf("cuMulticastCreate(numDevices=1, handleTypes=0x%llx, size=%zu) -> %d %s\n",
+             htypes[hi], sizes[si], (int)cr, es ? es : "?");
+    }
+  if (cr != CUDA_SUCCESS) {
+    mp.numDevices = 2;
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = sizes[0];
+    cr = cuMulticastCreate(&mch, &mp);
+    printf("cuMulticastCreate(numDevices=2) -> %d\n", (int)cr);
+    return 0;
+  }
   CK(cuMulticastAddDevice(mch, dev));
   CK(cuMulticastBindMem(mch, 0, mem, 0, size, 0));
   CUdeviceptr mcva;

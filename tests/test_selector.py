@@ -90,6 +90,26 @@ def test_hysteresis_holds_the_current_config_near_a_boundary():
     assert S.select(table, BOUNDS, 500, 7000, 1) == (0, True)
 
 
+def test_hysteresis_never_keeps_an_oom_configuration():
+    """Reading s2 + s3: hysteresis keeps the current configuration near a boundary, but never
+    into a range where it runs out of memory (TP4 OOM at long context).  Fig. 3
+    with TP4 OOM from 8K on: at 8.2K (200 tokens past the edge, hysteresis 500) the plain
+    hysteresis rule keeps TP4; with the OOM mask it must switch to TP8."""
+    tgs = [[131.0, 100.0, 100.0, 100.0], [100.0, 105.0, 105.0, 105.0]]
+    bounds = [0, 8 * K, 16 * K, 32 * K, 64 * K]
+    oom_from_8k = [[0, 1, 1, 1], [0, 0, 0, 0]]
+    oom_from_16k = [[0, 0, 1, 1], [0, 0, 0, 0]]
+    table = S.build_policy(TP, bounds, tgs, oom_from_8k)
+    assert table == [0, 1, 1, 1] == S.build_policy(TP, bounds, tgs, oom_from_16k)
+    assert S.select(table, bounds, 500, 8 * K + 200, 0) == (0, False)               # plain s3
+    assert S.select(table, bounds, 500, 8 * K + 200, 0, oom_from_16k) == (0, False)  # TP4 fits
+    assert S.select(table, bounds, 500, 8 * K + 200, 0, oom_from_8k) == (1, True)    # TP4 OOMs
+    earl = _lib()
+    p = earl.Policy(TP, bounds, tgs, oom_from_8k, 500)
+    assert p.select(8 * K + 200, 0) == (1, True)
+    p.destroy()
+
+
 def test_hysteresis_bound_at_most_one_switch_within_a_band():
     rng = random.Random(2)
     table = S.build_policy(TP, BOUNDS, FIG3)
@@ -165,7 +185,8 @@ def test_library_policy_matches_oracle(seed):
     for _ in range(60):
         x = rng.uniform(bounds[0], bounds[-1] - 1e-6)
         got = p.select(x, cur)
-        assert got == S.select(want, bounds, hyst, x, cur)
+        assert got == S.select(want, bounds, hyst, x, cur, oom)
+        assert not oom[got[0]][S.bucket_of(bounds, x)], "selected an OOM configuration"
         cur = got[0]
     p.destroy()
 
