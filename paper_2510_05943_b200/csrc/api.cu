@@ -156,6 +156,7 @@ struct earl_plan {
   earl_plan* parent = nullptr;
   int32_t* owned = nullptr;
   int refs = 1;
+  bool fast = false;          // the SP = 1 single-pass planner (planner_sp1_kernel)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -552,11 +553,23 @@ cudaError_t plan_launch(earl_plan* p, cudaStream_t s) {
   static const char* plan_trace = getenv("EARL_PLAN_TRACE");
   if (plan_trace) cudaMallocAsync((void**)&a.phase_ts, 16 * sizeof(uint64_t), s);
   clear_stale_error();
-  e = launch_planner(a, p->lpt_smem, p->grid, s);
+  e = launch_planner(a, p->lpt_smem, p->grid, p->fast, s);
   if (plan_trace && e == cudaSuccess) {  // debug only: synchronous read-back of phase times
     uint64_t ts[16];
     cudaMemcpyAsync(ts, a.phase_ts, sizeof(ts), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    if (p->fast) {  // planner_sp1_kernel stamps 0-4 and 7
+      fprintf(stderr, "earl plan trace (sp1) N=%lld G=%d us: lengths+reduce %.1f, P+assign %.1f, "
+              "histograms %.1f, bases+tables %.1f, emit %.1f, total %.1f\n", (long long)a.N, p->grid,
+              (ts[1] - ts[0]) / 1e3, (ts[2] - ts[1]) / 1e3, (ts[3] - ts[2]) / 1e3,
+              (ts[4] - ts[3]) / 1e3, (ts[7] - ts[4]) / 1e3, (ts[7] - ts[0]) / 1e3);
+      cudaFreeAsync(a.phase_ts, s);
+      a.phase_ts = nullptr;
+      if (e != cudaSuccess) return e;
+      g_launches.fetch_add(1);
+      use_end(p, s);
+      return cudaSuccess;
+    }
     fprintf(stderr, "earl plan trace N=%lld G=%d us:", (long long)a.N, p->grid);
     for (int k = 1; k < 8; ++k) fprintf(stderr, " p%d=%.1f", k - 1, (ts[k] - ts[k - 1]) / 1e3);
     fprintf(stderr, " total=%.1f [p5: loads %.1f, serial %.1f, publish %.1f]", (ts[7] - ts[0]) / 1e3,
@@ -635,6 +648,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   total += 2 * sz(N, 8) + 2 * sz(N, 4);
   total += 8 * sz(max_pieces, 4) + sz(max_pieces + 1, 8);
   total += sz(kMaxPlanGrid, 8) + sz((int64_t)kMaxPlanGrid * kMaxKeys, 4);
+  total += sz((int64_t)2 * kMaxPlanGrid * (kMaxKeys + 2 * kMaxShards), 8);
   const int64_t nscr = (N > max_pieces ? N : max_pieces) + 1;
   total += sz(nscr, 8) + 2 * sz(nscr, 4);
   total += 4 * sz(max_records, 4) + 3 * sz(max_records, 8) + sz(max_records + 1, 8);
@@ -673,6 +687,7 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
   a.ps_scan = carve<int64_t>(q, max_pieces + 1);
   a.cta_sums = carve<int64_t>(q, kMaxPlanGrid);
   a.ghist = carve<int32_t>(q, (int64_t)kMaxPlanGrid * kMaxKeys);
+  a.fhist = carve<int64_t>(q, (int64_t)2 * kMaxPlanGrid * (kMaxKeys + 2 * kMaxShards));
   a.vtmp = carve<int64_t>(q, nscr);
   a.ktmp = carve<int32_t>(q, nscr);
   a.ptmp = carve<int32_t>(q, nscr);
@@ -697,7 +712,13 @@ extern "C" earl_status_t earl_dispatch_plan(earl_comm_t c, const earl_layout_t* 
     while (n2 < N) n2 <<= 1;
     p->lpt_smem = (size_t)n2 * sizeof(uint64_t);
   }
-  p->grid = planner_grid(N, max_pieces, c->sm_count, p->lpt_smem);
+  // SP = 1 on both sides (ZIGZAG excepted: its two chunks per sequence are two pieces): the
+  // single-pass planner; EARL_PLAN_PATH=general forces the general one (tests compare them)
+  const char* path_env = getenv("EARL_PLAN_PATH");
+  const bool force_general = path_env && std::strcmp(path_env, "general") == 0;
+  p->fast = !force_general && src->sp == 1 && dst->sp == 1 && src->sp_split != EARL_SP_ZIGZAG &&
+            dst->sp_split != EARL_SP_ZIGZAG;
+  p->grid = planner_grid(N, max_pieces, c->sm_count, p->lpt_smem, p->fast);
   e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming);
   if (e != cudaSuccess) return abort_plan(EARL_ERR_CUDA, "plan event", e);
   e = plan_launch(p, s);

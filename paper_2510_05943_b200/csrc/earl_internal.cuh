@@ -92,6 +92,7 @@ struct PlanArgs {
   int64_t* vtmp;             // [max(N, max_pieces) + 1] scan inputs
   int32_t* ktmp;             // [max(N, max_pieces)] partition keys
   int32_t* ptmp;             // [max(N, max_pieces)] partition output (position -> index)
+  int64_t* fhist;            // SP = 1 fast path: [2][kMaxPlanGrid][kMaxKeys + 2 kMaxShards]
   uint64_t* phase_ts;        // debug (EARL_PLAN_TRACE): %globaltimer at phase boundaries
   int64_t max_pieces;
   int64_t max_records;
@@ -250,8 +251,8 @@ inline cudaError_t opt_in_dynamic_smem(F* func, int bytes, bool (&done)[64]) {
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
 int64_t returns_windows(int64_t tokens);
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s);
-int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem);
-cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s);
+int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem, bool fast);
+cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, bool fast, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
                                  int n_fields, const uint64_t* recv_off, uint64_t timeout_ns,

@@ -420,6 +420,103 @@ __device__ __noinline__ void lpt_assign(const PlanArgs& a, int l, uint64_t* keys
   __syncthreads();
 }
 
+// Per-(rank, dst shard) record / token bases and message byte offsets from the per-key piece
+// starts kstart[0..K] and token totals ktok[K] (key = src shard * Sd + dst shard).  Every CTA
+// derives them in shared memory (warp 0, two entries per lane, warp scans); CTA 0 publishes them
+// in the header for the copy kernels and the host, and writes the records' token-prefix sentinel.
+struct Tables {
+  int64_t rbase[kMaxWorld][kMaxShards], tbase[kMaxWorld][kMaxShards];
+  int64_t rec_begin[kMaxWorld + 1], tok_begin[kMaxWorld + 1];
+  int64_t msg_off[kMaxKeys], stage[kMaxShards], msgb[kMaxKeys];
+};
+
+__device__ __noinline__ void build_tables(const PlanArgs& a, int K, const int64_t* kstart,
+                                          const int64_t* ktok, Tables& tb) {
+  const int tid = threadIdx.x;
+  const LayoutDesc& S = a.lay[0];
+  const LayoutDesc& Dl = a.lay[1];
+  const int Sd = Dl.dp * Dl.sp;
+  const int nts = S.tp < Dl.tp ? S.tp : Dl.tp;
+  PlanHeader* h = a.hdr;
+  if (tid < 32) {
+    const int lane = tid;
+    const int E = a.world * Sd;
+    int64_t cnt[2], tk[2];
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      const int e = lane + 32 * hf;
+      cnt[hf] = 0;
+      tk[hf] = 0;
+      if (e < E) {
+        const int r = e / Sd, ds = e - (e / Sd) * Sd;
+        const int rr = r - S.rank0;
+        if (rr >= 0 && rr < S.dp * S.sp * S.tp && rr % S.tp < nts) {
+          const int key = (rr / S.tp) * Sd + ds;
+          cnt[hf] = kstart[key + 1] - kstart[key];
+          tk[hf] = ktok[key];
+        }
+      }
+    }
+    int64_t carry_c = 0, carry_t = 0;
+#pragma unroll
+    for (int hf = 0; hf < 2; ++hf) {
+      int64_t ic = cnt[hf], it = tk[hf];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t yc = __shfl_up_sync(kFull, ic, o), yt = __shfl_up_sync(kFull, it, o);
+        if (lane >= o) { ic += yc; it += yt; }
+      }
+      const int e = lane + 32 * hf;
+      if (e < E) {
+        const int r = e / Sd, ds = e - (e / Sd) * Sd;
+        tb.rbase[r][ds] = carry_c + ic - cnt[hf];
+        tb.tbase[r][ds] = carry_t + it - tk[hf];
+        if (ds == 0) { tb.rec_begin[r] = tb.rbase[r][0]; tb.tok_begin[r] = tb.tbase[r][0]; }
+      }
+      carry_c += __shfl_sync(kFull, ic, 31);
+      carry_t += __shfl_sync(kFull, it, 31);
+    }
+    if (lane == 0) { tb.rec_begin[a.world] = carry_c; tb.tok_begin[a.world] = carry_t; }
+    // message bytes per key, then the offset of each message inside its source shard's buffer
+    for (int key = lane; key < K; key += 32) {
+      int64_t mb = 0;
+      for (int f = 0; f < a.n_fields; ++f) mb += (ktok[key] * a.Bf[f] + 15) & ~15LL;
+      tb.msgb[key] = mb;
+    }
+    __syncwarp();
+    for (int key = lane; key < K; key += 32) {
+      const int ss = key / Sd, ds = key - ss * Sd;
+      int64_t off = 0;
+      for (int q = 0; q < ds; ++q) off += tb.msgb[ss * Sd + q];
+      tb.msg_off[key] = off;
+      if (ds == Sd - 1) tb.stage[ss] = off + tb.msgb[key];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (tid <= K) h->key_piece_start[tid] = kstart[tid];
+    if (tid < K) {
+      h->key_pieces[tid] = kstart[tid + 1] - kstart[tid];
+      h->key_tokens[tid] = ktok[tid];
+      h->msg_off[tid] = tb.msg_off[tid];
+    }
+    if (tid < S.dp * S.sp) h->stage_bytes_shard[tid] = tb.stage[tid];
+    if (tid <= a.world) {
+      h->rec_begin[tid] = tb.rec_begin[tid];
+      h->rec_tok_begin[tid] = tb.tok_begin[tid];
+    }
+    if (tid < a.world * Sd) {
+      h->rec_base[tid / Sd][tid % Sd] = tb.rbase[tid / Sd][tid % Sd];
+      h->rec_tok_base[tid / Sd][tid % Sd] = tb.tbase[tid / Sd][tid % Sd];
+    }
+    if (tid == 0) {
+      h->n_records = tb.rec_begin[a.world];
+      h->rec_tokens = tb.tok_begin[a.world];
+      a.rec.tok_prefix[tb.rec_begin[a.world]] = tb.tok_begin[a.world];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ PlanArgs a) {
   extern __shared__ uint64_t lpt_keys[];
   __shared__ int64_t sm_scan[NT / 32 + 1];
@@ -613,7 +710,6 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   const int K = S.dp * S.sp * Sd;
   partition_array(a.ktmp, M, K, a.ptmp, a.ghist, ps);
   __shared__ int64_t s_kstart[kMaxKeys + 1], s_ktok[kMaxKeys], s_kscan0[kMaxKeys];
-  __shared__ int64_t s_rbase[kMaxWorld][kMaxShards], s_tbase[kMaxWorld][kMaxShards];
   if (tid <= K) s_kstart[tid] = ps.bstart[tid];
   gsync();
   for (int64_t pos = gtid; pos < M; pos += gstride) {
@@ -632,8 +728,8 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   // ---- phase 5: bases and message offsets ---------------------------------------------
   stamp(a, 5);
   // Every CTA derives the <= 64-entry tables itself in shared memory (parallel loads of the
-  // published scan, then one thread walks <= 8 x 8 entries in shared memory); CTA 0 also
-  // publishes them in the header for the copy kernels and the host.
+  // published scan, then warp 0 scans <= 64 entries); CTA 0 also publishes them in the header
+  // for the copy kernels and the host.
   const int nts = S.tp < Dl.tp ? S.tp : Dl.tp;
   if (tid < K) {
     s_kscan0[tid] = a.ps_scan[s_kstart[tid]];
@@ -641,90 +737,9 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
   }
   __syncthreads();
   stamp(a, 8);
-  __shared__ int64_t s_rec_begin[kMaxWorld + 1], s_tok_begin[kMaxWorld + 1];
-  __shared__ int64_t s_msg_off[kMaxKeys], s_stage[kMaxShards];
-  // warp 0, in parallel: record/token bases over the (rank r, dst shard ds) entries in rank
-  // order (two entries per lane, warp scans), and message byte offsets inside each source
-  // shard's stage buffer (one key per lane, prefix within the row)
-  __shared__ int64_t s_msgb[kMaxKeys];
-  if (tid < 32) {
-    const int lane = tid;
-    const int E = a.world * Sd;
-    int64_t cnt[2], tk[2];
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      const int e = lane + 32 * hf;
-      cnt[hf] = 0;
-      tk[hf] = 0;
-      if (e < E) {
-        const int r = e / Sd, ds = e - (e / Sd) * Sd;
-        const int rr = r - S.rank0;
-        if (rr >= 0 && rr < S.dp * S.sp * S.tp && rr % S.tp < nts) {
-          const int key = (rr / S.tp) * Sd + ds;
-          cnt[hf] = s_kstart[key + 1] - s_kstart[key];
-          tk[hf] = s_ktok[key];
-        }
-      }
-    }
-    int64_t carry_c = 0, carry_t = 0;
-#pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-      int64_t ic = cnt[hf], it = tk[hf];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t yc = __shfl_up_sync(kFull, ic, o), yt = __shfl_up_sync(kFull, it, o);
-        if (lane >= o) { ic += yc; it += yt; }
-      }
-      const int e = lane + 32 * hf;
-      if (e < E) {
-        const int r = e / Sd, ds = e - (e / Sd) * Sd;
-        s_rbase[r][ds] = carry_c + ic - cnt[hf];
-        s_tbase[r][ds] = carry_t + it - tk[hf];
-        if (ds == 0) { s_rec_begin[r] = s_rbase[r][0]; s_tok_begin[r] = s_tbase[r][0]; }
-      }
-      carry_c += __shfl_sync(kFull, ic, 31);
-      carry_t += __shfl_sync(kFull, it, 31);
-    }
-    if (lane == 0) { s_rec_begin[a.world] = carry_c; s_tok_begin[a.world] = carry_t; }
-    // message bytes per key, then the offset of each message inside its source shard's buffer
-    for (int key = lane; key < K; key += 32) {
-      int64_t mb = 0;
-      for (int f = 0; f < a.n_fields; ++f) mb += (s_ktok[key] * a.Bf[f] + 15) & ~15LL;
-      s_msgb[key] = mb;
-    }
-    __syncwarp();
-    for (int key = lane; key < K; key += 32) {
-      const int ss = key / Sd, ds = key - ss * Sd;
-      int64_t off = 0;
-      for (int q = 0; q < ds; ++q) off += s_msgb[ss * Sd + q];
-      s_msg_off[key] = off;
-      if (ds == Sd - 1) s_stage[ss] = off + s_msgb[key];
-    }
-  }
-  __syncthreads();
+  __shared__ Tables tb;
+  build_tables(a, K, s_kstart, s_ktok, tb);
   stamp(a, 9);
-  if (lead) {
-    if (tid <= K) h->key_piece_start[tid] = s_kstart[tid];
-    if (tid < K) {
-      h->key_pieces[tid] = s_kstart[tid + 1] - s_kstart[tid];
-      h->key_tokens[tid] = s_ktok[tid];
-      h->msg_off[tid] = s_msg_off[tid];
-    }
-    if (tid < S.dp * S.sp) h->stage_bytes_shard[tid] = s_stage[tid];
-    if (tid <= a.world) {
-      h->rec_begin[tid] = s_rec_begin[tid];
-      h->rec_tok_begin[tid] = s_tok_begin[tid];
-    }
-    if (tid < a.world * Sd) {
-      h->rec_base[tid / Sd][tid % Sd] = s_rbase[tid / Sd][tid % Sd];
-      h->rec_tok_base[tid / Sd][tid % Sd] = s_tbase[tid / Sd][tid % Sd];
-    }
-    if (tid == 0) {
-      h->n_records = s_rec_begin[a.world];
-      h->rec_tokens = s_tok_begin[a.world];
-      a.rec.tok_prefix[s_rec_begin[a.world]] = s_tok_begin[a.world];
-    }
-  }
 
   // ---- phase 6: records ---------------------------------------------------------------
   stamp(a, 6);
@@ -737,7 +752,7 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
     const int ss = key / Sd, ds = key - ss * Sd;
     const int s = S.rank0 + ss * S.tp + ts;
     const int64_t rho = q - s_kstart[key];
-    const int64_t j = s_rbase[s][ds] + rho;
+    const int64_t j = tb.rbase[s][ds] + rho;
     const int i = a.ps_i[q];
     const int64_t x = a.ps_x[q], y = a.ps_y[q];
     const int64_t msg_tok = a.ps_scan[q] - s_kscan0[key];
@@ -761,7 +776,328 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
       a.rec.dst_tok[j] = dof;
     }
     a.rec.msg_tok[j] = msg_tok;
-    a.rec.tok_prefix[j] = s_tbase[s][ds] + msg_tok;
+    a.rec.tok_prefix[j] = tb.tbase[s][ds] + msg_tok;
+  }
+  stamp(a, 7);
+}
+
+// ---------------------------------------------------------------------------------------
+// SP = 1 fast path.  When neither layout splits sequences (sp == 1 on both sides, any
+// assignment), a piece is a whole sequence with L > 0 and every plan array is a stable
+// per-bucket rank or token prefix over three bucketings of the sequences: by message key
+// (src group, dst group; pieces only), by src group and by dst group (every sequence).  One
+// kernel computes them all with two grid barriers (three with LPT) instead of the general
+// path's ~20: each CTA owns a contiguous tile of sequences, histograms its buckets, and after
+// one barrier emits every output from (CTAs before it) + (chunks before) + (warps before) +
+// (lanes before).  Same outputs, bit for bit, as the general planner (tested against it and
+// against the oracle).
+// ---------------------------------------------------------------------------------------
+
+constexpr int kMaxBuckets = kMaxKeys + 2 * kMaxShards;
+
+struct FastSmem {
+  int32_t wcnt[NT / 32][kMaxBuckets];  // per-warp bucket counts of a chunk, then exclusive over warps
+  int64_t wtok[NT / 32][kMaxBuckets];
+  int64_t run_cnt[kMaxBuckets], run_tok[kMaxBuckets];      // before the current chunk
+  int64_t chunk_cnt[kMaxBuckets], chunk_tok[kMaxBuckets];  // the current chunk's totals
+  int64_t tot_cnt[kMaxBuckets], tot_tok[kMaxBuckets];      // whole batch
+  unsigned long long hcnt[kMaxBuckets], htok[kMaxBuckets];  // this CTA's histogram
+  int64_t gstart[2][kMaxShards + 1], gtok0[2][kMaxShards + 1];
+  int64_t kstart[kMaxKeys + 1], ktok[kMaxKeys];
+  int64_t carry, total;
+};
+
+// The calling lane's bucket u (-1: none) with weight L: its rank among the warp's lanes below
+// it in the same bucket, the token prefix over them, and -- on the highest lane of each bucket --
+// the bucket's warp count and tokens.  The token prefix runs one warp scan per distinct bucket
+// of the warp (1 for layouts that keep neighbours together, <= 8 for a round-robin one).
+__device__ __forceinline__ void warp_bucket(int u, int64_t L, int lane, int& rank, int64_t& tpre,
+                                            bool& last, int& gcnt, int64_t& gtok) {
+  const unsigned peers = __match_any_sync(kFull, u);
+  rank = __popc(peers & ((1u << lane) - 1u));
+  gcnt = __popc(peers);
+  last = (31 - __clz(peers)) == lane;
+  tpre = 0;
+  gtok = 0;
+  unsigned rem = kFull;
+  while (rem) {
+    const int leader = __ffs(rem) - 1;
+    const int ub = __shfl_sync(kFull, u, leader);
+    const bool mine = u == ub;
+    const unsigned m = __ballot_sync(kFull, mine);
+    int64_t v = mine ? L : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, v, o);
+      if (lane >= o) v += y;
+    }
+    if (mine) { tpre = v - L; gtok = v; }
+    rem &= ~m;
+  }
+}
+
+__device__ __forceinline__ int assign_group(const PlanArgs& a, const LayoutDesc& Ly, PlanHeader* h,
+                                            int64_t i, int64_t L, int64_t Pi, int64_t T, int64_t N) {
+  const int D = Ly.dp;
+  int g = 0;
+  if (Ly.assign == EARL_ASSIGN_GIVEN_COUNTS) {
+    while (g < D - 1 && i >= Ly.count_start[g + 1]) ++g;
+  } else if (Ly.assign == EARL_ASSIGN_CONTIG) {
+    if (T == 0) {
+      const int64_t q = N / D, r = N % D;
+      g = (i < r * (q + 1)) ? (int)(i / (q + 1)) : (int)(r + (i - r * (q + 1)) / q);
+    } else {
+      const int64_t m = ((int64_t)D * (2 * Pi + L)) / (2 * T);
+      g = (int)(m < D - 1 ? m : D - 1);
+    }
+  } else {  // EXPLICIT
+    g = Ly.group_of_seq[i];
+    if (g < 0 || g >= D) { latch(h, EARL_ERR_LAYOUT, (int)i); g = 0; }
+  }
+  return g;
+}
+
+__global__ void __launch_bounds__(NT, 1) planner_sp1_kernel(const __grid_constant__ PlanArgs a) {
+  extern __shared__ uint64_t lpt_keys[];
+  __shared__ int64_t sm_scan[NT / 32 + 1];
+  __shared__ FastSmem fs;
+  __shared__ Tables tb;
+  PlanHeader* h = a.hdr;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const bool lead = blockIdx.x == 0;
+  const int64_t N = a.N;
+  const int64_t lo = range_lo(N), hi = range_hi(N);
+  const int nchunks = (int)((hi - lo + NT - 1) / NT);
+  const LayoutDesc& S = a.lay[0];
+  const LayoutDesc& Dl = a.lay[1];
+  const int Ds = S.dp, Dd = Dl.dp;
+  const int K = Ds * Dd;
+  const int U = K + Ds + Dd;
+  const bool lpt = S.assign == EARL_ASSIGN_LPT || Dl.assign == EARL_ASSIGN_LPT;
+
+  // ---- lengths, the CTA's token sum; P and T after one barrier ------------------------
+  stamp(a, 0);
+  int64_t part = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t i = lo + (int64_t)c * NT + tid;
+    if (i < hi) {
+      int32_t L = a.seq_lens[i];
+      if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
+      a.lens[i] = L;
+      part += L;
+    }
+  }
+  {
+    int64_t tot;
+    block_excl_scan(part, tot, sm_scan);
+    if (tid == 0) a.cta_sums[blockIdx.x] = tot;
+  }
+  if (tid < kMaxBuckets) { fs.hcnt[tid] = 0; fs.htok[tid] = 0; }
+  gsync();
+  if (tid < 32) {
+    int64_t before = 0, all = 0;
+    for (int b = tid; b < (int)gridDim.x; b += 32) {
+      const int64_t v = __ldcg(&a.cta_sums[b]);
+      all += v;
+      if (b < (int)blockIdx.x) before += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(kFull, before, o);
+      all += __shfl_xor_sync(kFull, all, o);
+    }
+    if (tid == 0) { fs.carry = before; fs.total = all; }
+  }
+  __syncthreads();
+  const int64_t T = fs.total;
+  stamp(a, 1);
+  {
+    int64_t run = fs.carry;
+    for (int c = 0; c < nchunks; ++c) {
+      const int64_t i = lo + (int64_t)c * NT + tid;
+      const int64_t L = i < hi ? a.lens[i] : 0;
+      int64_t tot;
+      const int64_t ex = run + block_excl_scan(L, tot, sm_scan);
+      if (i < hi) {
+        a.P[i] = ex;
+        // assignment (LPT below, in CTA 0)
+        if (S.assign != EARL_ASSIGN_LPT) a.grp[0][i] = assign_group(a, S, h, i, L, ex, T, N);
+        if (Dl.assign != EARL_ASSIGN_LPT) a.grp[1][i] = assign_group(a, Dl, h, i, L, ex, T, N);
+      }
+      run += tot;
+    }
+  }
+  if (lead && tid == 0) { a.P[N] = T; h->T = T; }
+  if (lpt) {
+    __syncthreads();
+    if (lead) {
+      if (S.assign == EARL_ASSIGN_LPT) lpt_assign(a, 0, lpt_keys);
+      if (Dl.assign == EARL_ASSIGN_LPT) lpt_assign(a, 1, lpt_keys);
+    }
+    gsync();
+  }
+
+  // ---- this CTA's bucket histograms, published; totals and bases after one barrier ------
+  stamp(a, 2);
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t i = lo + (int64_t)c * NT + tid;
+    const bool ok = i < hi;
+    const int64_t L = ok ? a.lens[i] : 0;
+    const int gs = ok ? __ldcg(&a.grp[0][i]) : 0, gd = ok ? __ldcg(&a.grp[1][i]) : 0;
+    const int ub[3] = {ok && L > 0 ? gs * Dd + gd : -1, ok ? K + gs : -1, ok ? K + Ds + gd : -1};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      int rank, gcnt;
+      int64_t tpre, gtok;
+      bool last;
+      warp_bucket(ub[k], L, lane, rank, tpre, last, gcnt, gtok);
+      if (last && ub[k] >= 0) {
+        atomicAdd(&fs.hcnt[ub[k]], (unsigned long long)gcnt);
+        atomicAdd(&fs.htok[ub[k]], (unsigned long long)gtok);
+      }
+    }
+  }
+  __syncthreads();
+  int64_t* fh = a.fhist;  // [2][gridDim.x][kMaxBuckets]: counts, then tokens
+  if (tid < U) {
+    fh[(int64_t)blockIdx.x * kMaxBuckets + tid] = (int64_t)fs.hcnt[tid];
+    fh[((int64_t)gridDim.x + blockIdx.x) * kMaxBuckets + tid] = (int64_t)fs.htok[tid];
+  }
+  gsync();
+  stamp(a, 3);
+  // per bucket: the sum over the CTAs before this one and over all (warp q handles buckets
+  // q, q + 32, q + 64 of counts and of tokens; lanes stride over the CTAs)
+  for (int q = w; q < 2 * U; q += NT / 32) {
+    const int u = q < U ? q : q - U;
+    const int64_t* col = fh + (q < U ? 0 : (int64_t)gridDim.x * kMaxBuckets) + u;
+    int64_t before = 0, all = 0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) {
+      const int64_t v = __ldcg(col + (int64_t)b * kMaxBuckets);
+      all += v;
+      if (b < (int)blockIdx.x) before += v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      before += __shfl_xor_sync(kFull, before, o);
+      all += __shfl_xor_sync(kFull, all, o);
+    }
+    if (lane == 0) {
+      if (q < U) { fs.run_cnt[u] = before; fs.tot_cnt[u] = all; }
+      else { fs.run_tok[u] = before; fs.tot_tok[u] = all; }
+    }
+  }
+  __syncthreads();
+  // bases: group starts (sequence positions and tokens) per layout, message keys
+  if (tid == 0) {
+    for (int l = 0; l < 2; ++l) {
+      const int D = l ? Dd : Ds, b0 = l ? K + Ds : K;
+      int64_t cs = 0, ts = 0;
+      for (int g = 0; g < D; ++g) {
+        fs.gstart[l][g] = cs; fs.gtok0[l][g] = ts;
+        cs += fs.tot_cnt[b0 + g]; ts += fs.tot_tok[b0 + g];
+      }
+      fs.gstart[l][D] = cs; fs.gtok0[l][D] = ts;
+    }
+    int64_t ks = 0;
+    for (int k = 0; k < K; ++k) { fs.kstart[k] = ks; fs.ktok[k] = fs.tot_tok[k]; ks += fs.tot_cnt[k]; }
+    fs.kstart[K] = ks;
+  }
+  __syncthreads();
+  if (lead) {
+    for (int l = 0; l < 2; ++l) {
+      const LayoutDesc& Ly = a.lay[l];
+      const int D = Ly.dp;
+      if (tid <= D) h->group_start[l][tid] = fs.gstart[l][tid];
+      if (tid < D) {
+        const int64_t st = fs.gtok0[l][tid + 1] - fs.gtok0[l][tid];
+        h->group_count[l][tid] = fs.gstart[l][tid + 1] - fs.gstart[l][tid];
+        h->shard_tokens[l][tid] = st;
+        h->group_tokens[l][tid] = (Ly.split == EARL_SP_FLAT || Ly.split == EARL_SP_THRESHOLD) ? st : 0;
+        if (l == 1 && st > 0x7fffffffLL) latch(h, EARL_ERR_CAPACITY, tid);
+      }
+    }
+    if (tid == 0) { h->n_pieces = fs.kstart[K]; a.cum[0][N] = T; a.cum[1][N] = T; a.pbase[N] = fs.kstart[K]; }
+  }
+  build_tables(a, K, fs.kstart, fs.ktok, tb);
+  stamp(a, 4);
+
+  // ---- emission, chunk by chunk in sequence order ---------------------------------------
+  const int nts = S.tp < Dl.tp ? S.tp : Dl.tp;
+  const bool pos_s = S.split == EARL_SP_FLAT || S.split == EARL_SP_THRESHOLD;
+  const bool pos_d = Dl.split == EARL_SP_FLAT || Dl.split == EARL_SP_THRESHOLD;
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t i = lo + (int64_t)c * NT + tid;
+    const bool ok = i < hi;
+    const int64_t L = ok ? a.lens[i] : 0;
+    const int gs = ok ? __ldcg(&a.grp[0][i]) : 0, gd = ok ? __ldcg(&a.grp[1][i]) : 0;
+    const int ub[3] = {ok && L > 0 ? gs * Dd + gd : -1, ok ? K + gs : -1, ok ? K + Ds + gd : -1};
+    for (int q = tid; q < (NT / 32) * kMaxBuckets; q += NT) {
+      (&fs.wcnt[0][0])[q] = 0;
+      (&fs.wtok[0][0])[q] = 0;
+    }
+    __syncthreads();
+    int rk[3];
+    int64_t tp[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      int gcnt;
+      int64_t gtok;
+      bool last;
+      warp_bucket(ub[k], L, lane, rk[k], tp[k], last, gcnt, gtok);
+      if (last && ub[k] >= 0) { fs.wcnt[w][ub[k]] = gcnt; fs.wtok[w][ub[k]] = gtok; }
+    }
+    __syncthreads();
+    if (tid < U) {  // exclusive over warps, chunk totals
+      int64_t ac = 0, at = 0;
+      for (int ww = 0; ww < NT / 32; ++ww) {
+        const int64_t cc = fs.wcnt[ww][tid], tt = fs.wtok[ww][tid];
+        fs.wcnt[ww][tid] = (int32_t)ac;
+        fs.wtok[ww][tid] = at;
+        ac += cc;
+        at += tt;
+      }
+      fs.chunk_cnt[tid] = ac;
+      fs.chunk_tok[tid] = at;
+    }
+    __syncthreads();
+    if (ok) {
+      int64_t grank[3], gtp[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const int u = ub[k] < 0 ? 0 : ub[k];
+        grank[k] = fs.run_cnt[u] + fs.wcnt[w][u] + rk[k];
+        gtp[k] = fs.run_tok[u] + fs.wtok[w][u] + tp[k];
+      }
+      // layouts: sorted position, local offset, held-length scan
+      const int64_t ps = fs.gstart[0][gs] + grank[1], pd = fs.gstart[1][gd] + grank[2];
+      a.perm[0][ps] = (int32_t)i;
+      a.perm[1][pd] = (int32_t)i;
+      a.off[0][i] = gtp[1];
+      a.off[1][i] = gtp[2];
+      a.cum[0][ps] = fs.gtok0[0][gs] + gtp[1];
+      a.cum[1][pd] = fs.gtok0[1][gd] + gtp[2];
+      if (pos_s) { a.pos[0][i] = (int32_t)grank[1]; a.gpos[0][i] = gtp[1]; }
+      if (pos_d) { a.pos[1][i] = (int32_t)grank[2]; a.gpos[1][i] = gtp[2]; }
+      a.pbase[i] = L > 0 ? grank[0] : 0;  // (diagnostic: piece rank inside its key)
+      if (L > 0) {
+        const int key = ub[0];
+        for (int ts = 0; ts < nts; ++ts) {
+          const int s = S.rank0 + gs * S.tp + ts;
+          const int64_t j = tb.rbase[s][gd] + grank[0];
+          a.rec.seq[j] = (int32_t)i;
+          a.rec.x[j] = 0;
+          a.rec.n[j] = (int32_t)L;
+          a.rec.code[j] = (uint32_t)s | ((uint32_t)gs << 8) | ((uint32_t)gd << 16) | ((uint32_t)ts << 24);
+          a.rec.src_tok[j] = gtp[1];
+          a.rec.dst_tok[j] = gtp[2];
+          a.rec.msg_tok[j] = gtp[0];
+          a.rec.tok_prefix[j] = tb.tbase[s][gd] + gtp[0];
+        }
+        (void)key;
+      }
+    }
+    __syncthreads();
+    if (tid < U) { fs.run_cnt[tid] += fs.chunk_cnt[tid]; fs.run_tok[tid] += fs.chunk_tok[tid]; }
   }
   stamp(a, 7);
 }
@@ -793,22 +1129,26 @@ __global__ void local_meta_kernel(const __grid_constant__ PlanArgs a, int g, int
 
 // Grid size: one CTA per 4096 items (sequences or pieces), at most what can be co-resident.
 // EARL_PLAN_GRID=<g> forces g (tests use it to check that the plan does not depend on G).
-int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem) {
+int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem, bool fast) {
   static int per_sm = -1;
-  static int forced = -2;
-  static bool opted[64] = {};
+  static bool opted[64] = {}, opted_fast[64] = {};
   opt_in_dynamic_smem(planner_kernel, 64 * 1024, opted);
+  opt_in_dynamic_smem(planner_sp1_kernel, 64 * 1024, opted_fast);
   if (per_sm < 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, planner_kernel, NT, 64 * 1024) !=
-        cudaSuccess)
-      per_sm = 1;
+    int p1 = 1, p2 = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p1, planner_kernel, NT, 64 * 1024) != cudaSuccess)
+      p1 = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p2, planner_sp1_kernel, NT, 64 * 1024) != cudaSuccess)
+      p2 = 1;
     (void)cudaGetLastError();
+    per_sm = p1 < p2 ? p1 : p2;
     if (per_sm < 1) per_sm = 1;
-    const char* e = getenv("EARL_PLAN_GRID");
-    forced = e ? atoi(e) : -1;
   }
+  const char* env = getenv("EARL_PLAN_GRID");
+  const int forced = env ? atoi(env) : -1;
   const int64_t work = n_seqs > max_pieces ? n_seqs : max_pieces;
-  int64_t g = forced > 0 ? forced : (work + 4095) / 4096;
+  // the fast path's phases are one elementwise pass each: one CTA per 1024 sequences (a chunk)
+  int64_t g = forced > 0 ? forced : fast ? (n_seqs + 1023) / 1024 : (work + 4095) / 4096;
   const int64_t cap = (int64_t)sm_count * per_sm;
   if (g > cap) g = cap;
   if (g > kMaxPlanGrid) g = kMaxPlanGrid;
@@ -817,17 +1157,18 @@ int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_sm
   return (int)g;
 }
 
-cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, cudaStream_t s) {
-  static bool configured[64] = {};
+cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, bool fast, cudaStream_t s) {
+  static bool configured[64] = {}, configured_fast[64] = {};
   cudaError_t e = opt_in_dynamic_smem(planner_kernel, 64 * 1024, configured);
+  if (e == cudaSuccess) e = opt_in_dynamic_smem(planner_sp1_kernel, 64 * 1024, configured_fast);
   if (e != cudaSuccess) return e;
+  auto kern = fast ? planner_sp1_kernel : planner_kernel;
   if (grid == 1) {
-    planner_kernel<<<1, NT, lpt_smem, s>>>(a);
+    kern<<<1, NT, lpt_smem, s>>>(a);
     return cudaGetLastError();
   }
   void* args[] = {const_cast<PlanArgs*>(&a)};
-  return cudaLaunchCooperativeKernel((const void*)planner_kernel, dim3(grid), dim3(NT), args,
-                                     lpt_smem, s);
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(NT), args, lpt_smem, s);
 }
 
 cudaError_t launch_local_meta(const PlanArgs& a, int g, int k, int32_t* cu, int64_t* ids,

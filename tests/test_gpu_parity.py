@@ -778,3 +778,50 @@ def test_returns_repeat_and_graph(graph):
     """The look-back workspace is reused across launches and graph replays (device epoch)."""
     lens = W.lognormal_lengths(200, 1500, 0.8, 1, 6000, seed=9).tolist()
     _adv_case(lens, W.layout(dp=4, tp=2, assign="lpt"), 0.99, 8, repeats=5, graph=graph)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_sp1_fast_planner_equals_general_planner(seed, monkeypatch):
+    """The SP = 1 single-pass planner (planner_sp1_kernel) and the general phased planner give
+    the same plan, header tables and records included (earl_plan_hash), and the oracle's
+    segment table -- for random SP = 1 layout pairs of every assignment rule, N up to 40K
+    (multi-CTA grids), zero-length sequences and forced grid sizes."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    rng = random.Random(9100 + seed)
+    world = rng.randint(1, 8)
+    n = rng.choice([0, 1, 7, rng.randint(1, 600), rng.randint(600, 5000), rng.randint(5000, 40000)])
+    lens = [rng.choice([0, 1, rng.randint(0, 300), rng.randint(0, 9000)]) for _ in range(n)]
+
+    def sp1(lay):
+        lay = dict(lay, sp=1)
+        if lay["assign"] == "lpt" and n > 8192:
+            lay["assign"] = "contig"
+        lay["sp_split"] = rng.choice(["block", "flat", "threshold"])
+        lay["sp_min_len"] = rng.randint(0, 500)
+        return lay
+
+    src, dst = sp1(random_layout(rng, world, n)), sp1(random_layout(rng, world, n))
+    if src["assign"] == "given_counts" and src["counts"] is None:
+        src["counts"] = W.near_equal_counts(n, src["dp"])
+    fields = [("a", 4, 1, "x"), ("b", 2, 3, "x")]
+    ed = EmulatedDispatch(world)
+    lens_dev = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+    if seed % 4 == 3:
+        monkeypatch.setenv("EARL_PLAN_GRID", str(rng.choice([1, 2, 5, 17])))
+    monkeypatch.setenv("EARL_PLAN_PATH", "general")
+    pg = ed.plan(src, dst, lens_dev, fields)
+    monkeypatch.delenv("EARL_PLAN_PATH")
+    pf = ed.plan(src, dst, lens_dev, fields)
+    assert pf.hash() == pg.hash()
+    if n <= 5000:
+        assert pf.export() == O.route(src, dst, lens, world)
+    dst_ranks = range(dst["rank0"], dst["rank0"] + dst["dp"] * dst["sp"] * dst["tp"])
+    for r in dst_ranks:
+        cu_f, ids_f, ts_f = ed.meta(pf, r)
+        cu_g, ids_g, ts_g = ed.meta(pg, r)
+        assert cu_f.cpu().tolist() == cu_g.cpu().tolist()
+        assert ids_f.cpu().tolist() == ids_g.cpu().tolist()
+        assert ts_f.cpu().tolist() == ts_g.cpu().tolist()
+    pf.destroy()
+    pg.destroy()
