@@ -50,6 +50,14 @@ __device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
   if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
 }
 
+// gate (AggArgs::gate) on the batch's longest sequence, read on the device: lets the host launch
+// both returns kernels when it does not know the batch (one of them exits at once)
+__device__ __forceinline__ bool gated_out(const AggArgs& a) {
+  if (a.gate == 0) return false;
+  const int64_t m = *reinterpret_cast<const volatile int64_t*>(&a.hdr->max_len);
+  return a.gate == 1 ? m > kUnitMaxLen : m <= kUnitMaxLen;
+}
+
 __device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
   uint64_t v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -99,7 +107,7 @@ struct RankTable {
 
 // The window size adapts to the batch: 4096 tokens once there are two windows per warp of
 // the grid, down to one 512-token batch for small batches (every warp busy, short chains).
-__device__ void rank_table(const AggArgs& a, RankTable& rt, int64_t warps) {
+__device__ void rank_table(const AggArgs& a, RankTable& rt, int64_t warps, int nb_fixed = 0) {
   const PlanHeader* h = a.hdr;
   const LayoutDesc& S = a.plan.lay[0];
   rt.n = 0;
@@ -118,7 +126,7 @@ __device__ void rank_table(const AggArgs& a, RankTable& rt, int64_t warps) {
     batches += (rt.ntok[n] + kBatch - 1) / kBatch;
     rt.n = n + 1;
   }
-  rt.nb = (int)max((int64_t)1, min((int64_t)kMaxNB, batches / (2 * warps)));
+  rt.nb = nb_fixed > 0 ? nb_fixed : (int)max((int64_t)1, min((int64_t)kMaxNB, batches / (2 * warps)));
   const int64_t win = (int64_t)kBatch * rt.nb;
   rt.wbeg[0] = 0;
   for (int n = 0; n < rt.n; ++n) rt.wbeg[n + 1] = rt.wbeg[n] + (rt.ntok[n] + win - 1) / win;
@@ -441,6 +449,7 @@ __device__ __forceinline__ void returns_epilogue(const AggArgs& a, const RankTab
 }
 
 __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const __grid_constant__ AggArgs a) {
+  if (gated_out(a)) return;
   __shared__ RankTable rt;
   __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
   __shared__ float2 bmap[kWarps][kMaxNB];   // per batch: its map (pass 1), then its carry
@@ -639,6 +648,379 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
 }
 
+// ---------------------------------------------------------------------------------------
+// returns_units_kernel: single pass, no look-back.  A unit is the run of whole sequences that
+// start in [k * 4096, (k+1) * 4096) of a rank's buffer (the last unit also takes the trailing
+// zero-length ones), so no return crosses a unit boundary: a warp claims a unit and streams it
+// right to left in 512-token batches through a 3-slot TMA ring (2 batches ahead), composing each
+// batch's lane maps and applying the carry from the batch to its right in registers -- every
+// token read once from HBM and written once, no second pass, no published window maps.  Batches
+// that straddle a unit boundary are loaded lane by lane over the unit's own tokens only.  The
+// unit -> first sequence table comes from unit_table_kernel (one pass over the sequences).
+// Used when the batch's longest sequence is known to be <= kUnitMaxLen (a longer one would be
+// streamed by a single warp); otherwise returns_kernel.
+// ---------------------------------------------------------------------------------------
+
+#ifndef EARL_AGG_USLOTS
+#define EARL_AGG_USLOTS 3
+#endif
+constexpr int kUSlots = EARL_AGG_USLOTS;
+#ifndef EARL_AGG_UCTAS
+#define EARL_AGG_UCTAS 3
+#endif
+constexpr int kUCtasPerSm = EARL_AGG_UCTAS;
+
+// this lane's 16 tokens [t, t+16) restricted to [lo, hi): vector loads when whole and aligned
+__device__ __forceinline__ void load_batch_in(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
+                                              int64_t lo, int64_t hi, bool vec) {
+  if (vec && t >= lo && t + kTokLane <= hi) {
+    const float4* rp = reinterpret_cast<const float4*>(rw + t);
+    const uint4* mp = reinterpret_cast<const uint4*>(mk + t);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) B.r[k] = __ldcs(rp + k);
+    B.m = __ldcs(mp);
+    return;
+  }
+  // fully unrolled, predicated: the 32 loads issue back to back (a rolled loop through a local
+  // array serialised them, ~one memory latency per token)
+  float x[kTokLane];
+  uint32_t m[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < kTokLane; ++i) {
+    const bool in = t + i >= lo && t + i < hi;
+    x[i] = in ? rw[t + i] : 0.f;
+    m[i >> 2] |= (in ? (uint32_t)mk[t + i] : 0u) << (8 * (i & 3));
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) B.r[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+  B.m = make_uint4(m[0], m[1], m[2], m[3]);
+}
+
+// bit k (k < 4) set for every nonzero byte k of w (mask bytes: any nonzero byte is 1, reading n5)
+__device__ __forceinline__ uint32_t nonzero_bytes4(uint32_t w) {
+  const uint32_t nz = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
+  return (nz * 0x00204081u) >> 28;  // bytes' high bits 7, 15, 23, 31 -> bits 28..31
+}
+
+// Per-warp ring of SLOTS batches.  A batch's tokens inside [lo, hi) arrive by TMA bulk copies
+// (rewards from a 4-token boundary, mask from a 16-token boundary: the extra tokens of the
+// granules are masked by the consumer), so the boundary batches of a unit are prefetched like
+// the others; an unaligned buffer, or a granule past the rank buffer's end, falls back to lane
+// loads in get().
+template <int SLOTS>
+struct UnitRing {
+  uint8_t* mem;
+  uint64_t* bar;
+  uint32_t issued, got;
+  bool tma[SLOTS];
+
+  __device__ __forceinline__ void init(uint8_t* m, uint64_t* b, int lane) {
+    mem = m; bar = b; issued = got = 0;
+    for (int s = 0; s < SLOTS; ++s) tma[s] = false;
+    if (lane == 0) {
+      for (int s = 0; s < SLOTS; ++s)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  // batch [t0, t0 + kBatch) of a rank buffer of ntok tokens, restricted to [lo, hi)
+  __device__ __forceinline__ void issue(const float* rw, const uint8_t* mk, int64_t t0, int64_t lo,
+                                        int64_t hi, int64_t ntok, bool vec, int lane) {
+    const int s = issued % SLOTS;
+    const int64_t a = max(t0, lo), b = min(t0 + kBatch, hi);
+    const int64_t r0 = a & ~3LL, r1 = (b + 3) & ~3LL, m0 = a & ~15LL, m1 = (b + 15) & ~15LL;
+    const bool ok = vec && a < b && r1 <= ntok && m1 <= ntok;
+    tma[s] = ok;
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t bar_s = smem_addr(&bar[s]);
+      if (ok) {
+        uint8_t* dst = mem + s * kSlotBytes;
+        const uint32_t rb = (uint32_t)(r1 - r0) * 4u, mb = (uint32_t)(m1 - m0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s),
+                     "r"(rb + mb) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(dst + (r0 - t0) * 4)), "l"(rw + r0), "r"(rb), "r"(bar_s) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(dst + kBatch * 4 + (m0 - t0))), "l"(mk + m0), "r"(mb), "r"(bar_s)
+            : "memory");
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
+      }
+    }
+    ++issued;
+  }
+  // this lane's 16 tokens (starting at t) of the oldest issued batch; tokens outside [lo, hi)
+  // may hold anything (the caller masks them)
+  __device__ __forceinline__ void get(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
+                                      int64_t lo, int64_t hi, bool vec, int lane) {
+    const int s = got % SLOTS;
+    const uint32_t parity = (got / SLOTS) & 1;
+    const uint32_t b = smem_addr(&bar[s]);
+    uint32_t done;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          " selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done) : "r"(b), "r"(parity) : "memory");
+    } while (!done);
+    ++got;
+    if (!tma[s]) {
+      load_batch_in(B, rw, mk, t, lo, hi, vec);
+      return;
+    }
+    const uint8_t* rb = mem + s * kSlotBytes + 64 * lane;
+    const int rot = (lane >> 1) & 3;
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
+    float4 u[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) B.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
+    B.m = *reinterpret_cast<const uint4*>(mem + s * kSlotBytes + kBatch * 4 + 16 * lane);
+  }
+};
+
+// unit -> first sequence (sorted position p in [gs, pend]) of every unit of every source rank of
+// the launch: unit k of a rank starts at the first sequence whose start is >= k * kUnitTok.
+__global__ void unit_table_kernel(const __grid_constant__ AggArgs a) {
+  if (gated_out(a)) return;
+  __shared__ RankTable rt;
+  if (threadIdx.x == 0) rank_table(a, rt, 1, kUnitTok / kBatch);
+  __syncthreads();
+  if (rt.wbeg[rt.n] > a.win_cap) return;  // the unit kernel latches CAPACITY
+  const int64_t* cum = a.plan.cum[0];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  for (int ri = 0; ri < rt.n; ++ri) {
+    const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
+    if (nu == 0) continue;
+    const int64_t base = cum[gs];
+    int64_t* tab = a.unit_first + rt.wbeg[ri];
+    for (int64_t p = gs + tid; p <= pend; p += nth) {
+      const int64_t s = cum[p] - base;                   // start of sequence p (ntok for pend)
+      const int64_t kl = p == gs ? 0 : (cum[p - 1] - base) / kUnitTok + 1;
+      int64_t kh = s / kUnitTok;
+      if (p == pend || kh > nu - 1) kh = nu - 1;
+      for (int64_t k = kl; k <= kh; ++k) tab[k] = p;
+    }
+  }
+}
+
+// per-sequence return G_0 of sequences [p0, p1) (written by this warp: the caller syncs)
+__device__ __forceinline__ void unit_seq_returns(float* SR, const float* G, const int64_t* cum,
+                                                 int64_t base, int64_t gs, int64_t p0, int64_t p1,
+                                                 int lane) {
+  if (SR == nullptr) return;
+  for (int64_t p = p0 + lane; p < p1; p += 32) {
+    const int64_t s = cum[p] - base;
+    const int64_t L = cum[p + 1] - base - s;
+    SR[p - gs] = L > 0 ? G[s] : 0.f;
+  }
+}
+
+// One claimed unit as the warp sees it.
+struct UnitInfo {
+  int64_t p0, p1, ua, ub, bf, bl, base;
+  int ri, r, valid;
+};
+
+__global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_kernel(const __grid_constant__ AggArgs a) {
+  __shared__ RankTable rt;
+  __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
+  __shared__ double red[3][32];
+  extern __shared__ __align__(128) uint8_t uring_mem[];  // [kWarps][kUSlots][kSlotBytes]
+  __shared__ uint64_t uring_bar[kWarps][kUSlots];
+  __shared__ int s_ok;
+  __shared__ UnitInfo s_next[kWarps];  // every warp's early-claimed unit (lane 0 writes it)
+  if (gated_out(a)) return;
+  if (threadIdx.x == 0) {
+    rank_table(a, rt, 1, kUnitTok / kBatch);
+    s_ok = rt.wbeg[rt.n] <= a.win_cap;
+    if (!s_ok && blockIdx.x == 0)
+      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(rt.wbeg[rt.n], (int64_t)INT32_MAX));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
+  const float gamma = a.gamma;
+  const float g16 = a.gamma16;
+  uint32_t* bm = ends_bm[wid];
+  double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
+  UnitRing<kUSlots> ring;
+  ring.init(uring_mem + (size_t)wid * kUSlots * kSlotBytes, uring_bar[wid], lane);
+  const int64_t* cum = a.plan.cum[0];
+  UnitInfo& nx = s_next[wid];
+
+  // lane 0 claims the next unit and resolves its token range into this warp's shared slot
+  auto claim_next = [&]() {
+    if (lane == 0) {
+      const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
+      nx.valid = u < total;
+      if (u < total) {
+        int ri = 0;
+        while (u >= rt.wbeg[ri + 1]) ++ri;
+        const int64_t k = u - rt.wbeg[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
+        const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
+        const int64_t p0 = a.unit_first[u], p1 = k + 1 < nu ? a.unit_first[u + 1] : pend;
+        const int64_t base = cum[gs];
+        const int64_t ua = cum[p0] - base, ub = cum[p1] - base;
+        nx.ri = ri;
+        nx.r = rt.rank[ri];
+        nx.p0 = p0;
+        nx.p1 = p1;
+        nx.base = base;
+        nx.ua = ua;
+        nx.ub = ub;
+        nx.bf = ua / kBatch;
+        nx.bl = ua < ub ? (ub - 1) / kBatch : ua / kBatch - 1;  // no batches for an empty unit
+      }
+    }
+    __syncwarp();
+  };
+
+  // Producer: issues batches right to left through the claimed units, kUSlots - 1 ahead of the
+  // consumer; it claims the next unit as soon as the current one is fully issued, so the next
+  // unit's first batches load while this one finishes (units carry nothing between them: there
+  // is no look-back to wait for).
+  claim_next();
+  UnitInfo cu = nx;  // the unit being consumed
+  bool nx_claimed = false;
+  bool p_next = false;   // producer: issuing nx (else cu)
+  int64_t pb = cu.bl;    // producer: next batch to issue
+  auto produce = [&]() {
+    if (!p_next) {
+      if (!cu.valid) return;
+      if (pb >= cu.bf) {
+        const int r = cu.r;
+        const bool vec = aligned(a.rewards[r], 16) && aligned(a.mask[r], 16);
+        ring.issue(a.rewards[r], a.mask[r], pb * kBatch, cu.ua, cu.ub, rt.ntok[cu.ri], vec, lane);
+        --pb;
+        return;
+      }
+      if (!nx_claimed) { claim_next(); nx_claimed = true; }
+      p_next = true;
+      pb = nx.bl;
+    }
+    if (!nx.valid || pb < nx.bf) return;
+    const int r = nx.r;
+    const bool vec = aligned(a.rewards[r], 16) && aligned(a.mask[r], 16);
+    ring.issue(a.rewards[r], a.mask[r], pb * kBatch, nx.ua, nx.ub, rt.ntok[nx.ri], vec, lane);
+    --pb;
+  };
+  for (int d = 0; d < kUSlots - 1; ++d) produce();
+
+  while (cu.valid) {
+    const int r = cu.r;
+    const int64_t ntok_r = rt.ntok[cu.ri];
+    (void)ntok_r;
+    float* G = a.returns[r];
+    const float* rw = a.rewards[r];
+    const uint8_t* mk = a.mask[r];
+    const bool vec = aligned(rw, 16) && aligned(G, 16) && aligned(mk, 16);
+    const bool count_stats = rt.t[cu.ri] == 0;
+    const int64_t ua = cu.ua, ub = cu.ub;
+    float carry = 0.f;  // G right of the unit: its last token ends a sequence
+    int64_t seg_lo = 0;
+#pragma unroll 1
+    for (int64_t bb = cu.bl; bb >= cu.bf; --bb) {
+      if ((cu.bl - bb) % kMaxNB == 0) {  // a new segment of <= 8 batches: its sequence ends
+        seg_lo = max(cu.bf, bb - (kMaxNB - 1));
+        const int nb = (int)(bb - seg_lo + 1);
+        mark_ends(bm, nb * (kBatch / 32), cum, cu.base, cu.p0, cu.p1, seg_lo * kBatch,
+                  min(ub, (bb + 1) * kBatch), lane);
+      }
+      const int64_t lt = bb * kBatch + (int64_t)kTokLane * lane;
+      Batch cur;
+      ring.get(cur, rw, mk, lt, ua, ub, vec, lane);
+      produce();
+      const int bi = (int)(bb - seg_lo);
+      const uint32_t e = (bm[16 * bi + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu;
+      // this lane's tokens inside the unit, and the masked-in ones among them
+      uint32_t in16 = 0xffffu;
+      if (lt < ua) in16 &= lt + kTokLane <= ua ? 0u : (0xffffu << (uint32_t)(ua - lt)) & 0xffffu;
+      if (lt + kTokLane > ub) in16 &= lt >= ub ? 0u : 0xffffu >> (uint32_t)(lt + kTokLane - ub);
+      const uint32_t on16 = in16 & (nonzero_bytes4(cur.m.x) | nonzero_bytes4(cur.m.y) << 4 |
+                                    nonzero_bytes4(cur.m.z) << 8 | nonzero_bytes4(cur.m.w) << 12);
+      float v[kTokLane];
+#pragma unroll
+      for (int i = 0; i < kTokLane; ++i) v[i] = (on16 >> i) & 1u ? tok_r(cur, i) : 0.f;
+      float out[kTokLane];
+      float rS, rP, bS, bP;
+      if (!__any_sync(kFull, e != 0u)) {
+        // no sequence ends in the batch (most batches: sequences are ~thousands of tokens):
+        // every slope is gamma, no per-token selects
+        float S = 0.f;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(gamma, S, v[i]);
+        warp_compose(S, g16, lane, rS, rP, bS, bP);
+        float g_next = rS + rP * carry;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) {
+          out[i] = fmaf(gamma, g_next, v[i]);
+          g_next = out[i];
+        }
+      } else {
+        float S = 0.f;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, v[i]);
+        warp_compose(S, e ? 0.f : g16, lane, rS, rP, bS, bP);
+        float g_next = rS + rP * carry;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) {
+          out[i] = fmaf(((e >> i) & 1u) ? 0.f : gamma, g_next, v[i]);
+          g_next = out[i];
+        }
+      }
+      if (count_stats) {
+        float sg = 0.f, sg2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i) {
+          const float o = (on16 >> i) & 1u ? out[i] : 0.f;
+          sg += o;
+          sg2 = fmaf(o, o, sg2);
+        }
+        s_m += (double)__popc(on16);
+        s_g += (double)sg;
+        s_g2 += (double)sg2;
+      }
+      if (vec && in16 == 0xffffu) {
+        float4* gp = reinterpret_cast<float4*>(G + lt);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          __stcs(gp + q, make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i)
+          if ((in16 >> i) & 1u) G[lt + i] = out[i];
+      }
+      carry = bS + bP * carry;
+    }
+    __syncwarp();
+    unit_seq_returns(a.seq_return[r], G, cum, cu.base, rt.gs[cu.ri], cu.p0, cu.p1, lane);
+    __syncwarp();
+    // move on to the early-claimed unit (or claim one now)
+    if (!nx_claimed) { claim_next(); pb = nx.bl; p_next = true; }
+    cu = nx;
+    nx_claimed = false;
+    p_next = false;  // pb continues where the producer was in this unit
+    // keep kUSlots - 1 batches in flight
+    while (cu.valid && (int)(ring.issued - ring.got) < kUSlots - 1) {
+      const uint32_t before = ring.issued;
+      produce();
+      if (ring.issued == before) break;
+    }
+  }
+  returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
+}
+
 // A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks: one
 // flattened stream of 4-token quads over all ranks (4 quads in flight per thread), then the
 // unaligned remainders token by token.  Measured on the C5-lt batch: read-only-path loads
@@ -714,6 +1096,18 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
 }  // namespace
 
 int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWin + 16384; }
+
+cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s) {
+  unit_table_kernel<<<sm_count, 256, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  constexpr size_t kRingBytes = (size_t)kWarps * kUSlots * kSlotBytes;
+  static bool opted[64] = {};
+  e = opt_in_dynamic_smem(returns_units_kernel, (int)kRingBytes, opted);
+  if (e != cudaSuccess) return e;
+  returns_units_kernel<<<sm_count * kUCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
   // the batch ring: kSlots x 2.5 KB per warp of dynamic shared memory; with the static arrays

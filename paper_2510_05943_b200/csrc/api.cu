@@ -1576,7 +1576,8 @@ earl_status_t agg_workspace(earl_plan_t p, cudaStream_t s) {
     CUDA_TRY(cudaFree(p->agg_ws));
     p->agg_ws = nullptr;
   }
-  const size_t bytes = sizeof(AggWork) + sizeof(AggWindow) * (size_t)need;
+  // AggWork | AggWindow[need] (windowed kernel) | int64 unit_first[need] (unit kernel)
+  const size_t bytes = sizeof(AggWork) + (sizeof(AggWindow) + sizeof(int64_t)) * (size_t)need;
   CUDA_TRY(cudaMalloc(&p->agg_ws, bytes));
   p->agg_cap = need;
   CUDA_TRY(cudaMemsetAsync(p->agg_ws, 0, bytes, s));
@@ -1624,8 +1625,29 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   a.ws = static_cast<AggWork*>(p->agg_ws);
   a.win = reinterpret_cast<AggWindow*>(a.ws + 1);
   a.win_cap = p->agg_cap;
-  use_begin(p, static_cast<cudaStream_t>(stream));
-  cudaError_t e = launch_returns(a, p->comm->sm_count, static_cast<cudaStream_t>(stream));
+  a.unit_first = reinterpret_cast<int64_t*>(a.win + p->agg_cap);
+  // the single-pass unit kernel when the host knows the batch has no sequence longer than
+  // kUnitMaxLen tokens (one warp streams a unit); otherwise the windowed look-back kernel.
+  // EARL_RETURNS=units|windows forces one (tests).
+  // When the host does not know the batch (the plan was re-planned since its last sync), both
+  // are launched and each checks the planner's max_len on the device (one exits at once).
+  const char* force = getenv("EARL_RETURNS");
+  int which = p->synced ? (p->host_hdr.max_len <= kUnitMaxLen ? 1 : 2) : 3;
+  if (force && std::strcmp(force, "units") == 0) which = 1;
+  if (force && std::strcmp(force, "windows") == 0) which = 2;
+  cudaStream_t rs = static_cast<cudaStream_t>(stream);
+  use_begin(p, rs);
+  cudaError_t e = cudaSuccess;
+  if (which & 1) {
+    a.gate = which == 3 ? 1 : 0;
+    e = launch_returns_units(a, p->comm->sm_count, rs);
+    if (e == cudaSuccess) g_launches.fetch_add(1);  // + the unit table kernel
+  }
+  if (e == cudaSuccess && (which & 2)) {
+    a.gate = which == 3 ? 2 : 0;
+    e = launch_returns(a, p->comm->sm_count, rs);
+    if (e == cudaSuccess && which == 3) g_launches.fetch_add(1);
+  }
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "returns launch: %s", cudaGetErrorString(e));
   g_launches.fetch_add(1);
   const bool synced = p->synced;

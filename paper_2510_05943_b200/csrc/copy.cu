@@ -26,18 +26,14 @@ __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   *reinterpret_cast<uint4*>(p) = v;
 }
 
-// 16 bytes starting at byte sh (1..15) of the 32-byte pair (A, B).  s4 = sh/4 and
-// bits = 8*(sh%4) are warp-uniform (they depend on the source address only).
-__device__ __forceinline__ uint4 realign(const uint4& A, const uint4& B, int s4, int bits) {
-  uint32_t v0, v1, v2, v3, v4;
-  switch (s4) {
-    case 0: v0 = A.x; v1 = A.y; v2 = A.z; v3 = A.w; v4 = B.x; break;
-    case 1: v0 = A.y; v1 = A.z; v2 = A.w; v3 = B.x; v4 = B.y; break;
-    case 2: v0 = A.z; v1 = A.w; v2 = B.x; v3 = B.y; v4 = B.z; break;
-    default: v0 = A.w; v1 = B.x; v2 = B.y; v3 = B.z; v4 = B.w; break;
-  }
-  return make_uint4(__funnelshift_r(v0, v1, bits), __funnelshift_r(v1, v2, bits),
-                    __funnelshift_r(v2, v3, bits), __funnelshift_r(v3, v4, bits));
+// 16 bytes starting at byte sh (1..15) of the 32-byte pair (A, B): S4 = sh/4 (a template
+// parameter: the word selection is resolved at compile time, the loop below is instantiated per
+// S4 instead of switching per 16 B) and bits = 8*(sh%4), warp-uniform.
+template <int S4>
+__device__ __forceinline__ uint4 realign(const uint4& A, const uint4& B, int bits) {
+  const uint32_t w[8] = {A.x, A.y, A.z, A.w, B.x, B.y, B.z, B.w};
+  return make_uint4(__funnelshift_r(w[S4], w[S4 + 1], bits), __funnelshift_r(w[S4 + 1], w[S4 + 2], bits),
+                    __funnelshift_r(w[S4 + 2], w[S4 + 3], bits), __funnelshift_r(w[S4 + 3], w[S4 + 4], bits));
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -478,6 +474,22 @@ __device__ __forceinline__ bool fill_stage(const CopyArgs& a, const View& v, Wal
   return true;
 }
 
+// The realigning warp-store loop of a non-congruent range: 16-B outputs k = lane, lane + 32, ...
+// from the 32 bytes at sp + 16 (k - lane), one st.global.v4 per replica.
+template <int R, int S4>
+__device__ __forceinline__ void realign_loop(uint8_t* (&q)[R], const uint8_t* sp, uint32_t nvec,
+                                             int bits, int lane) {
+#pragma unroll 2
+  for (uint32_t k = lane; k < nvec; k += 32) {
+    const uint4 w0 = *reinterpret_cast<const uint4*>(sp);
+    const uint4 w1 = *reinterpret_cast<const uint4*>(sp + 16);
+    const uint4 o = realign<S4>(w0, w1, bits);
+#pragma unroll
+    for (int r = 0; r < R; ++r) { st_v4(q[r], o); q[r] += 512; }
+    sp += 512;
+  }
+}
+
 // Store one landed source range to its R destination replicas (whole warp); R is a
 // compile-time constant so the replica pointers stay in registers and the realign loop is
 // ~12 instructions per 512 B (a runtime-R loop cost ~100: profiles/r01_c5lt_note.txt).
@@ -528,19 +540,16 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
       }
     } else {
       const uint32_t sh = smo & 15;
-      const int s4 = (int)(sh >> 2), bits = (int)(sh & 3) * 8;
+      const int bits = (int)(sh & 3) * 8;
       const uint8_t* sp = stage + (smo & ~15u) + 16 * lane;
       uint8_t* q[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) q[r] = dp[r] + head + 16 * lane;
-#pragma unroll 2
-      for (uint32_t k = lane; k < nvec; k += 32) {
-        const uint4 w0 = *reinterpret_cast<const uint4*>(sp);
-        const uint4 w1 = *reinterpret_cast<const uint4*>(sp + 16);
-        const uint4 o = realign(w0, w1, s4, bits);
-#pragma unroll
-        for (int r = 0; r < R; ++r) { st_v4(q[r], o); q[r] += 512; }
-        sp += 512;
+      switch (sh >> 2) {
+        case 0: realign_loop<R, 0>(q, sp, nvec, bits, lane); break;
+        case 1: realign_loop<R, 1>(q, sp, nvec, bits, lane); break;
+        case 2: realign_loop<R, 2>(q, sp, nvec, bits, lane); break;
+        default: realign_loop<R, 3>(q, sp, nvec, bits, lane); break;
       }
     }
   }

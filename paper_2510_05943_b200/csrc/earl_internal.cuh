@@ -48,6 +48,7 @@ struct PlanHeader {
   int64_t rec_tok_begin[kMaxWorld + 1];     // tokens of those records (prefix)
   int64_t rec_base[kMaxWorld][kMaxShards];  // first record of block (s, ds)
   int64_t rec_tok_base[kMaxWorld][kMaxShards];
+  int64_t max_len;      // the batch's longest sequence (returns: unit kernel or windowed)
   uint32_t work_ctr;    // copy kernels: dynamic work-unit counter (reset by the last CTA)
   uint32_t fin_ctr;     // copy kernels: finished-CTA counter
 };
@@ -192,16 +193,20 @@ struct AggWindow {
   uint64_t pad;
 };
 struct AggWork {
-  uint32_t work_ctr;  // window claims (reset by the last CTA)
+  uint32_t work_ctr;  // window / unit claims (reset by the last CTA)
   uint32_t fin_ctr;   // finished CTAs
   uint32_t epoch;     // launches so far: flags of older launches never match
   uint32_t pad;
 };
+constexpr int kUnitTok = 4096;  // returns unit kernel: a unit = the sequences starting in [k*4096, (k+1)*4096)
+constexpr int64_t kUnitMaxLen = int64_t(1) << 17;  // ... used when no sequence is longer than this
 
 struct AggArgs {
   AggWork* ws;
   AggWindow* win;
   int64_t win_cap;
+  int64_t* unit_first;     // unit kernel: first sequence (sorted position) of every unit
+  int32_t gate;            // 0: run; 1: run only if hdr->max_len <= kUnitMaxLen; 2: only if >
   PlanArgs plan;
   const PlanHeader* hdr;
   int32_t world;
@@ -249,6 +254,7 @@ inline cudaError_t opt_in_dynamic_smem(F* func, int bytes, bool (&done)[64]) {
 
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
+cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s);
 int64_t returns_windows(int64_t tokens);
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem, bool fast);

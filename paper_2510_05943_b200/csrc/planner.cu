@@ -47,6 +47,15 @@ __device__ __forceinline__ void stamp(const PlanArgs& a, int k) {
   }
 }
 
+// The CTA's largest length into h->max_len (values >= 0).
+__device__ __forceinline__ void publish_max_len(PlanHeader* h, uint32_t m, unsigned* s_max) {
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0) atomicMax(s_max, m);
+  __syncthreads();
+  if (threadIdx.x == 0 && *s_max) atomicMax(reinterpret_cast<unsigned long long*>(&h->max_len),
+                                            (unsigned long long)*s_max);
+}
+
 __device__ __forceinline__ void gsync() {
   delay_inject(6);
   if (gridDim.x == 1) __syncthreads();
@@ -529,12 +538,18 @@ __global__ void __launch_bounds__(NT, 1) planner_kernel(const __grid_constant__ 
 
   // ---- phase 0: lengths, P, T -------------------------------------------------------
   stamp(a, 0);
+  __shared__ unsigned s_max;
+  if (tid == 0) s_max = 0;
+  __syncthreads();
+  uint32_t lmax = 0;
   for (int64_t i = gtid; i < N; i += gstride) {
     int32_t L = a.seq_lens[i];
     if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
     a.lens[i] = L;
     a.vtmp[i] = L;
+    lmax = max(lmax, (uint32_t)L);
   }
+  publish_max_len(h, lmax, &s_max);
   gsync();
   const int64_t T = scan_array(a.vtmp, a.P, N, a.cta_sums, sm_scan);
   if (lead && tid == 0) { a.P[N] = T; h->T = T; }
@@ -877,7 +892,11 @@ __global__ void __launch_bounds__(NT, 1) planner_sp1_kernel(const __grid_constan
 
   // ---- lengths, the CTA's token sum; P and T after one barrier ------------------------
   stamp(a, 0);
+  __shared__ unsigned s_max;
+  if (tid == 0) s_max = 0;
+  __syncthreads();
   int64_t part = 0;
+  uint32_t lmax = 0;
   for (int c = 0; c < nchunks; ++c) {
     const int64_t i = lo + (int64_t)c * NT + tid;
     if (i < hi) {
@@ -885,8 +904,10 @@ __global__ void __launch_bounds__(NT, 1) planner_sp1_kernel(const __grid_constan
       if (L < 0) { latch(h, EARL_ERR_INVALID_ARGUMENT, (int)i); L = 0; }
       a.lens[i] = L;
       part += L;
+      lmax = max(lmax, (uint32_t)L);
     }
   }
+  publish_max_len(h, lmax, &s_max);
   {
     int64_t tot;
     block_excl_scan(part, tot, sm_scan);
