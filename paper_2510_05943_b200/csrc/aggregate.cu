@@ -50,12 +50,27 @@ __device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
   if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
 }
 
-// gate (AggArgs::gate) on the batch's longest sequence, read on the device: lets the host launch
-// both returns kernels when it does not know the batch (one of them exits at once)
-__device__ __forceinline__ bool gated_out(const AggArgs& a) {
+// gate (AggArgs::gate) on the batch, read on the device: lets the host launch both returns
+// kernels when it does not know the batch (one of them exits at once).  Whole-CTA decision.
+__device__ bool gated_out(const AggArgs& a) {
   if (a.gate == 0) return false;
-  const int64_t m = *reinterpret_cast<const volatile int64_t*>(&a.hdr->max_len);
-  return a.gate == 1 ? m > kUnitMaxLen : m <= kUnitMaxLen;
+  __shared__ int s_out;
+  if (threadIdx.x == 0) {
+    const PlanHeader* h = a.hdr;
+    const LayoutDesc& S = a.plan.lay[0];
+    int64_t units = 0;
+    for (int r = 0; r < a.world; ++r) {
+      if (a.view_rank >= 0 && r != a.view_rank) continue;
+      const int q = r - S.rank0;
+      if (q < 0 || q >= S.dp * S.tp) continue;
+      units += (*reinterpret_cast<const volatile int64_t*>(&h->shard_tokens[0][q / S.tp]) + kUnitTok - 1) / kUnitTok;
+    }
+    const int64_t m = *reinterpret_cast<const volatile int64_t*>(&h->max_len);
+    const bool units_best = prefer_units(m, units, a.resident_warps);
+    s_out = a.gate == 1 ? !units_best : units_best;
+  }
+  __syncthreads();
+  return s_out != 0;
 }
 
 __device__ __forceinline__ uint64_t ld_word(const uint64_t* p) {
@@ -861,6 +876,7 @@ __global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_kernel
 
   // lane 0 claims the next unit and resolves its token range into this warp's shared slot
   auto claim_next = [&]() {
+    delay_inject(8);
     if (lane == 0) {
       const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
       nx.valid = u < total;

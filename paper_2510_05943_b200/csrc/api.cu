@@ -1632,7 +1632,19 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   // When the host does not know the batch (the plan was re-planned since its last sync), both
   // are launched and each checks the planner's max_len on the device (one exits at once).
   const char* force = getenv("EARL_RETURNS");
-  int which = p->synced ? (p->host_hdr.max_len <= kUnitMaxLen ? 1 : 2) : 3;
+  a.resident_warps = (int64_t)p->comm->sm_count * kUnitWarpsPerSm;
+  int which = 3;
+  if (p->synced) {
+    const earl_layout_t& S = p->lay[0];
+    int64_t units = 0;
+    for (int r = 0; r < p->comm->world; ++r) {
+      if (!p->comm->emulated && r != p->comm->rank) continue;
+      const int q = r - S.rank0;
+      if (q < 0 || q >= S.dp * S.tp) continue;
+      units += (p->host_hdr.shard_tokens[0][q / S.tp] + kUnitTok - 1) / kUnitTok;
+    }
+    which = prefer_units(p->host_hdr.max_len, units, a.resident_warps) ? 1 : 2;
+  }
   if (force && std::strcmp(force, "units") == 0) which = 1;
   if (force && std::strcmp(force, "windows") == 0) which = 2;
   cudaStream_t rs = static_cast<cudaStream_t>(stream);

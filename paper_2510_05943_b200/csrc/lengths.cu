@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kThreads) gather_lengths_kernel(const __grid_c
       *a.ctr = 0;
       a.my_pad[kLensEpochSlot] = epoch;
     }
+    delay_inject(7);
     __threadfence_system();
     if (lane < a.world && lane != a.me) st_release_sys_u64(a.peer_pad[lane] + kLensSlot + a.me, epoch);
     unsigned missing = 0;

@@ -44,4 +44,29 @@ _adv_case([20_000, 3, 0, 1500, 7, 0], W.layout(dp=2, assign="given_counts", coun
 _adv_case([1 + (i % 5) for i in range(700)], W.layout(dp=3, tp=2, assign="lpt"), 0.9, 8, shift=1)
 _adv_case(W.lognormal_lengths(60, 900, 0.8, 1, 5000, seed=3).tolist(), W.layout(dp=4, assign="contig"),
           0.99, 4, repeats=2)
+# round 2: the returns unit kernel on the same cases (EARL_RETURNS=units), the general planner
+# on an SP = 1 layout (EARL_PLAN_PATH=general; the SP = 1 fast planner ran in every case above),
+# the emulated a1 gather, and a multi-CTA fast-planner grid with an LPT source
+os.environ["EARL_RETURNS"] = "units"
+_adv_case([20_000, 3, 0, 1500, 7, 0], W.layout(dp=2, assign="given_counts", counts=[3, 3]), 1.0, 4)
+_adv_case([1 + (i % 5) for i in range(700)], W.layout(dp=3, tp=2, assign="lpt"), 0.9, 8, shift=1)
+_adv_case(W.lognormal_lengths(600, 900, 0.8, 1, 5000, seed=3).tolist(), W.layout(dp=4, assign="contig"),
+          0.99, 4, repeats=2)
+del os.environ["EARL_RETURNS"]
+os.environ["EARL_PLAN_PATH"] = "general"
+run_gpu_case(W.rollout_layout(9000, 4), W.layout(dp=4, assign="explicit", group_of_seq=[i % 4 for i in range(9000)]),
+             lensN, fields, 4)
+del os.environ["EARL_PLAN_PATH"]
+run_gpu_case(W.layout(dp=3, assign="lpt"), W.layout(dp=2, tp=2, assign="contig"), lensN[:5000], fields, 4)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_2510_05943_b200.dispatch import EmulatedDispatch  # noqa: E402
+ed = EmulatedDispatch(4)
+cnts = [700, 0, 1301, 5]
+ln = np.random.default_rng(1).integers(0, 5000, size=sum(cnts)).astype(np.int32)
+edges = np.concatenate([[0], np.cumsum(cnts)])
+loc = [torch.as_tensor(ln[edges[r]:edges[r + 1]]).cuda() if cnts[r] else None for r in range(4)]
+got = ed.allgather_lens(loc, cnts)
+torch.cuda.synchronize()
+assert got.cpu().numpy().tolist() == ln.tolist()
 print("sanitize cases ok")

@@ -2,10 +2,10 @@
 
 For payload P per rank in 1 MiB .. 4 GiB, uniform (L = 4096) and long-tail (C2 distribution)
 lengths, scalar6-fp32 fields (series A) and +hidden2560 (series B, P >= 64 MiB):
-  * a2a  : earl_dispatch_plan + earl_dispatch_exec, DP8 -> DP8 EXPLICIT round-robin
+  * a2a  : earl_plan_replan + earl_dispatch_exec, DP8 -> DP8 EXPLICIT round-robin
            (uniform all-to-allv), i.e. the decentralized dispatch (PAPER.md:195-196);
   * cent : the centralized gather-and-dispatch baseline (reading c13): DP8 ->
-           DP1 on rank 0, then DP1 -> DP8, two plans + two execs.
+           DP1 on rank 0, then DP1 -> DP8, two replans + two execs.
 Times are CUDA-event medians with an L2 flush before every timed repetition.  Beside the
 measured (HBM-bound, one GPU) times it reports the NVLink model of SURVEY.md §8(d):
 t_a2a = max_r max(egress_r, ingress_r) / 770 GB/s, t_cent = (ingress_0 + egress_0) / 770 GB/s
@@ -58,7 +58,7 @@ def timed(fn, reps, flush):
 
 
 def main():
-    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
     dev = torch.device("cuda", 0)
     flush = torch.empty(512 * MiB, dtype=torch.uint8, device=dev)
     ed = EmulatedDispatch(R)
@@ -87,18 +87,18 @@ def main():
                 midb = ed.flat(ed.alloc_recv(p_1, fields))
                 recv2 = ed.flat(ed.alloc_recv(p_2, fields))
 
+                # steady state (the timed region allocates nothing): the plan
+                # objects are made once and every repetition re-plans the batch on the device
+                # (earl_plan_replan) before dispatching it
                 def a2a():
-                    q = ed.plan(src, dst, lens_dev, fields)
-                    q.exec(send, recv)
-                    q.destroy()
+                    p_a.replan(lens_dev)
+                    p_a.exec(send, recv)
 
                 def cent():
-                    q1 = ed.plan(src, mid, lens_dev, fields)
-                    q1.exec(send, midb)
-                    q2 = ed.plan(mid, dst, lens_dev, fields)
-                    q2.exec(midb, recv2)
-                    q1.destroy()
-                    q2.destroy()
+                    p_1.replan(lens_dev)
+                    p_1.exec(send, midb)
+                    p_2.replan(lens_dev)
+                    p_2.exec(midb, recv2)
 
                 for _ in range(2):
                     a2a(); cent()
@@ -132,8 +132,8 @@ def main():
 def write_md(rows, tag, path):
     head = [
         f"# C5 bandwidth sweep, {tag} (1 B200, 8-rank emulation; scripts/sweep.py)", "",
-        "a2a = plan + fused exec (DP8 -> DP8 round-robin all-to-allv); cent = centralized gather-and-dispatch "
-        "via rank 0 (two plans + two execs).",
+        "a2a = replan + fused exec (DP8 -> DP8 round-robin all-to-allv; the plan object made once, nothing "
+        "allocated in the timed region); cent = centralized gather-and-dispatch via rank 0 (two replans + two execs).",
         "Measured times are CUDA-event medians with an L2 flush before each repetition. On one GPU every byte "
         "moves through HBM, so the",
         "measured centralized/a2a ratio is ~2 (two passes). The NVLink columns are the SURVEY.md §8(d) model "
