@@ -171,6 +171,24 @@ EARL_API earl_status_t earl_comm_destroy(earl_comm_t comm);
  * evidence of the N-rank data plane).  Emulated comm: 0. */
 EARL_API earl_status_t earl_comm_peer_mask(earl_comm_t comm, uint32_t* mask);
 
+/* NEXT-3: NVLS multicast for TP-replicated destinations.  With EARL_NVLS=1 in
+ * the environment at earl_comm_create, a multi-process comm allocates its window with cuMemCreate
+ * (exported as a POSIX file descriptor that peers fetch with pidfd_getfd; export/import as
+ * above) and can bind it to multicast teams.  A team is a set of ranks (bit mask), normally the
+ * TP replicas of one destination shard: the lowest rank of the team calls earl_comm_mc_create
+ * (cuMulticastCreate over popcount(mask) devices; *handle_out, EARL_HANDLE_BYTES, to broadcast),
+ * then every rank of the comm calls earl_comm_mc_join with that handle (members add their device,
+ * bind their whole window at multicast offset 0 and map the multicast address -- concurrently:
+ * the bind waits for every member; other ranks return at once).  An exec whose destination shard
+ * has a team containing the sending rank, whose source layout has tp == 1 and whose members put
+ * the field at the same window offset stores the 16-B interior of each record once with
+ * multimem.st (NVSwitch writes every replica) instead of once per replica; heads and tails and
+ * everything else stay unicast.  Errors: UNSUPPORTED (no EARL_NVLS window, or the driver / device
+ * cannot create the team -- e.g. a box with one visible GPU), INVALID_ARGUMENT, CAPACITY (> 8
+ * teams). */
+EARL_API earl_status_t earl_comm_mc_create(earl_comm_t comm, uint32_t team_mask, void* handle_out);
+EARL_API earl_status_t earl_comm_mc_join(earl_comm_t comm, uint32_t team_mask, const void* handle);
+
 /* Step a1: the global length vector every rank plans from (the layout
  * knowledge of PAPER.md:178), gathered on the device.  Global order is rank-major (reading c6):
  * rank r's counts[r] lengths occupy [sum_{q<r} counts[q], +counts[r]) of the output.

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libearl_dispatch.so")
-SOURCES = ["api.cu", "planner.cu", "copy.cu", "aggregate.cu", "lengths.cu", "selector.cpp"]
+SOURCES = ["api.cu", "planner.cu", "copy.cu", "aggregate.cu", "lengths.cu", "vmm.cu", "selector.cpp"]
 HEADERS = ["earl_internal.cuh"]
 PUBLIC_HEADER = os.path.join(ROOT, "include", "earl_dispatch.h")
 

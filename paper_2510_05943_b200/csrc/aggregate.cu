@@ -877,6 +877,7 @@ __global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_kernel
   // lane 0 claims the next unit and resolves its token range into this warp's shared slot
   auto claim_next = [&]() {
     delay_inject(8);
+    __syncwarp();  // every lane's reads of the previous claim precede lane 0's writes
     if (lane == 0) {
       const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
       nx.valid = u < total;

@@ -4,6 +4,8 @@
 // CUDA-IPC peer mappings, signal pads), plan lifetime (stream-ordered allocations from the
 // device memory pool, so a steady-state plan allocates nothing from the driver), and the
 // launches of the planner (planner.cu) and the copy kernels (copy.cu).
+#include <unistd.h>
+
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -106,17 +108,49 @@ struct earl_comm {
   void* nst[2] = {};
   uint64_t nst_bytes[2] = {};
   void* nreg[2] = {};
+  // NEXT-3 (EARL_NVLS=1): the window from cuMemCreate, peers imported by file descriptor, and
+  // the multicast teams this rank belongs to (each bound to the whole window at offset 0)
+  bool vmm = false;
+  VmmMem vwin{0, 0, 0, -1};
+  VmmMem vpeer[kMaxWorld] = {};
+  struct Team {
+    uint32_t mask;
+    VmmMem mc;
+  } teams[kMaxShards] = {};
+  int n_teams = 0;
 };
+
+namespace {
+constexpr uint32_t kVmmMagic = 0x4d4d5645u;   // "EVMM": a cuMemCreate window handle
+constexpr uint32_t kTeamMagic = 0x544d4345u;  // "ECMT": a multicast team handle
+struct FdHandle {
+  uint32_t magic;
+  int32_t pid;
+  int32_t fd;
+  int32_t pad;
+  uint64_t size;
+  uint32_t mask;
+};
+static_assert(sizeof(FdHandle) <= EARL_HANDLE_BYTES, "handle size");
+}  // namespace
 
 namespace {
 void comm_release(earl_comm* c) {
   if (--c->refs > 0) return;
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
-  for (int p = 0; p < kMaxWorld; ++p)
-    if (c->peer_mapped[p]) cudaIpcCloseMemHandle(c->peer[p]);
-  for (int r = 0; r < kMaxWorld; ++r)
-    if (c->win[r]) cudaFree(c->win[r]);
+  for (int t = 0; t < c->n_teams; ++t) mc_free(&c->teams[t].mc, c->device);
+  for (int p = 0; p < kMaxWorld; ++p) {
+    if (!c->peer_mapped[p]) continue;
+    if (c->vmm) vmm_free(&c->vpeer[p]);
+    else cudaIpcCloseMemHandle(c->peer[p]);
+  }
+  if (c->vmm) {
+    vmm_free(&c->vwin);
+  } else {
+    for (int r = 0; r < kMaxWorld; ++r)
+      if (c->win[r]) cudaFree(c->win[r]);
+  }
   for (int k = 0; k < 2; ++k) {
     if (c->nreg[k]) ncclCommDeregister(c->nccl, c->nreg[k]);
     if (c->nst[k]) {
@@ -232,8 +266,22 @@ extern "C" earl_status_t earl_comm_create(int32_t rank, int32_t world, int32_t c
     return st;
   };
   const int nwin = c->emulated ? world : 1;
+  const char* nvls = getenv("EARL_NVLS");
+  c->vmm = !c->emulated && world > 1 && nvls && atoi(nvls) != 0;
   for (int r = 0; r < nwin; ++r) {
     const int rr = c->emulated ? r : rank;
+    if (c->vmm) {  // NEXT-3: a cuMemCreate window (bindable to multicast teams)
+      const char* why = "";
+      if (!vmm_create(cuda_device, c->window_bytes, &c->vwin, &why))
+        return cleanup(fail(EARL_ERR_UNSUPPORTED, "EARL_NVLS=1: cuMemCreate window: %s", why));
+      c->window_bytes = c->vwin.size;
+      c->win[rr] = reinterpret_cast<uint8_t*>(c->vwin.va);
+      cudaError_t e = cudaMemset(c->win[rr], 0, kPadBytes);
+      if (e != cudaSuccess) return cleanup(fail(EARL_ERR_CUDA, "pad memset: %s", cudaGetErrorString(e)));
+      c->peer[rr] = c->win[rr];
+      c->alloc_off[rr] = c->pad_bytes;
+      continue;
+    }
     cudaError_t e = cudaMalloc(&c->win[rr], c->window_bytes);
     if (e != cudaSuccess)
       return cleanup(fail(EARL_ERR_CUDA, "window cudaMalloc(%llu): %s",
@@ -261,9 +309,20 @@ extern "C" earl_status_t earl_comm_export_handle(earl_comm_t c, void* handle_out
   if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm has no peers to export to");
   static_assert(sizeof(cudaIpcMemHandle_t) <= EARL_HANDLE_BYTES, "handle size");
   DeviceGuard g(c->device);
+  std::memset(handle_out, 0, EARL_HANDLE_BYTES);
+  if (c->vmm) {
+    FdHandle fh{};
+    const char* why = "";
+    if (!vmm_export(&c->vwin, &fh.fd, &why))
+      return fail(EARL_ERR_CUDA, "window export: %s", why);
+    fh.magic = kVmmMagic;
+    fh.pid = (int32_t)getpid();
+    fh.size = c->vwin.size;
+    std::memcpy(handle_out, &fh, sizeof(fh));
+    return EARL_OK;
+  }
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, c->win[c->rank]));
-  std::memset(handle_out, 0, EARL_HANDLE_BYTES);
   std::memcpy(handle_out, &h, sizeof(h));
   return EARL_OK;
 }
@@ -275,6 +334,18 @@ extern "C" earl_status_t earl_comm_import_peers(earl_comm_t c, const void* handl
   const uint8_t* hb = static_cast<const uint8_t*>(handles);
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank || c->peer_mapped[p]) continue;
+    FdHandle fh;
+    std::memcpy(&fh, hb + (size_t)p * EARL_HANDLE_BYTES, sizeof(fh));
+    if ((fh.magic == kVmmMagic) != c->vmm)
+      return fail(EARL_ERR_INVALID_ARGUMENT, "peer %d's window kind differs (EARL_NVLS must match on every rank)", p);
+    if (c->vmm) {
+      const char* why = "";
+      if (!vmm_import(c->device, fh.pid, fh.fd, fh.size, &c->vpeer[p], &why))
+        return fail(EARL_ERR_CUDA, "import of peer %d's window: %s", p, why);
+      c->peer[p] = reinterpret_cast<uint8_t*>(c->vpeer[p].va);
+      c->peer_mapped[p] = true;
+      continue;
+    }
     cudaIpcMemHandle_t h;
     std::memcpy(&h, hb + (size_t)p * EARL_HANDLE_BYTES, sizeof(h));
     void* ptr = nullptr;
@@ -394,6 +465,63 @@ extern "C" earl_status_t earl_comm_peer_mask(earl_comm_t c, uint32_t* mask) {
   for (int p = 0; p < c->world; ++p)
     if (c->peer_mapped[p]) m |= 1u << p;
   *mask = m;
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_mc_create(earl_comm_t c, uint32_t team_mask, void* handle_out) {
+  if (!c || !handle_out) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!c->vmm) return fail(EARL_ERR_UNSUPPORTED, "multicast teams need EARL_NVLS=1 at earl_comm_create");
+  const uint32_t all = c->world >= 32 ? ~0u : (1u << c->world) - 1u;
+  if (team_mask == 0 || (team_mask & ~all) || !(team_mask >> c->rank & 1))
+    return fail(EARL_ERR_INVALID_ARGUMENT, "team mask 0x%x: not a subset of the comm containing this rank", team_mask);
+  if (c->n_teams >= kMaxShards) return fail(EARL_ERR_CAPACITY, "at most %d multicast teams", kMaxShards);
+  DeviceGuard g(c->device);
+  VmmMem mc{0, 0, 0, -1};
+  const char* why = "";
+  if (!mc_create(__builtin_popcount(team_mask), c->vwin.size, &mc, &why))
+    return fail(EARL_ERR_UNSUPPORTED, "cuMulticastCreate(%d devices): %s", __builtin_popcount(team_mask), why);
+  FdHandle fh{};
+  if (!vmm_export(&mc, &fh.fd, &why)) {
+    mc_free(&mc, c->device);
+    return fail(EARL_ERR_CUDA, "multicast export: %s", why);
+  }
+  fh.magic = kTeamMagic;
+  fh.pid = (int32_t)getpid();
+  fh.size = mc.size;
+  fh.mask = team_mask;
+  // the creator keeps the object (and its descriptor, until destroy) as a pending team
+  c->teams[c->n_teams].mask = 0;  // joined below (earl_comm_mc_join)
+  c->teams[c->n_teams].mc = mc;
+  std::memset(handle_out, 0, EARL_HANDLE_BYTES);
+  std::memcpy(handle_out, &fh, sizeof(fh));
+  return EARL_OK;
+}
+
+extern "C" earl_status_t earl_comm_mc_join(earl_comm_t c, uint32_t team_mask, const void* handle) {
+  if (!c || !handle) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!c->vmm) return fail(EARL_ERR_UNSUPPORTED, "multicast teams need EARL_NVLS=1 at earl_comm_create");
+  FdHandle fh;
+  std::memcpy(&fh, handle, sizeof(fh));
+  if (fh.magic != kTeamMagic || fh.mask != team_mask)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "not a multicast team handle for mask 0x%x", team_mask);
+  if (!(team_mask >> c->rank & 1)) return EARL_OK;  // not a member: nothing to map
+  if (c->n_teams >= kMaxShards) return fail(EARL_ERR_CAPACITY, "at most %d multicast teams", kMaxShards);
+  DeviceGuard g(c->device);
+  earl_comm::Team* t = &c->teams[c->n_teams];
+  const char* why = "";
+  const bool creator = fh.pid == (int32_t)getpid() && t->mc.handle && t->mask == 0;
+  if (!creator) {
+    VmmMem mc{0, 0, 0, -1};
+    if (!mc_import(fh.pid, fh.fd, fh.size, &mc, &why))
+      return fail(EARL_ERR_CUDA, "multicast import: %s", why);
+    t->mc = mc;
+  }
+  if (!mc_join(&t->mc, c->device, c->vwin, &why)) {
+    mc_free(&t->mc, c->device);
+    return fail(EARL_ERR_UNSUPPORTED, "multicast join: %s", why);
+  }
+  t->mask = team_mask;
+  c->n_teams += 1;
   return EARL_OK;
 }
 
@@ -1251,10 +1379,26 @@ earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
       return v && std::strcmp(v, "tma") == 0 ? 1 : 0;
     }();
     a.remote_tma = remote_tma;
+    // NEXT-3: dst shards whose replicas form one of this rank's multicast teams (each source
+    // feeds every replica: tp_src == 1); the entry barrier checks the members' offsets agree
+    McTeams mct{};
+    if (c->n_teams > 0 && a.tp_s == 1 && a.tp_d > 1) {
+      for (int ds = 0; ds < a.n_dst_shards && ds < kMaxShards; ++ds) {
+        uint32_t want = 0;
+        for (int t = 0; t < a.tp_d; ++t) want |= 1u << (a.rank0_d + ds * a.tp_d + t);
+        for (int k = 0; k < c->n_teams; ++k)
+          if (c->teams[k].mask == want && c->teams[k].mc.va) {
+            mct.va[ds] = c->teams[k].mc.va;
+            mct.mask[ds] = want;
+            a.mc_on = 1;
+          }
+      }
+    }
+    a.mc_tab = reinterpret_cast<uint8_t* const*>(a.my_pad + kMcTabSlot);
     use_begin(p, s);
     clear_stale_error();
-    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, F, off, c->timeout_ns,
-                                         a.err, a.err_detail, s);
+    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, F, off, mct,
+                                         c->timeout_ns, a.err, a.err_detail, s);
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1);
   }

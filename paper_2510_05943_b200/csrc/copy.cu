@@ -25,6 +25,14 @@ constexpr uint64_t kUnitsPerWarp = 8;
 __device__ __forceinline__ void st_v4(void* p, const uint4& v) {
   *reinterpret_cast<uint4*>(p) = v;
 }
+// NEXT-3: one 16-B store to a multicast address reaches every member of the team (NVSwitch
+// replicates it); the payload is opaque, the .f32 vector form only moves the bits
+__device__ __forceinline__ void multimem_st_v4(void* p, const uint4& v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
+               "f"(__uint_as_float(v.w))
+               : "memory");
+}
 
 // 16 bytes starting at byte sh (1..15) of the 32-byte pair (A, B): S4 = sh/4 (a template
 // parameter: the word selection is resolved at compile time, the loop below is instantiated per
@@ -84,7 +92,7 @@ __device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad,
 // rank rewrites them only in its next exec, after every peer released its done flag (i.e.
 // finished reading).
 __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world, int me,
-                                     int n_fields, RecvOffsets offs, uint64_t timeout_ns,
+                                     int n_fields, RecvOffsets offs, McTeams mct, uint64_t timeout_ns,
                                      int32_t* err, int32_t* err_detail) {
   const int lane = threadIdx.x & 31;
   uint64_t epoch = 0;
@@ -114,6 +122,30 @@ __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world,
   }
   if (lane == 0 && miss) {
     if (atomicCAS(err, 0, EARL_ERR_TIMEOUT) == 0) *err_detail = (int32_t)miss;
+  }
+  // NEXT-3: the multicast base of (dst shard ds, field f) when every member of ds's team put
+  // field f at the same window offset (a multicast store lands at one offset on all of them)
+  __syncwarp();
+  __threadfence_block();
+  uint64_t* mtab = my_pad + kMcTabSlot;
+  if (lane < kMaxShards) {
+    const int ds = lane;
+    for (int f = 0; f < kMaxFields; ++f) {
+      uint64_t v = 0;
+      if (mct.va[ds] != 0 && f < n_fields && !miss) {
+        uint64_t off = kNoOffset;
+        bool same = true;
+        for (int p = 0; p < world && same; ++p) {
+          if (!(mct.mask[ds] >> p & 1)) continue;
+          const uint64_t b = tab[p * kMaxFields + f];
+          const uint64_t o = b ? b - reinterpret_cast<uint64_t>(pads.p[p]) : kNoOffset;
+          if (o == kNoOffset || (off != kNoOffset && o != off)) same = false;
+          off = o;
+        }
+        if (same && off != kNoOffset) v = mct.va[ds] + off;
+      }
+      mtab[ds * kMaxFields + f] = v;
+    }
   }
 }
 
@@ -280,6 +312,7 @@ struct Walker {
   uint64_t prem;
   int pf, pd0;
   uint8_t* const* dt;  // the launch's destination field bases [kMaxWorld][kMaxFields] (smem)
+  uint8_t* const* mt;  // NEXT-3: multicast bases [kMaxShards][kMaxFields] (smem), or nullptr
 
   __device__ __forceinline__ void set_block(const View& v, int bb) {
     b = bb;
@@ -399,6 +432,8 @@ struct Walker {
           pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
           if (base0 == nullptr) R = 0;
           pd0 = d0;
+          // NEXT-3: every replica of this shard is in a multicast team with this rank
+          if (mt != nullptr && R > 1 && mt[ds * kMaxFields + f] != nullptr) R |= 0x80u;
         }
         prem = u1 - u0;
         pf = f;
@@ -561,6 +596,75 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
   }
 }
 
+// NEXT-3: a range whose R replicas form a multicast team this rank belongs to: the 16-B interior
+// leaves once, by multimem.st to the team's address (reaching every replica, this rank's own
+// included); heads and tails (< 16 B each) go byte by byte to every replica.
+template <int R>
+__device__ __forceinline__ void store_sub_mc(const CopyArgs& a, uint8_t* const* dt,
+                                             uint8_t* const* mt, const SubDesc& S, uint8_t* stage,
+                                             int lane) {
+  const uint32_t len = S.len;
+  const uint8_t* sm = stage + S.so + S.off;
+  uint8_t* dp[R];
+  dp[0] = S.dst0;
+#pragma unroll
+  for (int r = 1; r < R; ++r)
+    dp[r] = S.dst0 + (dt[(S.d0 + r * a.tp_s) * kMaxFields + S.f] - dt[S.d0 * kMaxFields + S.f]);
+  const int ds = (S.d0 - a.rank0_d) / a.tp_d;
+  uint8_t* mc = mt[ds * kMaxFields + S.f] + (S.dst0 - dt[S.d0 * kMaxFields + S.f]);
+  uint32_t head = (16 - (uint32_t)((uintptr_t)S.dst0 & 15)) & 15;
+  if (head > len) head = len;
+  if (lane < (int)head) {
+    const uint8_t v = sm[lane];
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r][lane] = v;
+  }
+  const uint32_t rest = len - head;
+  const uint32_t nvec = rest >> 4;
+  if (nvec > 0) {
+    const uint32_t smo = S.so + S.off + head;
+    const uint32_t sh = smo & 15;
+    const uint8_t* sp = stage + (smo & ~15u);
+    for (uint32_t k = lane; k < nvec; k += 32) {
+      uint4 o;
+      const uint4 w0 = *reinterpret_cast<const uint4*>(sp + 16 * k);
+      if (sh == 0) {
+        o = w0;
+      } else {
+        const uint4 w1 = *reinterpret_cast<const uint4*>(sp + 16 * k + 16);
+        const int bits = (int)(sh & 3) * 8;
+        switch (sh >> 2) {
+          case 0: o = realign<0>(w0, w1, bits); break;
+          case 1: o = realign<1>(w0, w1, bits); break;
+          case 2: o = realign<2>(w0, w1, bits); break;
+          default: o = realign<3>(w0, w1, bits); break;
+        }
+      }
+      multimem_st_v4(mc + head + 16 * k, o);
+    }
+  }
+  const uint32_t t0 = head + nvec * 16;
+  if (lane < (int)(len - t0)) {
+    const uint8_t v = sm[t0 + lane];
+#pragma unroll
+    for (int r = 0; r < R; ++r) dp[r][t0 + lane] = v;
+  }
+}
+
+__device__ __forceinline__ void store_sub_mc_any(const CopyArgs& a, uint8_t* const* dt,
+                                                 uint8_t* const* mt, const SubDesc& S,
+                                                 uint8_t* stage, int lane) {
+  switch (S.R & 0x7f) {
+    case 2: store_sub_mc<2>(a, dt, mt, S, stage, lane); break;
+    case 3: store_sub_mc<3>(a, dt, mt, S, stage, lane); break;
+    case 4: store_sub_mc<4>(a, dt, mt, S, stage, lane); break;
+    case 5: store_sub_mc<5>(a, dt, mt, S, stage, lane); break;
+    case 6: store_sub_mc<6>(a, dt, mt, S, stage, lane); break;
+    case 7: store_sub_mc<7>(a, dt, mt, S, stage, lane); break;
+    default: store_sub_mc<8>(a, dt, mt, S, stage, lane); break;
+  }
+}
+
 __device__ __forceinline__ void store_sub(const CopyArgs& a, uint8_t* const* dt, const SubDesc& S,
                                           uint8_t* stage, int lane) {
   switch (S.R) {
@@ -580,11 +684,14 @@ constexpr size_t copy_smem_bytes() {
   return (size_t)WARPS * STAGES * CHUNK + (size_t)WARPS * STAGES * (sizeof(StageDesc) + 8);
 }
 
-template <int WARPS, int STAGES, int CHUNK>
+template <int WARPS, int STAGES, int CHUNK, bool MC>
 __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_constant__ CopyArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ unsigned s_last;
   __shared__ uint8_t* s_dst[kMaxWorld * kMaxFields];
+  __shared__ uint8_t* s_mc[MC ? kMaxShards * kMaxFields : 1];  // NEXT-3: multicast bases
+  if (MC)
+    for (int k = threadIdx.x; k < kMaxShards * kMaxFields; k += WARPS * 32) s_mc[k] = a.mc_tab[k];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   // destination field bases: the kernel parameter, or (multi-process exec) the table the entry
   // barrier resolved from every destination's published offsets
@@ -614,6 +721,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       build_view(a, c0, v);
       wk.setup(a, v, c0, nwarps);
       wk.dt = s_dst;
+      wk.mt = MC ? s_mc : nullptr;
       const uint64_t total = wk.total;
       // units: every warp starts on unit `wid`, then claims units >= nwarps dynamically
       uint64_t unit = (total + nwarps * kUnitsPerWarp - 1) / (nwarps * kUnitsPerWarp);
@@ -634,7 +742,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       mbar_wait(&bar[st], (uint32_t)((c / STAGES) & 1));
       uint8_t* stage = data + (size_t)st * CHUNK;
       const uint32_t nsub = desc[st].n;
-      for (uint32_t k = 0; k < nsub; ++k) store_sub(a, s_dst, desc[st].sub[k], stage, lane);
+      for (uint32_t k = 0; k < nsub; ++k) {
+        if (MC && (desc[st].sub[k].R & 0x80))
+          store_sub_mc_any(a, s_dst, s_mc, desc[st].sub[k], stage, lane);
+        else
+          store_sub(a, s_dst, desc[st].sub[k], stage, lane);
+      }
       if (lane == 0) { bulk_commit(); bulk_wait_read1(); }
       __syncwarp();
       int ok = 0;
@@ -695,11 +808,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
   }
 }
 
-template <int WARPS, int STAGES, int CHUNK>
+template <int WARPS, int STAGES, int CHUNK, bool MC = false>
 cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
   constexpr size_t smem = copy_smem_bytes<WARPS, STAGES, CHUNK>();
   static bool configured[64] = {};
-  auto kern = copy_kernel<WARPS, STAGES, CHUNK>;
+  auto kern = copy_kernel<WARPS, STAGES, CHUNK, MC>;
   cudaError_t e = opt_in_dynamic_smem(kern, (int)smem, configured);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
@@ -726,6 +839,8 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t
     forced = e ? atoi(e) : -1;
   }
   const int cfg = shape >= 100 ? shape - 100 : forced >= 0 ? forced : (shape ? 14 : 3);
+  if (a.mc_on)  // NEXT-3: the multicast-capable instantiations of the two default shapes
+    return cfg == 14 ? launch_cfg<2, 2, 16384, true>(a, sm_count, s) : launch_cfg<8, 3, 8192, true>(a, sm_count, s);
   switch (cfg) {
     case 1: return launch_cfg<8, 4, 4096>(a, sm_count, s);
     case 2: return launch_cfg<4, 4, 8192>(a, sm_count, s);
@@ -741,14 +856,15 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t
 }
 
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 int n_fields, const uint64_t* recv_off, uint64_t timeout_ns,
-                                 int32_t* err, int32_t* err_detail, cudaStream_t s) {
+                                 int n_fields, const uint64_t* recv_off, const McTeams& mct,
+                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
+                                 cudaStream_t s) {
   PeerPads pads;
   for (int p = 0; p < kMaxWorld; ++p) pads.p[p] = peer_pad[p];
   RecvOffsets offs;
   for (int f = 0; f < kMaxFields; ++f) offs.v[f] = f < n_fields ? recv_off[f] : kNoOffset;
-  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, n_fields, offs, timeout_ns, err,
-                                        err_detail);
+  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, n_fields, offs, mct, timeout_ns,
+                                        err, err_detail);
   return cudaGetLastError();
 }
 

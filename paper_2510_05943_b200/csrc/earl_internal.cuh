@@ -103,6 +103,10 @@ struct PlanArgs {
 struct PeerPads {
   uint64_t* p[kMaxWorld];
 };
+struct McTeams {             // NEXT-3: per dst shard, the multicast address of its team (0: none)
+  uint64_t va[kMaxShards];
+  uint32_t mask[kMaxShards];  // the team's ranks
+};
 struct RecvOffsets {
   uint64_t v[kMaxFields];   // window-relative receive offsets of this rank (kNoOffset = NULL)
 };
@@ -117,6 +121,8 @@ struct CopyArgs {
   int32_t rank0_s, tp_s, rank0_d, tp_d, sp_d, n_dst_shards, n_src_shards;
   int32_t protocol;        // 1: multi-process fused exec (epoch release / acquire at the end)
   int32_t remote_tma;      // 1: peer replicas by bulk TMA stores too (EARL_REMOTE_STORE=tma)
+  int32_t mc_on;           // NEXT-3: some dst shard's replicas form a multicast team with this rank
+  uint8_t* const* mc_tab;  // [kMaxShards][kMaxFields] multicast bases (entry barrier), protocol 1
   const uint8_t* recv_stage;                  // unpack on a real rank: received messages
   uint32_t Bf[kMaxFields];
   uint64_t Bpre[kMaxFields + 1];  // prefix of Bf
@@ -154,6 +160,7 @@ constexpr int kLensEpochSlot = 17;  // this rank's length-gather epoch (a1)
 constexpr int kLensSlot = 24;       // [24, 32): length-gather flags written by peer p at p
 constexpr int kOffSlot = 32;
 constexpr int kDstTabSlot = 64;
+constexpr int kMcTabSlot = 192;  // [192, 320): multicast bases [kMaxShards][kMaxFields] (NEXT-3)
 constexpr uint64_t kNoOffset = ~0ull;
 
 // step a1 (lengths.cu): the device gather of the global length vector
@@ -261,6 +268,24 @@ inline cudaError_t opt_in_dynamic_smem(F* func, int bytes, bool (&done)[64]) {
   return e;
 }
 
+// NEXT-3 (vmm.cu): cuMemCreate windows shared by POSIX file descriptor, NVLS multicast teams
+struct VmmMem {
+  uint64_t handle;  // CUmemGenericAllocationHandle
+  uint64_t va;      // mapped address in this process (0: not mapped)
+  uint64_t size;
+  int32_t fd;       // exported descriptor (-1: none)
+};
+bool vmm_available();
+bool multicast_entry_points();
+bool vmm_create(int device, uint64_t bytes, VmmMem* out, const char** why);
+bool vmm_export(VmmMem* m, int32_t* fd, const char** why);
+bool vmm_import(int device, int32_t pid, int32_t fd, uint64_t size, VmmMem* out, const char** why);
+void vmm_free(VmmMem* m);
+bool mc_create(int n_devices, uint64_t size, VmmMem* out, const char** why);
+bool mc_import(int32_t pid, int32_t fd, uint64_t size, VmmMem* out, const char** why);
+bool mc_join(VmmMem* mc, int device, const VmmMem& window, const char** why);
+void mc_free(VmmMem* mc, int device);
+
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s);
@@ -270,8 +295,9 @@ int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_sm
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, bool fast, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t s);
 cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 int n_fields, const uint64_t* recv_off, uint64_t timeout_ns,
-                                 int32_t* err, int32_t* err_detail, cudaStream_t s);
+                                 int n_fields, const uint64_t* recv_off, const McTeams& mct,
+                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
+                                 cudaStream_t s);
 cudaError_t launch_gather_lengths(const LensArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t s);
 cudaError_t launch_local_meta(const PlanArgs& a, int rank_g, int rank_k, int32_t* cu, int64_t* ids,

@@ -259,6 +259,33 @@ class Dispatcher:
         for p, hbuf in host_recv.items():
             recv_stage[ro[p]:ro[p] + rb[p]].copy_(hbuf)
 
+    def enable_multicast(self, dst):
+        """NEXT-3: one NVLS multicast team per TP group of layout `dst` (needs EARL_NVLS=1 when
+        the comm was made).  The team's lowest rank creates it, the process group carries the
+        handle, every rank joins (members bind their window).  Raises EarlError (UNSUPPORTED)
+        on every rank when the device cannot create a team.  Returns the team masks."""
+        r0, dp, sp, tp = (int(dst.get(k, d)) for k, d in (("rank0", 0), ("dp", 1), ("sp", 1), ("tp", 1)))
+        masks = []
+        if tp < 2:
+            return masks
+        for ds in range(dp * sp):
+            ranks = [r0 + ds * tp + t for t in range(tp)]
+            mask = sum(1 << r for r in ranks)
+            made = None
+            if self.rank == ranks[0]:
+                try:
+                    made = (self.comm.mc_create(mask), None)
+                except earl.EarlError as e:
+                    made = (None, (e.status, str(e)))
+            objs = [None] * self.world
+            self.dist.all_gather_object(objs, made, group=self.group)
+            handle, err = objs[ranks[0]]
+            if err is not None:
+                raise earl.EarlError(err[0], err[1])
+            self.comm.mc_join(mask, handle)
+            masks.append(mask)
+        return masks
+
     def init_nccl(self):
         """K8: the library's own NCCL communicator over this group's ranks (rank 0 draws the
         unique id, the process group broadcasts it).  Needs one GPU per rank (NCCL rejects two

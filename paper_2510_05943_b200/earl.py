@@ -42,7 +42,7 @@ EXPORTED = [
     "earl_policy_table", "earl_policy_select", "earl_policy_destroy", "earl_plan_mean_length",
     "earl_allgather_lengths", "earl_comm_check", "earl_comm_peer_mask",
     "earl_nccl_unique_id", "earl_comm_init_nccl", "earl_dispatch_exchange", "earl_dispatch_exec_staged",
-    "earl_plan_seq_fields",
+    "earl_plan_seq_fields", "earl_comm_mc_create", "earl_comm_mc_join",
 ]
 
 
@@ -128,6 +128,8 @@ def lib():
         "earl_dispatch_exchange": [vp, vp, vp, vp],
         "earl_dispatch_exec_staged": [vp, pvp, pvp, vp],
         "earl_plan_seq_fields": [vp, C.POINTER(Field), i32, vp, pvp],
+        "earl_comm_mc_create": [vp, C.c_uint32, vp],
+        "earl_comm_mc_join": [vp, C.c_uint32, vp],
         "earl_dispatch_plan": [vp, C.POINTER(Layout), C.POINTER(Layout), vp, i64,
                                C.POINTER(Field), i32, vp, pvp],
         "earl_plan_sync": [vp],
@@ -277,6 +279,17 @@ class Comm:
         """earl_comm_init_nccl (collective): the staged exchange's NCCL communicator."""
         buf = (C.c_uint8 * EARL_HANDLE_BYTES).from_buffer_copy(unique_id)
         check(lib().earl_comm_init_nccl(self.h, buf))
+
+    def mc_create(self, team_mask: int) -> bytes:
+        """earl_comm_mc_create (NEXT-3; the team's lowest rank): the team handle to broadcast."""
+        buf = (C.c_uint8 * EARL_HANDLE_BYTES)()
+        check(lib().earl_comm_mc_create(self.h, int(team_mask), buf))
+        return bytes(buf)
+
+    def mc_join(self, team_mask: int, handle: bytes):
+        """earl_comm_mc_join (NEXT-3; every rank, members concurrently)."""
+        buf = (C.c_uint8 * EARL_HANDLE_BYTES).from_buffer_copy(handle)
+        check(lib().earl_comm_mc_join(self.h, int(team_mask), buf))
 
     def peer_mapped(self, p: int) -> bool:
         """earl_comm_peer_mask: is peer p's window mapped into this process?"""

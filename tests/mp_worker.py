@@ -459,3 +459,62 @@ def gpu_nccl_main(rank, world, port, q, case):
         q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_nvls_main(rank, world, port, q, case):
+    """NEXT-3 plumbing with EARL_NVLS=1: cuMemCreate windows exported by file descriptor
+    (pidfd_getfd) instead of CUDA IPC, fused exec bit-exact against the oracle, then the
+    multicast teams of the destination's TP groups -- created and used when the device can (a
+    multi-GPU NVSwitch box), EARL_ERR_UNSUPPORTED on every rank when it cannot (one visible GPU),
+    after which the unicast exec still matches the oracle."""
+    try:
+        import os
+        os.environ["EARL_NVLS"] = "1"
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, src, dst, fields = case
+        T = sum(lens)
+        glob = W.gen_global_fields(fields, T, seed_base=31, random_bits=True)
+        src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+        want, _, _ = O.dispatch(src, dst, lens, src_arrays, fields, world)
+        D = Dispatcher(window_bytes=T * W.bytes_per_token(fields) + (1 << 20), device=0)
+        assert all(D.comm.peer_mapped(p) for p in range(world) if p != rank)
+        mine = [torch.from_numpy(a).cuda() if a.size else None for a in src_arrays.get(rank, [])] \
+            if rank in src_arrays else [None] * len(fields)
+        glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+
+        def run(tag):
+            plan = D.plan(src, dst, glens, fields)
+            ptrs, views = D.alloc_recv(plan, fields)
+            for v in views:
+                v.fill_(0xA5)
+            plan.exec(mine, ptrs)
+            torch.cuda.synchronize()
+            plan.sync()
+            if rank in want:
+                for f in range(len(fields)):
+                    assert np.array_equal(views[f].cpu().numpy(), want[rank][f]), (tag, rank, f)
+            plan.destroy()
+
+        run("vmm windows")
+        msg = "ok"
+        try:
+            masks = D.enable_multicast(dst)
+            run("multicast")
+            msg = f"ok (multicast teams {masks})"
+        except EarlError as e:
+            if e.name != "EARL_ERR_UNSUPPORTED":
+                raise
+            run("unicast after UNSUPPORTED")
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok" if msg.startswith("ok") else msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

@@ -218,3 +218,26 @@ def test_p2p_store_variants(name, env, monkeypatch):
         world, lens = 4, W.c4_lengths(0)[:10].tolist()
         src, dst = W.config_layouts("c4", 4, 10)
     run_procs(mp_worker.gpu_main, world, extra=((lens, src, dst, f3, 2, "fused"),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["dp1_to_tp4", "c3_dp4_dp1tp4", "c4_dp4_sp2"])
+def test_nvls_vmm_windows(name):
+    """NEXT-3: EARL_NVLS=1 windows (cuMemCreate + file-descriptor export) carry the fused exec
+    bit-exactly; multicast teams are used where the device can make them, and report
+    EARL_ERR_UNSUPPORTED otherwise (one visible GPU: cuMulticastCreate refuses every team)."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    f = W.field_set("tiny3") + [("m", 1, 1, "mask"), ("h", 2, 40, "hidden")]
+    if name == "dp1_to_tp4":      # the egress-bound case NVLS is for: one source, a TP4 group
+        world, lens = 4, W.c2_lengths(0)[:20].tolist()
+        src, dst = W.rollout_layout(20, 1), W.layout(dp=1, tp=4, assign="contig")
+    elif name == "c3_dp4_dp1tp4":
+        world, lens = 4, W.c2_lengths(0)[:40].tolist()
+        src, dst = W.config_layouts("c3", 4, 40)
+    else:
+        world, lens = 4, W.c4_lengths(0)[:10].tolist()
+        src, dst = W.config_layouts("c4", 4, 10)
+    run_procs(mp_worker.gpu_nvls_main, world, extra=((lens, src, dst, f),), timeout=600)
