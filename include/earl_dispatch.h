@@ -186,6 +186,25 @@ EARL_API earl_status_t earl_comm_peer_mask(earl_comm_t comm, uint32_t* mask);
  * everything else stay unicast.  Errors: UNSUPPORTED (no EARL_NVLS window, or the driver / device
  * cannot create the team -- e.g. a box with one visible GPU), INVALID_ARGUMENT, CAPACITY (> 8
  * teams). */
+/* NEXT-4 ("further gains with RDMA"): a comm spanning several
+ * nodes of node_size consecutive ranks each (node n = ranks [n*node_size, (n+1)*node_size)).  Call
+ * before earl_comm_import_peers: only same-node windows are mapped.  Then, on this comm:
+ *   earl_dispatch_exec        moves the records whose destination replica is on this node (fused
+ *                             P2P; the barrier and done flags involve the node's ranks only);
+ *   earl_dispatch_pack / earl_plan_messages / earl_dispatch_exchange / earl_dispatch_unpack /
+ *   earl_dispatch_exec_staged cover exactly the messages between nodes (pack: the destination
+ *                             shards with a replica on another node; unpack: the messages from
+ *                             other nodes' ranks, concatenated in source-rank order);
+ *   earl_dispatch_exec_hier   does both: fused P2P inside the node, then the NCCL exchange
+ *                             (earl_comm_init_nccl: NCCL picks IB / RoCE between nodes).
+ * The two legs write disjoint parts of the receive arrays.  earl_allgather_lengths is
+ * UNSUPPORTED on such a comm (gather the lengths over the process group).
+ * Errors: INVALID_ARGUMENT (node_size does not divide the world, or peers already imported),
+ * UNSUPPORTED (emulated comm). */
+EARL_API earl_status_t earl_comm_set_nodes(earl_comm_t comm, int32_t node_size);
+EARL_API earl_status_t earl_dispatch_exec_hier(earl_plan_t plan, const void* const* send_bufs,
+                                               void* const* recv_bufs, void* stream);
+
 EARL_API earl_status_t earl_comm_mc_create(earl_comm_t comm, uint32_t team_mask, void* handle_out);
 EARL_API earl_status_t earl_comm_mc_join(earl_comm_t comm, uint32_t team_mask, const void* handle);
 

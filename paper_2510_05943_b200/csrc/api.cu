@@ -110,6 +110,7 @@ struct earl_comm {
   void* nreg[2] = {};
   // NEXT-3 (EARL_NVLS=1): the window from cuMemCreate, peers imported by file descriptor, and
   // the multicast teams this rank belongs to (each bound to the whole window at offset 0)
+  int32_t node_size = 0;   // NEXT-4: ranks per node (0: the whole comm is one node)
   bool vmm = false;
   VmmMem vwin{0, 0, 0, -1};
   VmmMem vpeer[kMaxWorld] = {};
@@ -121,6 +122,15 @@ struct earl_comm {
 };
 
 namespace {
+// NEXT-4: the node of a rank, and the ranks of this rank's node
+inline int node_of(const earl_comm* c, int r) { return c->node_size > 0 ? r / c->node_size : 0; }
+inline bool same_node(const earl_comm* c, int a, int b) { return node_of(c, a) == node_of(c, b); }
+inline uint32_t node_mask(const earl_comm* c) {
+  uint32_t m = 0;
+  for (int p = 0; p < c->world; ++p)
+    if (c->emulated || same_node(c, p, c->rank)) m |= 1u << p;
+  return m;
+}
 constexpr uint32_t kVmmMagic = 0x4d4d5645u;   // "EVMM": a cuMemCreate window handle
 constexpr uint32_t kTeamMagic = 0x544d4345u;  // "ECMT": a multicast team handle
 struct FdHandle {
@@ -334,6 +344,7 @@ extern "C" earl_status_t earl_comm_import_peers(earl_comm_t c, const void* handl
   const uint8_t* hb = static_cast<const uint8_t*>(handles);
   for (int p = 0; p < c->world; ++p) {
     if (p == c->rank || c->peer_mapped[p]) continue;
+    if (!same_node(c, p, c->rank)) continue;  // NEXT-4: other nodes are reached by NCCL only
     FdHandle fh;
     std::memcpy(&fh, hb + (size_t)p * EARL_HANDLE_BYTES, sizeof(fh));
     if ((fh.magic == kVmmMagic) != c->vmm)
@@ -426,6 +437,9 @@ extern "C" earl_status_t earl_allgather_lengths(earl_comm_t c, const int64_t* co
   DeviceGuard g(c->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   clear_stale_error();
+  if (c->node_size > 0)
+    return fail(EARL_ERR_UNSUPPORTED,
+                "multi-node comm: the device gather reaches one node; gather lengths over the process group");
   if (!c->emulated && c->world == 1) {  // one rank: the global vector is the local one
     if (tot > 0) CUDA_TRY(cudaMemcpyAsync(global_lens, a.local, tot * 4, cudaMemcpyDeviceToDevice, s));
     return EARL_OK;
@@ -457,6 +471,17 @@ extern "C" earl_status_t earl_comm_check(earl_comm_t c, void* stream) {
   if (h[0] == 0) return EARL_OK;
   CUDA_TRY(cudaMemset(c->dev_err, 0, sizeof(h)));
   return fail((earl_status_t)h[0], "length gather: peers missing (mask 0x%x)", h[1]);
+}
+
+extern "C" earl_status_t earl_comm_set_nodes(earl_comm_t c, int32_t node_size) {
+  if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm: one process holds every rank");
+  if (c->peers_ready && c->world > 1)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "earl_comm_set_nodes must precede earl_comm_import_peers");
+  if (node_size < 1 || c->world % node_size != 0)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "node size %d does not divide the world of %d", node_size, c->world);
+  c->node_size = node_size >= c->world ? 0 : node_size;
+  return EARL_OK;
 }
 
 extern "C" earl_status_t earl_comm_peer_mask(earl_comm_t c, uint32_t* mask) {
@@ -1228,6 +1253,9 @@ earl_status_t fill_copy_args(earl_plan_t p, CopyArgs& a, int mode) {
   a.rec = p->args.rec;
   a.world = c->world;
   a.me = c->emulated ? -1 : c->rank;
+  a.peer_mask = node_mask(c);
+  a.ds_mask = ~0u;
+  a.src_mask = ~0u;
   a.done_ctr = c->done_ctr;
   a.timeout_ns = c->timeout_ns;
   a.err = &p->args.hdr->err;
@@ -1397,8 +1425,8 @@ earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
     a.mc_tab = reinterpret_cast<uint8_t* const*>(a.my_pad + kMcTabSlot);
     use_begin(p, s);
     clear_stale_error();
-    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, c->rank, F, off, mct,
-                                         c->timeout_ns, a.err, a.err_detail, s);
+    cudaError_t e = launch_entry_barrier(a.my_pad, pads, c->world, a.peer_mask, c->rank, F, off,
+                                         mct, c->timeout_ns, a.err, a.err_detail, s);
     if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "entry barrier: %s", cudaGetErrorString(e));
     g_launches.fetch_add(1);
   }
@@ -1435,6 +1463,24 @@ extern "C" earl_status_t earl_dispatch_exec_src(earl_plan_t p, int32_t src_rank,
   return exec_impl(p, src_rank, send_bufs, recv_bufs, stream);
 }
 
+namespace {
+// NEXT-4: the destination shards of which this rank feeds a replica on another node
+uint32_t remote_shards(earl_plan_t p) {
+  const earl_comm* c = p->comm;
+  const earl_layout_t& S = p->lay[0];
+  const earl_layout_t& D = p->lay[1];
+  int g, k, t;
+  uint32_t m = 0;
+  if (!coords(S, c->rank, &g, &k, &t)) return 0;
+  for (int d = 0; d < c->world; ++d) {
+    int gd, kd, td;
+    if (!coords(D, d, &gd, &kd, &td) || td % S.tp != t) continue;
+    if (!same_node(c, d, c->rank)) m |= 1u << (gd * D.sp + kd);
+  }
+  return m;
+}
+}  // namespace
+
 extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* send_bufs,
                                             void* const* stage_bufs, void* stream) {
   NvtxRange nvtx("earl_dispatch_pack");
@@ -1452,6 +1498,7 @@ extern "C" earl_status_t earl_dispatch_pack(earl_plan_t p, const void* const* se
       return fail(EARL_ERR_INVALID_ARGUMENT, "stage buffer %d not 16-B aligned", rr);
     a.stage[rr] = static_cast<uint8_t*>(stage_bufs[r]);
   }
+  if (c->node_size > 0) a.ds_mask = remote_shards(p);  // NEXT-4: messages that leave the node
   use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "pack launch: %s", cudaGetErrorString(e));
@@ -1493,6 +1540,7 @@ extern "C" earl_status_t earl_dispatch_unpack(earl_plan_t p, const void* const* 
         return fail(EARL_ERR_INVALID_ARGUMENT, "recv buffer field %d not 16-B aligned", f);
       a.dst[c->rank][f] = static_cast<uint8_t*>(ptr);
     }
+    if (c->node_size > 0) a.src_mask = ~node_mask(c);  // NEXT-4: messages from other nodes
   }
   use_begin(p, static_cast<cudaStream_t>(stream));
   cudaError_t e = traced_launch(a, c, static_cast<cudaStream_t>(stream));
@@ -1518,13 +1566,16 @@ void message_table(earl_plan_t p, int rank, int64_t* send_off, int64_t* send_byt
     return b;
   };
   for (int q = 0; q < W; ++q) { send_off[q] = send_bytes[q] = recv_off[q] = recv_bytes[q] = 0; }
+  const earl_comm* c = p->comm;
   int g, k, t;
-  // sends: this rank's message to dst shard ds goes to every replica td == ts (mod tp_src)
+  // sends: this rank's message to dst shard ds goes to every replica td == ts (mod tp_src);
+  // a multi-node comm (NEXT-4) stages only the messages that leave the node
   if (coords(S, rank, &g, &k, &t) && t < nts) {
     const int ss = g * S.sp + k;
     for (int d = 0; d < W; ++d) {
       int gd, kd, td;
       if (!coords(D, d, &gd, &kd, &td) || td % S.tp != t) continue;
+      if (c->node_size > 0 && same_node(c, d, rank)) continue;
       const int ds = gd * D.sp + kd;
       send_off[d] = h.msg_off[ss * Sd + ds];
       send_bytes[d] = msg_bytes(ss * Sd + ds);
@@ -1537,6 +1588,7 @@ void message_table(earl_plan_t p, int rank, int64_t* send_off, int64_t* send_byt
     for (int s = 0; s < W; ++s) {
       int gs, ks, ts;
       if (!coords(S, s, &gs, &ks, &ts) || ts >= nts || t % S.tp != ts) continue;
+      if (c->node_size > 0 && same_node(c, s, rank)) continue;
       const int key = (gs * S.sp + ks) * Sd + ds;
       recv_off[s] = off;
       recv_bytes[s] = msg_bytes(key);
@@ -1685,6 +1737,17 @@ extern "C" earl_status_t earl_dispatch_exec_staged(earl_plan_t p, const void* co
   if ((st = earl_dispatch_pack(p, send_bufs, stage_s, stream)) != EARL_OK) return st;
   if ((st = exchange_impl(p, c->nst[0], c->nst[1], stream)) != EARL_OK) return st;
   return earl_dispatch_unpack(p, stage_r, recv_bufs, stream);
+}
+
+extern "C" earl_status_t earl_dispatch_exec_hier(earl_plan_t p, const void* const* send_bufs,
+                                                 void* const* recv_bufs, void* stream) {
+  NvtxRange nvtx("earl_dispatch_exec_hier");
+  if (!p) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (p->comm->node_size == 0)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "earl_comm_set_nodes was not called (one node: use earl_dispatch_exec)");
+  earl_status_t st = exec_impl(p, -1, send_bufs, recv_bufs, stream);  // inside the node: fused P2P
+  if (st != EARL_OK) return st;
+  return earl_dispatch_exec_staged(p, send_bufs, recv_bufs, stream);  // across nodes: NCCL
 }
 
 // ---------------------------------------------------------------------------------------

@@ -58,17 +58,19 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   return v;
 }
 
-// Signal every peer (store `value` into slot `slot_base + me` of its pad), then wait until every
+// Signal every peer of `peers` (bit p: rank p takes part; a multi-node comm's peers are its node's
+// ranks) by storing `value` into slot `slot_base + me` of its pad, then wait until every such
 // peer's slot in my pad holds at least `want`.  Lane p handles peer p.  Returns the mask of peers
 // that timed out; *got (lane p) is the value peer p left in my pad.
-__device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
+__device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad, uint32_t peers, int me,
                                     int slot_base, uint64_t value, uint64_t want,
                                     uint64_t timeout_ns, uint64_t* got) {
   const int lane = threadIdx.x & 31;
-  if (lane < world && lane != me) st_release_sys(peer_pad[lane] + slot_base + me, value);
+  const bool mine = (peers >> lane & 1u) && lane != me;
+  if (mine) st_release_sys(peer_pad[lane] + slot_base + me, value);
   unsigned missing = 0;
   uint64_t v = want;
-  if (lane < world && lane != me) {
+  if (mine) {
     const uint64_t t0 = globaltimer();
     while ((v = ld_acquire_sys(my_pad + slot_base + lane)) < want) {
       if (globaltimer() - t0 > timeout_ns) { missing = 1u << lane; break; }
@@ -91,9 +93,9 @@ __device__ unsigned signal_and_wait(uint64_t* my_pad, uint64_t* const* peer_pad,
 // Ordering: a peer reads these offsets only after acquiring this epoch's ready flag, and this
 // rank rewrites them only in its next exec, after every peer released its done flag (i.e.
 // finished reading).
-__global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world, int me,
-                                     int n_fields, RecvOffsets offs, McTeams mct, uint64_t timeout_ns,
-                                     int32_t* err, int32_t* err_detail) {
+__global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world, uint32_t peers,
+                                     int me, int n_fields, RecvOffsets offs, McTeams mct,
+                                     uint64_t timeout_ns, int32_t* err, int32_t* err_detail) {
   const int lane = threadIdx.x & 31;
   uint64_t epoch = 0;
   if (lane == 0) {
@@ -105,14 +107,14 @@ __global__ void entry_barrier_kernel(uint64_t* my_pad, PeerPads pads, int world,
   __threadfence_system();
   __syncwarp();
   delay_inject(1);
-  const unsigned miss = signal_and_wait(my_pad, pads.p, world, me, kReadySlot, epoch, epoch,
+  const unsigned miss = signal_and_wait(my_pad, pads.p, peers, me, kReadySlot, epoch, epoch,
                                         timeout_ns, nullptr);
   // lane p: peer p's (or, for p == me, this rank's own) destination bases
   uint64_t* tab = my_pad + kDstTabSlot;
   if (lane < kMaxWorld) {
     for (int f = 0; f < kMaxFields; ++f) {
       uint64_t o = kNoOffset;
-      if (lane < world && f < n_fields && !(miss >> lane & 1)) {
+      if (lane < world && (lane == me || (peers >> lane & 1u)) && f < n_fields && !(miss >> lane & 1)) {
         o = lane == me ? offs.v[f]
                        : *reinterpret_cast<volatile const uint64_t*>(pads.p[lane] + kOffSlot + f);
       }
@@ -168,7 +170,9 @@ struct __align__(16) SubDesc {
   const uint8_t* src_al;  // 16-B aligned source address of the load
   uint8_t* dst0;          // destination of the first byte for replica 0
   uint32_t so;            // stage offset of the load (multiple of 16)
-  uint32_t load_bytes;    // multiple of 16
+  uint16_t load_bytes;    // multiple of 16 (<= CHUNK <= 16 KB)
+  uint8_t rmask;          // replicas r < R that receive (a NULL receive buffer, another node)
+  uint8_t pad_;
   uint32_t len;           // bytes
   uint8_t off;            // src & 15
   uint8_t R;              // destination replicas
@@ -259,7 +263,14 @@ __device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
   if (a.view_rank < 0) {
     add(0, h->n_records, nullptr);
   } else if (a.mode != kUnpack) {
-    add(h->rec_begin[a.view_rank], h->rec_begin[a.view_rank + 1], nullptr);
+    if (a.ds_mask == ~0u) {
+      add(h->rec_begin[a.view_rank], h->rec_begin[a.view_rank + 1], nullptr);
+    } else {  // NEXT-4: only the destination shards in ds_mask (messages that leave the node)
+      const int Sd = a.n_dst_shards, r = a.view_rank;
+      for (int ds = 0; ds < Sd; ++ds)
+        if (a.ds_mask >> ds & 1u)
+          add(h->rec_base[r][ds], ds + 1 < Sd ? h->rec_base[r][ds + 1] : h->rec_begin[r + 1], nullptr);
+    }
   } else {
     const int Sd = a.n_dst_shards;
     const int rr = a.me - a.rank0_d;
@@ -271,6 +282,7 @@ __device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
       if (q < 0 || q >= a.n_src_shards * a.tp_s) continue;
       const int ts = q % a.tp_s, ss = q / a.tp_s;
       if (ts >= a.nts || td % a.tp_s != ts) continue;
+      if (!(a.src_mask >> s & 1u)) continue;  // NEXT-4: messages from other nodes only
       const int key = ss * Sd + ds;
       const int64_t rb = h->rec_base[s][ds];
       const int64_t re = (ds + 1 < Sd) ? h->rec_base[s][ds + 1] : h->rec_begin[s + 1];
@@ -308,7 +320,7 @@ struct Walker {
   // current piece (its own field and replica-0 rank: the walker may already have advanced)
   const uint8_t* psrc;
   uint8_t* pdst;
-  uint32_t R;
+  uint32_t R, rmask;
   uint64_t prem;
   int pf, pd0;
   uint8_t* const* dt;  // the launch's destination field bases [kMaxWorld][kMaxFields] (smem)
@@ -418,22 +430,35 @@ struct Walker {
         if (a.mode == kPack) {
           pdst = a.stage[s] + msg_field;
           R = 1;
+          rmask = 1;
           pd0 = d0;
         } else if (unpack_rank) {
           uint8_t* base = dt[a.me * kMaxFields + f];
           pdst = base + dst_tok * (int64_t)Bf + (int64_t)u0;
           R = base != nullptr ? 1 : 0;
+          rmask = 1;
           pd0 = a.me;
         } else {
+          // replicas td = ts, ts + tp_s, ... of the shard; the ones with a receive buffer in
+          // this launch (NULL: the rank receives nothing, or it is on another node) form rmask,
+          // counted from the first present one
+          uint32_t m = 0;
+          int nrep = 0;
+          for (int td = ts; td < a.tp_d; td += a.tp_s, ++nrep)
+            if (dt[(d0 + (td - ts)) * kMaxFields + f] != nullptr) m |= 1u << nrep;
           R = 0;
-          uint8_t* base0 = dt[d0 * kMaxFields + f];
-          for (int td = ts; td < a.tp_d; td += a.tp_s)
-            if (dt[(d0 + (td - ts)) * kMaxFields + f] != nullptr) ++R;
-          pdst = base0 + dst_tok * (int64_t)Bf + (int64_t)u0;
-          if (base0 == nullptr) R = 0;
+          rmask = 0;
           pd0 = d0;
+          if (m) {
+            const int r0 = __ffs(m) - 1;
+            rmask = m >> r0;
+            R = 32 - __clz(rmask);
+            pd0 = d0 + r0 * a.tp_s;
+            pdst = dt[pd0 * kMaxFields + f] + dst_tok * (int64_t)Bf + (int64_t)u0;
+          }
           // NEXT-3: every replica of this shard is in a multicast team with this rank
-          if (mt != nullptr && R > 1 && mt[ds * kMaxFields + f] != nullptr) R |= 0x80u;
+          if (mt != nullptr && R > 1 && rmask == (1u << R) - 1u && mt[ds * kMaxFields + f] != nullptr)
+            R |= 0x80u;
         }
         prem = u1 - u0;
         pf = f;
@@ -478,8 +503,9 @@ struct Walker {
     d.dst0 = pdst;
     d.off = (uint8_t)off;
     d.len = len;
-    d.load_bytes = (off + len + 15) & ~15u;
+    d.load_bytes = (uint16_t)((off + len + 15) & ~15u);
     d.R = (uint8_t)R;
+    d.rmask = (uint8_t)rmask;
     d.f = (uint8_t)pf;
     d.d0 = (uint8_t)pd0;
     psrc += len;
@@ -512,15 +538,18 @@ __device__ __forceinline__ bool fill_stage(const CopyArgs& a, const View& v, Wal
 // The realigning warp-store loop of a non-congruent range: 16-B outputs k = lane, lane + 32, ...
 // from the 32 bytes at sp + 16 (k - lane), one st.global.v4 per replica.
 template <int R, int S4>
-__device__ __forceinline__ void realign_loop(uint8_t* (&q)[R], const uint8_t* sp, uint32_t nvec,
-                                             int bits, int lane) {
+__device__ __forceinline__ void realign_loop(uint8_t* (&q)[R], const bool (&on)[R], const uint8_t* sp,
+                                             uint32_t nvec, int bits, int lane) {
 #pragma unroll 2
   for (uint32_t k = lane; k < nvec; k += 32) {
     const uint4 w0 = *reinterpret_cast<const uint4*>(sp);
     const uint4 w1 = *reinterpret_cast<const uint4*>(sp + 16);
     const uint4 o = realign<S4>(w0, w1, bits);
 #pragma unroll
-    for (int r = 0; r < R; ++r) { st_v4(q[r], o); q[r] += 512; }
+    for (int r = 0; r < R; ++r) {
+      if (on[r]) st_v4(q[r], o);
+      q[r] += 512;
+    }
     sp += 512;
   }
 }
@@ -528,13 +557,18 @@ __device__ __forceinline__ void realign_loop(uint8_t* (&q)[R], const uint8_t* sp
 // Store one landed source range to its R destination replicas (whole warp); R is a
 // compile-time constant so the replica pointers stay in registers and the realign loop is
 // ~12 instructions per 512 B (a runtime-R loop cost ~100: profiles/r01_c5lt_note.txt).
+// Replica r receives only if bit r of S.rmask is set (its rank passed a receive buffer and, in a
+// multi-node comm, is on this node).
 template <int R>
 __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* dt, const SubDesc& S,
                                             uint8_t* stage, int lane) {
   const uint32_t len = S.len;
   const uint8_t* sm = stage + S.so + S.off;
   uint8_t* dp[R];
+  bool on[R];
   dp[0] = S.dst0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) on[r] = (S.rmask >> r) & 1u;
 #pragma unroll
   for (int r = 1; r < R; ++r)
     dp[r] = S.dst0 + (dt[(S.d0 + r * a.tp_s) * kMaxFields + S.f] - dt[S.d0 * kMaxFields + S.f]);
@@ -543,7 +577,8 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
   if (lane < (int)head) {
     const uint8_t v = sm[lane];
 #pragma unroll
-    for (int r = 0; r < R; ++r) dp[r][lane] = v;
+    for (int r = 0; r < R; ++r)
+      if (on[r]) dp[r][lane] = v;
   }
   const uint32_t rest = len - head;
   const uint32_t nvec = rest >> 4;
@@ -557,13 +592,13 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
       bool any_remote = false;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        remote[r] = !a.remote_tma && a.mode != kPack && a.me >= 0 && (S.d0 + r * a.tp_s) != a.me;
+        remote[r] = on[r] && !a.remote_tma && a.mode != kPack && a.me >= 0 && (S.d0 + r * a.tp_s) != a.me;
         any_remote |= remote[r];
       }
       if (lane == 0) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          if (!remote[r]) tma_store(dp[r] + head, stage + smo, nvec * 16);
+          if (on[r] && !remote[r]) tma_store(dp[r] + head, stage + smo, nvec * 16);
       }
       if (any_remote) {
         for (uint32_t k = lane; k < nvec; k += 32) {
@@ -581,10 +616,10 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
 #pragma unroll
       for (int r = 0; r < R; ++r) q[r] = dp[r] + head + 16 * lane;
       switch (sh >> 2) {
-        case 0: realign_loop<R, 0>(q, sp, nvec, bits, lane); break;
-        case 1: realign_loop<R, 1>(q, sp, nvec, bits, lane); break;
-        case 2: realign_loop<R, 2>(q, sp, nvec, bits, lane); break;
-        default: realign_loop<R, 3>(q, sp, nvec, bits, lane); break;
+        case 0: realign_loop<R, 0>(q, on, sp, nvec, bits, lane); break;
+        case 1: realign_loop<R, 1>(q, on, sp, nvec, bits, lane); break;
+        case 2: realign_loop<R, 2>(q, on, sp, nvec, bits, lane); break;
+        default: realign_loop<R, 3>(q, on, sp, nvec, bits, lane); break;
       }
     }
   }
@@ -592,7 +627,8 @@ __device__ __forceinline__ void store_sub_r(const CopyArgs& a, uint8_t* const* d
   if (lane < (int)(len - t0)) {
     const uint8_t v = sm[t0 + lane];
 #pragma unroll
-    for (int r = 0; r < R; ++r) dp[r][t0 + lane] = v;
+    for (int r = 0; r < R; ++r)
+      if (on[r]) dp[r][t0 + lane] = v;
   }
 }
 
@@ -796,10 +832,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       const uint64_t epoch = *reinterpret_cast<volatile uint64_t*>(a.my_pad + kEpochSlot);
       const uint64_t failed = *reinterpret_cast<volatile const int32_t*>(a.err) != 0 ? 1 : 0;
       uint64_t got = 0;
-      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.world, a.me, kDoneSlot,
+      const unsigned miss = signal_and_wait(a.my_pad, a.peer_pad, a.peer_mask, a.me, kDoneSlot,
                                             2 * epoch + failed, 2 * epoch, a.timeout_ns, &got);
       const int lane = threadIdx.x;
-      const unsigned bad = __ballot_sync(kFull, lane < a.world && lane != a.me &&
+      const unsigned bad = __ballot_sync(kFull, (a.peer_mask >> lane & 1u) && lane != a.me &&
                                                     !(miss >> lane & 1) && got == 2 * epoch + 1);
       if (lane == 0 && (miss | bad)) {
         if (atomicCAS(a.err, 0, EARL_ERR_TIMEOUT) == 0) *a.err_detail = (int32_t)(miss | bad << 8);
@@ -855,16 +891,16 @@ cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t
   }
 }
 
-cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 int n_fields, const uint64_t* recv_off, const McTeams& mct,
-                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
-                                 cudaStream_t s) {
+cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world,
+                                 uint32_t peers, int me, int n_fields, const uint64_t* recv_off,
+                                 const McTeams& mct, uint64_t timeout_ns, int32_t* err,
+                                 int32_t* err_detail, cudaStream_t s) {
   PeerPads pads;
   for (int p = 0; p < kMaxWorld; ++p) pads.p[p] = peer_pad[p];
   RecvOffsets offs;
   for (int f = 0; f < kMaxFields; ++f) offs.v[f] = f < n_fields ? recv_off[f] : kNoOffset;
-  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, me, n_fields, offs, mct, timeout_ns,
-                                        err, err_detail);
+  entry_barrier_kernel<<<1, 32, 0, s>>>(my_pad, pads, world, peers, me, n_fields, offs, mct,
+                                        timeout_ns, err, err_detail);
   return cudaGetLastError();
 }
 

@@ -122,6 +122,9 @@ struct CopyArgs {
   int32_t protocol;        // 1: multi-process fused exec (epoch release / acquire at the end)
   int32_t remote_tma;      // 1: peer replicas by bulk TMA stores too (EARL_REMOTE_STORE=tma)
   int32_t mc_on;           // NEXT-3: some dst shard's replicas form a multicast team with this rank
+  uint32_t peer_mask;      // ranks taking part in the completion protocol (a node's, NEXT-4)
+  uint32_t ds_mask;        // pack (real rank): destination shards to pack (~0: all)
+  uint32_t src_mask;       // unpack (real rank): source ranks whose messages are in recv_stage
   uint8_t* const* mc_tab;  // [kMaxShards][kMaxFields] multicast bases (entry barrier), protocol 1
   const uint8_t* recv_stage;                  // unpack on a real rank: received messages
   uint32_t Bf[kMaxFields];
@@ -294,10 +297,10 @@ cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cu
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem, bool fast);
 cudaError_t launch_planner(const PlanArgs& a, size_t lpt_smem, int grid, bool fast, cudaStream_t s);
 cudaError_t launch_copy(const CopyArgs& a, int sm_count, int shape, cudaStream_t s);
-cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world, int me,
-                                 int n_fields, const uint64_t* recv_off, const McTeams& mct,
-                                 uint64_t timeout_ns, int32_t* err, int32_t* err_detail,
-                                 cudaStream_t s);
+cudaError_t launch_entry_barrier(uint64_t* my_pad, uint64_t* const* peer_pad, int world,
+                                 uint32_t peers, int me, int n_fields, const uint64_t* recv_off,
+                                 const McTeams& mct, uint64_t timeout_ns, int32_t* err,
+                                 int32_t* err_detail, cudaStream_t s);
 cudaError_t launch_gather_lengths(const LensArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_fill_i32(int32_t* p, int32_t v, int64_t n, cudaStream_t s);
 cudaError_t launch_local_meta(const PlanArgs& a, int rank_g, int rank_k, int32_t* cu, int64_t* ids,

@@ -148,7 +148,9 @@ def max_over_ranks(values, group=None):
 class Dispatcher:
     """One process per GPU (torch.distributed initialised).  Fused P2P exchange."""
 
-    def __init__(self, window_bytes: int, device=None, group=None):
+    def __init__(self, window_bytes: int, device=None, group=None, node_size=None):
+        """node_size (NEXT-4): ranks per node when the group spans nodes; only same-node
+        windows are mapped, exec moves the node-local records, exec_hier adds the rest."""
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -156,6 +158,9 @@ class Dispatcher:
         self.world = dist.get_world_size(group)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
         self.comm = Comm(self.rank, self.world, self.device.index, window_bytes)
+        self.node_size = node_size if node_size and node_size < self.world else None
+        if self.node_size:
+            self.comm.set_nodes(self.node_size)
         if self.world > 1:
             handles = [None] * self.world
             dist.all_gather_object(handles, self.comm.export_handle(), group=group)
@@ -285,6 +290,16 @@ class Dispatcher:
             self.comm.mc_join(mask, handle)
             masks.append(mask)
         return masks
+
+    def exec_hier(self, plan, send_bufs, recv_bufs, stream=None):
+        """NEXT-4: the fused P2P exec inside this rank's node, then the messages between nodes
+        (the library's NCCL exchange after init_nccl, else over the process group -- gloo in the
+        one-GPU tests, where 'nodes' are groups of processes)."""
+        if getattr(self, "_nccl", False):
+            plan.exec_hier(send_bufs, recv_bufs, stream)
+            return
+        plan.exec(send_bufs, recv_bufs, stream)
+        self.exec_staged(plan, send_bufs, recv_bufs, stream=stream)
 
     def init_nccl(self):
         """K8: the library's own NCCL communicator over this group's ranks (rank 0 draws the

@@ -42,7 +42,8 @@ EXPORTED = [
     "earl_policy_table", "earl_policy_select", "earl_policy_destroy", "earl_plan_mean_length",
     "earl_allgather_lengths", "earl_comm_check", "earl_comm_peer_mask",
     "earl_nccl_unique_id", "earl_comm_init_nccl", "earl_dispatch_exchange", "earl_dispatch_exec_staged",
-    "earl_plan_seq_fields", "earl_comm_mc_create", "earl_comm_mc_join",
+    "earl_plan_seq_fields", "earl_comm_mc_create", "earl_comm_mc_join", "earl_comm_set_nodes",
+    "earl_dispatch_exec_hier",
 ]
 
 
@@ -129,6 +130,8 @@ def lib():
         "earl_dispatch_exec_staged": [vp, pvp, pvp, vp],
         "earl_plan_seq_fields": [vp, C.POINTER(Field), i32, vp, pvp],
         "earl_comm_mc_create": [vp, C.c_uint32, vp],
+        "earl_comm_set_nodes": [vp, i32],
+        "earl_dispatch_exec_hier": [vp, pvp, pvp, vp],
         "earl_comm_mc_join": [vp, C.c_uint32, vp],
         "earl_dispatch_plan": [vp, C.POINTER(Layout), C.POINTER(Layout), vp, i64,
                                C.POINTER(Field), i32, vp, pvp],
@@ -280,6 +283,10 @@ class Comm:
         buf = (C.c_uint8 * EARL_HANDLE_BYTES).from_buffer_copy(unique_id)
         check(lib().earl_comm_init_nccl(self.h, buf))
 
+    def set_nodes(self, node_size: int):
+        """earl_comm_set_nodes (NEXT-4): node_size consecutive ranks per node; before import."""
+        check(lib().earl_comm_set_nodes(self.h, int(node_size)))
+
     def mc_create(self, team_mask: int) -> bytes:
         """earl_comm_mc_create (NEXT-3; the team's lowest rank): the team handle to broadcast."""
         buf = (C.c_uint8 * EARL_HANDLE_BYTES)()
@@ -429,6 +436,11 @@ class Plan:
         """earl_dispatch_exchange: grouped ncclSend / ncclRecv of this rank's messages."""
         check(lib().earl_dispatch_exchange(self.h, _ptr(send_stage) or None, _ptr(recv_stage) or None,
                                            _stream(stream)))
+
+    def exec_hier(self, send_bufs, recv_bufs, stream=None):
+        """earl_dispatch_exec_hier (NEXT-4): fused P2P inside the node, NCCL between nodes."""
+        s, r = _ptr_array(send_bufs), _ptr_array(recv_bufs)
+        check(lib().earl_dispatch_exec_hier(self.h, s, r, _stream(stream)))
 
     def exec_staged(self, send_bufs, recv_bufs, stream=None):
         """earl_dispatch_exec_staged: pack + NCCL exchange + unpack (library stage buffers)."""

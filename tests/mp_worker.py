@@ -518,3 +518,67 @@ def gpu_nvls_main(rank, world, port, q, case):
         q.put((rank, "ok" if msg.startswith("ok") else msg))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_hier_main(rank, world, port, q, case):
+    """NEXT-4 with virtual nodes on one GPU: node_size consecutive processes form a 'node'
+    (CUDA-IPC windows mapped inside it only); exec_hier = the fused P2P exec inside the node +
+    the node-to-node messages (pack of the shards with a replica on another node, exchange over
+    the process group -- NCCL between real nodes, gloo here -- unpack of the other nodes'
+    messages).  Every destination byte equals the oracle's; the device length gather refuses
+    a multi-node comm."""
+    try:
+        import numpy as np
+        import torch
+        from oracle import earl_oracle as O
+        from paper_2510_05943_b200 import workloads as W
+        from paper_2510_05943_b200.dispatch import Dispatcher, rank_counts
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        lens, src, dst, fields, node_size = case
+        T = sum(lens)
+        glob = W.gen_global_fields(fields, T, seed_base=57, random_bits=True)
+        src_arrays = O.rank_arrays_from_global(src, lens, O.assign_groups(src, lens), glob, fields)
+        want, _, _ = O.dispatch(src, dst, lens, src_arrays, fields, world)
+        D = Dispatcher(window_bytes=T * W.bytes_per_token(fields) + (1 << 20), device=0,
+                       node_size=node_size)
+        node = rank // node_size
+        for p in range(world):
+            if p != rank:
+                assert D.comm.peer_mapped(p) == (p // node_size == node), (rank, p)
+        mine = [torch.from_numpy(a).cuda() if a.size else None for a in src_arrays.get(rank, [])] \
+            if rank in src_arrays else [None] * len(fields)
+        if src.get("assign") == "given_counts":
+            cnts = rank_counts(src, world)
+            edges = np.concatenate([[0], np.cumsum(cnts)]).astype(int)
+            local = torch.as_tensor(np.asarray(lens[edges[rank]:edges[rank + 1]], dtype=np.int32)).cuda()
+            try:
+                D.allgather_lens(local, counts=cnts)
+                raise AssertionError("device gather accepted a multi-node comm")
+            except EarlError as e:
+                assert e.name == "EARL_ERR_UNSUPPORTED", e
+            glens, _ = D.allgather_lens(local)  # the process-group path
+        else:
+            glens = torch.as_tensor(np.asarray(lens, dtype=np.int32)).cuda()
+        assert glens.cpu().tolist() == list(lens)
+        for it in range(2):
+            plan = D.plan(src, dst, glens, fields)
+            ptrs, views = D.alloc_recv(plan, fields)
+            for v in views:
+                v.fill_(0xA5)
+            torch.cuda.synchronize()
+            D.exec_hier(plan, mine, ptrs)
+            torch.cuda.synchronize()
+            plan.sync()
+            if rank in want:
+                for f in range(len(fields)):
+                    got = views[f].cpu().numpy()
+                    assert np.array_equal(got, want[rank][f]), f"iter {it} rank {rank} field {f}"
+            plan.destroy()
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

@@ -98,9 +98,11 @@ def _host_bytes_available():
         return None
 
 
-@pytest.mark.parametrize("config,fields_name,ram_factor", [
-    ("c3", "scalar6-fp32+hidden2560", 9), ("c4", "scalar6-fp32+hidden8192", 3.5)])
-def test_bench_workload_full_digest_parity(config, fields_name, ram_factor):
+@pytest.mark.parametrize("config,fields_name,ram_factor,n_seqs", [
+    ("c3", "scalar6-fp32+hidden2560", 9, 512), ("c4", "scalar6-fp32+hidden8192", 3.5, 512),
+    ("c2-lpt", "scalar6-fp32+hidden2560", 4, 512),
+    ("c5-lt", "scalar6-fp32", 4, 39250)])  # the sweep's 256 MiB/rank long-tail point: misaligned
+def test_bench_workload_full_digest_parity(config, fields_name, ram_factor, n_seqs):
     """SURVEY.md §8(c) GPU parity above 1 GB: the WHOLE bench batch (every byte of every field on
     every destination rank, TP replicas included) as BLAKE2b-256 digests per (rank, field), the
     GPU's fused exec (replan + exec, bench.py's launch) against the oracle's dispatch of the
@@ -115,7 +117,7 @@ def test_bench_workload_full_digest_parity(config, fields_name, ram_factor):
     build.build()
     dev = torch.device("cuda", 0)
     R = 8
-    lens, src, dst, fields, _ = bench.workload(config, R, fields_name)
+    lens, src, dst, fields, _ = bench.workload(config, R, fields_name, n_seqs=n_seqs)
     lens = [int(x) for x in lens]
     F = len(fields)
     payload = sum(lens) * W.bytes_per_token(fields)

@@ -241,3 +241,35 @@ def test_nvls_vmm_windows(name):
         world, lens = 4, W.c4_lengths(0)[:10].tolist()
         src, dst = W.config_layouts("c4", 4, 10)
     run_procs(mp_worker.gpu_nvls_main, world, extra=((lens, src, dst, f),), timeout=600)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c3_2x4", "c4_2x4", "c3_4x2", "tp_spans_nodes", "random_2x3"])
+def test_hierarchical_exec_virtual_nodes(name):
+    """NEXT-4: a comm spanning 'nodes' (groups of processes sharing one GPU): fused P2P inside a
+    node, staged messages between nodes; bit-exact against the oracle."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    f = W.field_set("tiny3") + [("m", 1, 1, "mask"), ("h", 2, 24, "hidden")]
+    if name == "c3_2x4":          # 2 nodes x 4 ranks: DP8 -> DP2 x TP4 (a TP group per node)
+        world, ns, lens = 8, 4, W.c2_lengths(0)[:64].tolist()
+        src, dst = W.config_layouts("c3", 8, 64)
+    elif name == "c4_2x4":        # DP8 -> DP4 x SP2
+        world, ns, lens = 8, 4, W.c4_lengths(0)[:24].tolist()
+        src, dst = W.config_layouts("c4", 8, 24)
+    elif name == "c3_4x2":        # 4 nodes x 2 ranks: every TP4 group spans two nodes
+        world, ns, lens = 8, 2, W.c2_lengths(1)[:48].tolist()
+        src, dst = W.config_layouts("c3", 8, 48)
+    elif name == "tp_spans_nodes":  # one source, a TP4 group across 2 nodes of 2
+        world, ns, lens = 4, 2, W.c2_lengths(2)[:20].tolist()
+        src, dst = W.rollout_layout(20, 1), W.layout(dp=1, tp=4, assign="contig")
+    else:
+        from tests.helpers import random_layout
+        rng = random.Random(29)
+        world, ns, n = 6, 3, 40
+        lens = [rng.randint(0, 300) for _ in range(n)]
+        src = random_layout(rng, world, n, allow_lpt=True)
+        dst = random_layout(rng, world, n, allow_lpt=True)
+    run_procs(mp_worker.gpu_hier_main, world, extra=((lens, src, dst, f, ns),), timeout=900)
