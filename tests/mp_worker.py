@@ -582,3 +582,38 @@ def gpu_hier_main(rank, world, port, q, case):
         q.put((rank, "ok"))
     except Exception:
         q.put((rank, traceback.format_exc()))
+
+
+def gpu_gather_timeout_main(rank, world, port, q, case):
+    """a1's failure detection: the last rank never joins the device length gather; the others'
+    gather kernel times out (EARL_TIMEOUT_MS) and earl_comm_check reports EARL_ERR_TIMEOUT with
+    the missing rank's bit."""
+    try:
+        import os
+        os.environ["EARL_TIMEOUT_MS"] = "300"
+        import numpy as np
+        import torch
+        from paper_2510_05943_b200.dispatch import Dispatcher
+        from paper_2510_05943_b200.earl import EarlError
+        torch.cuda.set_device(0)
+        init(rank, world, port, "gloo")
+        import torch.distributed as dist
+        counts = [5] * world
+        D = Dispatcher(window_bytes=1 << 20, device=0)
+        local = torch.arange(5, dtype=torch.int32, device="cuda") + 10 * rank
+        missing = world - 1
+        msg = "ok"
+        if rank != missing:
+            D.allgather_lens(local, counts=counts)
+            try:
+                D.comm.check()
+                msg = f"rank {rank}: no timeout reported"
+            except EarlError as e:
+                if e.name != "EARL_ERR_TIMEOUT" or f"mask 0x{1 << missing:x}" not in str(e):
+                    msg = f"rank {rank}: unexpected error {e}"
+            D.comm.check()  # the latch was cleared by the report
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, msg))
+    except Exception:
+        q.put((rank, traceback.format_exc()))

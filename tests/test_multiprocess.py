@@ -273,3 +273,14 @@ def test_hierarchical_exec_virtual_nodes(name):
         src = random_layout(rng, world, n, allow_lpt=True)
         dst = random_layout(rng, world, n, allow_lpt=True)
     run_procs(mp_worker.gpu_hier_main, world, extra=((lens, src, dst, f, ns),), timeout=900)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_length_gather_missing_peer_times_out(world):
+    """a1 on the device: a rank that never joins the gather is named by the others' TIMEOUT."""
+    if not _gpu_ok():
+        pytest.skip("needs a GPU")
+    from paper_2510_05943_b200 import build
+    build.build()
+    run_procs(mp_worker.gpu_gather_timeout_main, world, extra=(None,), timeout=300)
