@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/e2e/cpu)")
     ap.add_argument("--exchange", choices=["p2p", "staged"], default="p2p",
                     help="N>1: fused P2P stores (default) or pack + grouped NCCL send/recv + unpack")
+    ap.add_argument("--no-tune", action="store_true",
+                    help="N>1: skip the pass that picks the NVLink store variant by measurement")
     return ap.parse_args()
 
 
@@ -534,6 +536,37 @@ def run_multi(args):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    # choose the NVLink options by measurement (north_star: "whichever ... is faster"): peer
+    # replicas by warp stores or TMA bulk stores, the default copy-engine shape or 8 warps;
+    # every variant moves the same bytes, the fastest (max over ranks) is used for the timed loop
+    tuning = None
+    if not (staged or args.profile or args.no_tune):
+        from paper_2510_05943_b200.dispatch import max_over_ranks as _mor
+        variants = [(-1, -1), (1, -1), (0, 3), (1, 3)]
+        times = []
+        for rs, shape in variants:
+            D.comm.set_exec_options(rs, shape)
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ta_, tb_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta_.record(stream)
+            for _ in range(3):
+                step()
+            tb_.record(stream)
+            torch.cuda.synchronize()
+            times.append(_mor([ta_.elapsed_time(tb_) / 3])[0])
+        best = min(range(len(variants)), key=lambda k: times[k])
+        D.comm.set_exec_options(*variants[best])
+        names = ["warp stores, default shape", "TMA stores, default shape",
+                 "warp stores, 8 warps x 3 x 8 KB", "TMA stores, 8 warps x 3 x 8 KB"]
+        tuning = {"ms_per_step": {names[k]: times[k] for k in range(len(variants))},
+                  "chosen": names[best]}
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     l0 = earl.kernel_launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -680,6 +713,8 @@ def run_multi(args):
         if graph_ms is not None:
             out["graph"] = {"ms_per_step": graph_ms, "value": payload / (graph_ms * 1e-3) / 1e9,
                             "note": "a1 gather + replan + exec captured once as a CUDA graph"}
+        if tuning is not None:
+            out["nvlink_options"] = tuning
         if all_clocks[0] is not None:
             c0 = dict(all_clocks[0])
             c0["per_rank"] = all_clocks

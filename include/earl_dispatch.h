@@ -202,6 +202,14 @@ EARL_API earl_status_t earl_comm_peer_mask(earl_comm_t comm, uint32_t* mask);
  * Errors: INVALID_ARGUMENT (node_size does not divide the world, or peers already imported),
  * UNSUPPORTED (emulated comm). */
 EARL_API earl_status_t earl_comm_set_nodes(earl_comm_t comm, int32_t node_size);
+/* The NVLink options of the multi-process fused exec, for choosing by measurement (the bench's
+ * N > 1 tuning pass): remote_store 0 = peer replicas by 16-B warp stores, 1 = by bulk TMA stores
+ * to the peer address, -1 = EARL_REMOTE_STORE's choice (warp stores by default); p2p_shape = a
+ * copy-engine shape id (1-8, 11, 14; e.g. 3 = 8 warps x 3 stages x 8 KB, 14 = 2 x 2 x 16 KB), or
+ * -1 = EARL_COPY_CFG_P2P's choice (else chosen from the field widths).  Bytes moved are identical
+ * for every setting.  Errors: INVALID_ARGUMENT. */
+EARL_API earl_status_t earl_comm_set_exec_options(earl_comm_t comm, int32_t remote_store,
+                                                  int32_t p2p_shape);
 EARL_API earl_status_t earl_dispatch_exec_hier(earl_plan_t plan, const void* const* send_bufs,
                                                void* const* recv_bufs, void* stream);
 

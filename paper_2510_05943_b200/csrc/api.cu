@@ -111,6 +111,8 @@ struct earl_comm {
   // NEXT-3 (EARL_NVLS=1): the window from cuMemCreate, peers imported by file descriptor, and
   // the multicast teams this rank belongs to (each bound to the whole window at offset 0)
   int32_t node_size = 0;   // NEXT-4: ranks per node (0: the whole comm is one node)
+  int32_t opt_remote_tma = -1;  // earl_comm_set_exec_options (-1: the environment's choice)
+  int32_t opt_p2p_shape = -1;
   bool vmm = false;
   VmmMem vwin{0, 0, 0, -1};
   VmmMem vpeer[kMaxWorld] = {};
@@ -149,7 +151,8 @@ void comm_release(earl_comm* c) {
   if (--c->refs > 0) return;
   DeviceGuard g(c->device);
   cudaDeviceSynchronize();
-  for (int t = 0; t < c->n_teams; ++t) mc_free(&c->teams[t].mc, c->device);
+  for (int t = 0; t < kMaxShards; ++t)  // joined teams, and a created one not joined yet
+    if (c->teams[t].mc.handle) mc_free(&c->teams[t].mc, c->device);
   for (int p = 0; p < kMaxWorld; ++p) {
     if (!c->peer_mapped[p]) continue;
     if (c->vmm) vmm_free(&c->vpeer[p]);
@@ -473,6 +476,20 @@ extern "C" earl_status_t earl_comm_check(earl_comm_t c, void* stream) {
   return fail((earl_status_t)h[0], "length gather: peers missing (mask 0x%x)", h[1]);
 }
 
+extern "C" earl_status_t earl_comm_set_exec_options(earl_comm_t c, int32_t remote_store,
+                                                    int32_t p2p_shape) {
+  if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
+  if (remote_store < -1 || remote_store > 1)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "remote_store %d outside {-1, 0, 1}", remote_store);
+  static const int shapes[] = {-1, 1, 2, 3, 4, 5, 6, 7, 8, 11, 14};
+  bool known = false;
+  for (int v : shapes) known |= v == p2p_shape;
+  if (!known) return fail(EARL_ERR_INVALID_ARGUMENT, "unknown copy-engine shape %d", p2p_shape);
+  c->opt_remote_tma = remote_store;
+  c->opt_p2p_shape = p2p_shape;
+  return EARL_OK;
+}
+
 extern "C" earl_status_t earl_comm_set_nodes(earl_comm_t c, int32_t node_size) {
   if (!c) return fail(EARL_ERR_INVALID_ARGUMENT, "NULL comm");
   if (c->emulated) return fail(EARL_ERR_UNSUPPORTED, "emulated comm: one process holds every rank");
@@ -500,6 +517,8 @@ extern "C" earl_status_t earl_comm_mc_create(earl_comm_t c, uint32_t team_mask, 
   if (team_mask == 0 || (team_mask & ~all) || !(team_mask >> c->rank & 1))
     return fail(EARL_ERR_INVALID_ARGUMENT, "team mask 0x%x: not a subset of the comm containing this rank", team_mask);
   if (c->n_teams >= kMaxShards) return fail(EARL_ERR_CAPACITY, "at most %d multicast teams", kMaxShards);
+  if (c->teams[c->n_teams].mc.handle)
+    return fail(EARL_ERR_INVALID_ARGUMENT, "a created team must be joined (earl_comm_mc_join) before the next");
   DeviceGuard g(c->device);
   VmmMem mc{0, 0, 0, -1};
   const char* why = "";
@@ -1291,11 +1310,12 @@ int congruent_heavy(const CopyArgs& a) {
 // The copy-engine shape of a launch: chosen from the field widths (launch_copy), or, for the
 // multi-process exec whose stores cross NVLink, forced by EARL_COPY_CFG_P2P (a launch_copy
 // shape id; e.g. 3 = 8 warps x 3 x 8 KB, more warps issuing remote stores).
-int launch_shape(const CopyArgs& a) {
-  static const int p2p = [] {
+int launch_shape(const CopyArgs& a, const earl_comm* c) {
+  static const int p2p_env = [] {
     const char* v = getenv("EARL_COPY_CFG_P2P");
     return v ? atoi(v) : -1;
   }();
+  const int p2p = c->opt_p2p_shape >= 0 ? c->opt_p2p_shape : p2p_env;
   if (a.protocol && p2p >= 0) return 100 + p2p;
   return congruent_heavy(a);
 }
@@ -1303,12 +1323,12 @@ int launch_shape(const CopyArgs& a) {
 cudaError_t traced_launch(CopyArgs& a, earl_comm* c, cudaStream_t s) {
   clear_stale_error();
   CopyTrace& t = trace_state();
-  if (!t.path) return launch_copy(a, copy_grid(c), launch_shape(a), s);
+  if (!t.path) return launch_copy(a, copy_grid(c), launch_shape(a, c), s);
   const size_t n = (size_t)c->sm_count * 64 * 4;
   if (!t.dev) { cudaMalloc(&t.dev, n * 8); t.n = n; }
   cudaMemsetAsync(t.dev, 0, n * 8, s);
   a.trace = t.dev;
-  cudaError_t e = launch_copy(a, copy_grid(c), launch_shape(a), s);
+  cudaError_t e = launch_copy(a, copy_grid(c), launch_shape(a, c), s);
   if (e != cudaSuccess) return e;
   std::vector<uint64_t> h(n);
   cudaMemcpyAsync(h.data(), t.dev, n * 8, cudaMemcpyDeviceToHost, s);
@@ -1406,7 +1426,7 @@ earl_status_t exec_impl(earl_plan_t p, int view, const void* const* send_bufs,
       const char* v = getenv("EARL_REMOTE_STORE");
       return v && std::strcmp(v, "tma") == 0 ? 1 : 0;
     }();
-    a.remote_tma = remote_tma;
+    a.remote_tma = c->opt_remote_tma >= 0 ? c->opt_remote_tma : remote_tma;
     // NEXT-3: dst shards whose replicas form one of this rank's multicast teams (each source
     // feeds every replica: tp_src == 1); the entry barrier checks the members' offsets agree
     McTeams mct{};

@@ -43,7 +43,7 @@ EXPORTED = [
     "earl_allgather_lengths", "earl_comm_check", "earl_comm_peer_mask",
     "earl_nccl_unique_id", "earl_comm_init_nccl", "earl_dispatch_exchange", "earl_dispatch_exec_staged",
     "earl_plan_seq_fields", "earl_comm_mc_create", "earl_comm_mc_join", "earl_comm_set_nodes",
-    "earl_dispatch_exec_hier",
+    "earl_dispatch_exec_hier", "earl_comm_set_exec_options",
 ]
 
 
@@ -131,6 +131,7 @@ def lib():
         "earl_plan_seq_fields": [vp, C.POINTER(Field), i32, vp, pvp],
         "earl_comm_mc_create": [vp, C.c_uint32, vp],
         "earl_comm_set_nodes": [vp, i32],
+        "earl_comm_set_exec_options": [vp, i32, i32],
         "earl_dispatch_exec_hier": [vp, pvp, pvp, vp],
         "earl_comm_mc_join": [vp, C.c_uint32, vp],
         "earl_dispatch_plan": [vp, C.POINTER(Layout), C.POINTER(Layout), vp, i64,
@@ -282,6 +283,10 @@ class Comm:
         """earl_comm_init_nccl (collective): the staged exchange's NCCL communicator."""
         buf = (C.c_uint8 * EARL_HANDLE_BYTES).from_buffer_copy(unique_id)
         check(lib().earl_comm_init_nccl(self.h, buf))
+
+    def set_exec_options(self, remote_store: int = -1, p2p_shape: int = -1):
+        """earl_comm_set_exec_options: NVLink store variant and copy-engine shape (-1: default)."""
+        check(lib().earl_comm_set_exec_options(self.h, int(remote_store), int(p2p_shape)))
 
     def set_nodes(self, node_size: int):
         """earl_comm_set_nodes (NEXT-4): node_size consecutive ranks per node; before import."""

@@ -67,6 +67,7 @@ def test_bench_gpus_flag_self_launches_torchrun():
     assert d["n_gpus"] == 2
     assert d["data_plane"]["mapped_peers_per_rank"] == [1, 1]
     assert "graph" in d and d["graph"]["ms_per_step"] > 0
+    assert d["nvlink_options"]["chosen"] in d["nvlink_options"]["ms_per_step"]
 
 
 def test_bench_rejects_world_size_mismatch():
