@@ -5,7 +5,8 @@
  *                          L = [5,17,64,9,33,12,48,21], src DP2 GIVEN_COUNTS [4,4] -> dst DP1),
  *                          one int32 field whose token t of sequence i holds 1000*i + t; checks
  *                          the destination bytes, cu_seqlens and the plan export against the
- *                          hand-worked values of tests/golden/c1_tiny.json.
+ *                          hand-worked values of tests/golden/c1_tiny.json; then the device
+ *                          length gather, a per-sequence field plan and option validation.
  * Exit code 0 on success.
  */
 #include <stdint.h>
@@ -108,9 +109,51 @@ static int gpu_part(void) {
     CHECK(seq[j] == j && s[j] == (j < 4 ? 0 : 1) && d[j] == 0 && x[j] == 0 && y[j] == L[j], "segment %d", j);
     CHECK(dof[j] == want_cu[j], "segment %d dst offset", j);
   }
-  earl_plan_destroy(plan);
+  /* step a1 on the device: the two ranks' local lengths, gathered rank-major */
+  int32_t* d_loc[2] = {NULL, NULL};
+  int32_t* d_glob = NULL;
+  for (int r = 0; r < 2; ++r) {
+    CHECK(cudaMalloc((void**)&d_loc[r], 4 * 4) == cudaSuccess, "malloc");
+    CHECK(cudaMemcpy(d_loc[r], L + 4 * r, 4 * 4, cudaMemcpyHostToDevice) == cudaSuccess, "copy");
+  }
+  CHECK(cudaMalloc((void**)&d_glob, sizeof(L)) == cudaSuccess, "malloc");
+  const void* loc[2] = {d_loc[0], d_loc[1]};
+  CHECK(earl_allgather_lengths(comm, counts, loc, d_glob, NULL) == EARL_OK, "gather: %s", earl_last_error());
+  int32_t glob[8];
+  CHECK(cudaMemcpy(glob, d_glob, sizeof(glob), cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
+  CHECK(memcmp(glob, L, sizeof(L)) == 0, "gathered lengths differ");
+  /* per-sequence fields (reading n4): one int32 record per sequence, routed with the token plan */
+  earl_plan_t splan = NULL;
+  earl_field_t rec = {4, 1};
+  CHECK(earl_plan_seq_fields(plan, &rec, 1, NULL, &splan) == EARL_OK, "seq plan: %s", earl_last_error());
+  int32_t host_rec[2][4];
+  for (int i = 0; i < 8; ++i) host_rec[i / 4][i % 4] = 7 * i + 1;
+  void* d_rec_src[2] = {NULL, NULL};
+  void* d_rec_dst = NULL;
+  for (int r = 0; r < 2; ++r) {
+    CHECK(cudaMalloc(&d_rec_src[r], 16) == cudaSuccess, "malloc");
+    CHECK(cudaMemcpy(d_rec_src[r], host_rec[r], 16, cudaMemcpyHostToDevice) == cudaSuccess, "copy");
+  }
+  CHECK(cudaMalloc(&d_rec_dst, 32) == cudaSuccess, "malloc");
+  const void* rsend[2] = {d_rec_src[0], d_rec_src[1]};
+  void* rrecv[2] = {d_rec_dst, NULL};
+  CHECK(earl_dispatch_exec(splan, rsend, rrecv, NULL) == EARL_OK, "seq exec: %s", earl_last_error());
+  int32_t got_rec[8];
+  CHECK(cudaMemcpy(got_rec, d_rec_dst, 32, cudaMemcpyDeviceToHost) == cudaSuccess, "copy back");
+  for (int i = 0; i < 8; ++i) CHECK(got_rec[i] == 7 * i + 1, "sequence record %d", i);
+  /* options of a multi-process comm are refused on an emulated one, or validated */
+  CHECK(earl_comm_set_nodes(comm, 1) == EARL_ERR_UNSUPPORTED, "set_nodes on an emulated comm");
+  CHECK(earl_comm_set_exec_options(comm, 2, -1) == EARL_ERR_INVALID_ARGUMENT, "remote_store 2");
+  CHECK(earl_comm_set_exec_options(comm, 1, 9) == EARL_ERR_INVALID_ARGUMENT, "shape 9");
+  CHECK(earl_comm_set_exec_options(comm, -1, -1) == EARL_OK, "default options");
+  earl_plan_destroy(plan);   /* the sequence plan keeps its token plan alive */
+  CHECK(earl_dispatch_exec(splan, rsend, rrecv, NULL) == EARL_OK, "seq exec after token destroy");
+  CHECK(cudaDeviceSynchronize() == cudaSuccess, "sync");
+  earl_plan_destroy(splan);
   earl_comm_destroy(comm);
   cudaFree(d_lens); cudaFree(d_src[0]); cudaFree(d_src[1]); cudaFree(d_dst[0]); cudaFree(d_cu);
+  cudaFree(d_loc[0]); cudaFree(d_loc[1]); cudaFree(d_glob); cudaFree(d_rec_src[0]);
+  cudaFree(d_rec_src[1]); cudaFree(d_rec_dst);
   printf("abi_smoke: GPU dispatch checks passed\n");
   return 0;
 }
