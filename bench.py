@@ -162,6 +162,30 @@ class ClockSampler:
                 "samples": len(use), "samples_in_timed_region": len(inwin)}
 
 
+def nvlink_bytes(gpu):
+    """Total NVLink data Tx and Rx bytes of one GPU from `nvidia-smi nvlink -gt d` (an independent
+    cross-check of the plan's byte accounting); None when unavailable."""
+    import re
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu)],
+                             capture_output=True, text=True, timeout=20).stdout
+    except Exception:
+        return None
+    tx = rx = 0
+    seen = False
+    for line in out.splitlines():
+        m = re.search(r"(Tx|Rx)[^:]*:\s*([0-9]+)\s*(KiB|MiB|GiB|B)?", line)
+        if not m:
+            continue
+        seen = True
+        scale = {"KiB": 1024, "MiB": 1 << 20, "GiB": 1 << 30, "B": 1, None: 1024}[m.group(3)]
+        if m.group(1) == "Tx":
+            tx += int(m.group(2)) * scale
+        else:
+            rx += int(m.group(2)) * scale
+    return (tx, rx) if seen else None
+
+
 def emit(obj):
     print(json.dumps(obj), flush=True)
 
@@ -185,13 +209,40 @@ def oracle_prepare(config, fields_name, n_seq_sample, seed=0):
     return (src, dst, lens, src_arrays, fields), sum(lens) * W.bytes_per_token(fields), sum(lens)
 
 
+def oracle_core():
+    """The core the oracle is pinned to (one core, reported): the first core of
+    GPU 0's NUMA node when nvidia-smi reports its CPU affinity, else the first allowed core."""
+    allowed = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else [0]
+    try:
+        out = subprocess.run(["nvidia-smi", "topo", "-m"], capture_output=True, text=True,
+                             timeout=20).stdout
+        for line in out.splitlines():
+            if line.startswith("GPU0"):
+                for tok in line.split():
+                    if "-" in tok and tok.replace("-", "").replace(",", "").isdigit():
+                        first = int(tok.split(",")[0].split("-")[0])
+                        if first in allowed:
+                            return first
+    except Exception:
+        pass
+    return allowed[0]
+
+
 def oracle_run(prep):
-    """Time the oracle's decentralized dispatch once."""
+    """Time the oracle's decentralized dispatch once, pinned to one
+    core (the affinity is restored afterwards)."""
     from oracle import earl_oracle as O
     src, dst, lens, src_arrays, fields = prep
-    t0 = time.perf_counter()
-    O.dispatch(src, dst, lens, src_arrays, fields, 8)
-    return time.perf_counter() - t0
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    if old is not None:
+        os.sched_setaffinity(0, {oracle_core()})
+    try:
+        t0 = time.perf_counter()
+        O.dispatch(src, dst, lens, src_arrays, fields, 8)
+        return time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
 
 
 def cpu_threads():
@@ -225,6 +276,7 @@ def run_reference(args):
           "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
           "config": {"workload": desc, "sample": sample},
           "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                           "pinned_core": oracle_core(),
                            "sample": sample},
           "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
@@ -446,6 +498,7 @@ def run_single(args):
         del prep
         out["cpu_baseline"] = {
             "value": nbytes / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "pinned_core": oracle_core(),
             "host_cores": os.cpu_count(), "affinity_cores": cpu_threads(), "seconds": dt,
             "sample": f"first {CPU_BASELINE_SEQS} sequences ({ntok} tokens, {nbytes} B) of the "
                       f"workload, same layout shapes over 8 simulated ranks; single-threaded "
@@ -568,6 +621,7 @@ def run_multi(args):
         torch.cuda.synchronize()
         dist.barrier()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    nvl0 = nvlink_bytes(local) if not (shared or args.profile) else None
     l0 = earl.kernel_launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
@@ -580,6 +634,11 @@ def run_multi(args):
     t1 = time.time()
     launches = earl.kernel_launch_count() - l0
     from paper_2510_05943_b200.dispatch import max_over_ranks
+    nvl1 = nvlink_bytes(local) if nvl0 is not None else None
+    nvl_counted = None if (nvl0 is None or nvl1 is None) else \
+        {"tx_bytes": nvl1[0] - nvl0[0], "rx_bytes": nvl1[1] - nvl0[1]}
+    all_nvl = [None] * world
+    dist.all_gather_object(all_nvl, nvl_counted)
     my_exec = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     ms_step, t_exec, t_plan, t_a1, neg_exec_min = max_over_ranks(
         [a.elapsed_time(b) / args.steps, my_exec,
@@ -688,7 +747,10 @@ def run_multi(args):
                           "ingress_per_rank": [int(x) for x in st["ingress"]],
                           "self_per_rank": [int(x) for x in st["self"]],
                           "note": "t_exec includes the entry barrier (rank skew): "
-                                  "t_exec_ms is the max, t_exec_min_ms the min over ranks"},
+                                  "t_exec_ms is the max, t_exec_min_ms the min over ranks",
+                          "nvidia_smi_counters_timed_region": all_nvl,
+                          "plan_bytes_timed_region": {"egress_per_rank": [int(x) * args.steps for x in st["egress"]],
+                                                      "ingress_per_rank": [int(x) * args.steps for x in st["ingress"]]}},
                "data_plane": {"kind": "CUDA IPC windows, fused P2P stores" if not staged
                               else ("pack + library NCCL grouped send/recv + unpack" if not shared
                                     else "pack + exchange over the gloo group + unpack"),
