@@ -325,6 +325,7 @@ def run_single(args):
     # the plan object (device scratch) is made once; every step re-plans the batch on the
     # device (earl_plan_replan: header reset + planner) and dispatches it -- no allocation
     splan = ed.plan(src, dst, lens_dev, fields, stream)
+    send_p, recv_p = earl.PtrArray(send), earl.PtrArray(recv)   # marshalled once (earl.PtrArray)
 
     def step(ev=None):
         if ev is not None:
@@ -332,7 +333,7 @@ def run_single(args):
         splan.replan(lens_dev, stream)
         if ev is not None:
             ev[1].record(stream)
-        splan.exec(send, recv, stream)
+        splan.exec(send_p, recv_p, stream)
         if ev is not None:
             ev[2].record(stream)
 
@@ -463,7 +464,7 @@ def run_single(args):
                     ready[r].record(copy_stream)
             for r in range(R):
                 stream.wait_event(ready[r])
-                splan.exec_src(r, send, recv, stream)
+                splan.exec_src(r, send_p, recv_p, stream)
             for r in dst_ranks:
                 splan.local_meta(r, metas[r], None, None, stream)
                 meta_host[r].copy_(metas[r], non_blocking=True)
@@ -564,6 +565,7 @@ def run_multi(args):
     if staged and not shared:
         D.init_nccl()   # K8: the library's grouped ncclSend / ncclRecv (one GPU per rank)
     mplan = D.plan(src, dst, glens, fields, stream)
+    send_p, recv_p = earl.PtrArray(send), earl.PtrArray(recv_ptrs)
 
     def step(ev=None):
         if ev is not None:
@@ -579,7 +581,7 @@ def run_multi(args):
             # per-peer byte table is read from the plan every step (a host sync NCCL needs)
             D.exec_staged(p, send, recv_ptrs, stream=stream)
         else:       # fused P2P: one pass, stores straight into the peers' windows
-            p.exec(send, recv_ptrs, stream)
+            p.exec(send_p, recv_p, stream)
         if ev is not None:
             ev[2].record(stream)
 
@@ -697,7 +699,7 @@ def run_multi(args):
             if staged:
                 D.exec_staged(mplan, send, recv_ptrs, stream=stream)
             else:
-                mplan.exec(send, recv_ptrs, stream)
+                mplan.exec(send_p, recv_p, stream)
             mplan.local_meta(rank, cu_dev, None, None, stream)
             cu_host.copy_(cu_dev, non_blocking=True)
 

@@ -851,9 +851,18 @@ cudaError_t launch_cfg(const CopyArgs& a, int sm_count, cudaStream_t s) {
   auto kern = copy_kernel<WARPS, STAGES, CHUNK, MC>;
   cudaError_t e = opt_in_dynamic_smem(kern, (int)smem, configured);
   if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
-  if (per_sm < 1) per_sm = 1;
+  // resident CTAs per SM of this shape, queried once per device (a host call per launch showed
+  // up in the small-batch step time)
+  static int per_sm_of[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = dev >= 0 && dev < 64 ? per_sm_of[dev] : 0;
+  if (per_sm <= 0) {
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARPS * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (dev >= 0 && dev < 64) per_sm_of[dev] = per_sm;
+  }
   kern<<<sm_count * per_sm, WARPS * 32, smem, s>>>(a);
   return cudaGetLastError();
 }

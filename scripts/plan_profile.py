@@ -15,6 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2510_05943_b200 import workloads as W  # noqa: E402
 from paper_2510_05943_b200.dispatch import EmulatedDispatch  # noqa: E402
+from paper_2510_05943_b200.earl import PtrArray  # noqa: E402
 
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
     if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6.65e12
@@ -50,7 +51,8 @@ def main():
                 for r in range(R) for f in range(F)]
         plan = ed.plan(src, dst, lens_dev, fields)
         st = plan.stats()
-        recv = ed.flat(ed.alloc_recv(plan, fields))
+        recv = PtrArray(ed.flat(ed.alloc_recv(plan, fields)))
+        send = PtrArray(send)
         alg = sum(st["read_bytes"]) + st["total"]
         for _ in range(3):
             plan.replan(lens_dev)

@@ -24,6 +24,7 @@ sys.path.insert(0, ROOT)
 
 from paper_2510_05943_b200 import workloads as W  # noqa: E402
 from paper_2510_05943_b200.dispatch import EmulatedDispatch  # noqa: E402
+from paper_2510_05943_b200.earl import PtrArray  # noqa: E402
 
 NVL = 770e9
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] * 1e9 \
@@ -86,6 +87,8 @@ def main():
                 recv = ed.flat(ed.alloc_recv(p_a, fields))
                 midb = ed.flat(ed.alloc_recv(p_1, fields))
                 recv2 = ed.flat(ed.alloc_recv(p_2, fields))
+                # pointer arrays marshalled once: small sizes are otherwise host-bound
+                send, recv, midb, recv2 = (PtrArray(x) for x in (send, recv, midb, recv2))
 
                 # steady state (the timed region allocates nothing): the plan
                 # objects are made once and every repetition re-plans the batch on the device

@@ -97,3 +97,17 @@ def test_c_program_dispatches_on_gpu(tmp_path):
     r = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "GPU dispatch checks passed" in r.stdout
+
+
+def test_ptr_array_marshals_once():
+    """earl.PtrArray: the pointer array is built once and passed through unchanged; None and 0
+    entries become NULL, ints pass as addresses, tensors as their data pointers."""
+    import torch
+    t = torch.zeros(4, dtype=torch.uint8)
+    pa = earl.PtrArray([t, None, 0x1000, 0])
+    assert len(pa) == 4
+    arr = earl._ptr_array(pa)
+    assert arr is pa.arr and earl._ptr_array(pa) is arr
+    assert [arr[k] for k in range(4)] == [t.data_ptr(), None, 0x1000, None]
+    fresh = earl._ptr_array([t, None, 0x1000, 0])
+    assert [fresh[k] for k in range(4)] == [arr[k] for k in range(4)]
