@@ -846,7 +846,7 @@ struct UnitInfo {
   int ri, r, valid;
 };
 
-__global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_kernel(const __grid_constant__ AggArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_v1_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
   __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
   __shared__ double red[3][32];
@@ -1038,6 +1038,373 @@ __global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_kernel
   returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
 }
 
+// ---------------------------------------------------------------------------------------
+// returns_units_kernel (v2): the unit kernel with a lean per-batch path.  Same units, same ring,
+// same arithmetic; what changed is the bookkeeping around a 512-token batch (the v1 kernel spent
+// ~670 warp instructions per batch, two thirds of them outside the recurrence, ncu source
+// counters in profiles/r02_units_sass.txt):
+//  * lane 0 alone produces: it claims units into a per-warp queue in shared memory (skipping
+//    units that hold no sequence), tracks its own issue cursor and issues the TMA copies; the
+//    other lanes never execute producer code;
+//  * no per-slot flags: producer and consumer derive "this batch came by TMA" from the batch's
+//    range (vec, unit bounds, buffer end), so nothing lives in local memory;
+//  * sequence ends come from a register window of the unit's sequence starts (lane j holds the
+//    j-th start from the right; one ballot per batch, a shuffle per end), not from a shared-memory
+//    bitmap rebuilt every 8 batches;
+//  * a batch fully inside its unit with no sequence end takes a path with constant slopes: the
+//    lane composition shuffles S only (the slopes are gamma^(16 * 2^k) and gamma^(16 * (31 - l)),
+//    per-lane constants), no per-token slope selects, no unit-bound masks;
+//  * the next unit's sequence starts are loaded while the current unit runs (the load's latency
+//    hides behind its batches), and per-sequence returns come from that window too.
+// ---------------------------------------------------------------------------------------
+
+#ifndef EARL_AGG_UQ
+#define EARL_AGG_UQ 8
+#endif
+constexpr int kUQ = EARL_AGG_UQ;  // claimed units queued per warp (power of two)
+#ifndef EARL_AGG_U2CTAS
+#define EARL_AGG_U2CTAS 2
+#endif
+constexpr int kU2Ctas = EARL_AGG_U2CTAS;  // CTAs per SM (8 warps each)
+
+struct UnitQ {
+  int64_t p0, p1;     // sequences [p0, p1) (sorted positions)
+  int64_t ua, ub;     // the unit's tokens [ua, ub) of the rank buffer
+  int64_t base;       // cum[gs] of the rank
+  int32_t ri;         // rank index in the RankTable; -1: no more units
+  int32_t pad;
+};
+
+constexpr int kNoStart = INT32_MIN / 2;  // an empty window entry (left of every batch)
+
+__global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(const __grid_constant__ AggArgs a) {
+  __shared__ RankTable rt;
+  __shared__ double red[3][32];
+  extern __shared__ __align__(128) uint8_t uring_mem[];  // [kWarps][kUSlots][kSlotBytes]
+  __shared__ uint64_t uring_bar[kWarps][kUSlots];
+  __shared__ UnitQ s_q[kWarps][kUQ];
+  __shared__ int s_ok;
+  if (gated_out(a)) return;
+  if (threadIdx.x == 0) {
+    rank_table(a, rt, 1, kUnitTok / kBatch);
+    s_ok = rt.wbeg[rt.n] <= a.win_cap;
+    if (!s_ok && blockIdx.x == 0)
+      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(rt.wbeg[rt.n], (int64_t)INT32_MAX));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
+  const int64_t* cum = a.plan.cum[0];
+  const float gamma = a.gamma;
+  // slopes of the constant-slope path: gpw[k] = gamma^(16 * 2^k) (a lane run of 2^k lanes),
+  // rPl = gamma^(16 * (31 - lane)) (the lanes right of this one), g512 = gamma^512 (a batch)
+  float gpw[5];
+  gpw[0] = a.gamma16;
+#pragma unroll
+  for (int k = 1; k < 5; ++k) gpw[k] = gpw[k - 1] * gpw[k - 1];
+  const float g512 = gpw[4] * gpw[4];
+  float rPl = 1.f;
+#pragma unroll
+  for (int k = 0; k < 5; ++k)
+    if (((31 - lane) >> k) & 1) rPl *= gpw[k];
+
+  uint8_t* ring = uring_mem + (size_t)wid * kUSlots * kSlotBytes;
+  uint64_t* bar = uring_bar[wid];
+  UnitQ* q = s_q[wid];
+  if (lane == 0) {
+    for (int s = 0; s < kUSlots; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+
+  // ---- producer state (lane 0 only) ----
+  int p_nclaim = 0;        // units queued so far
+  int p_iu = -1;           // queue index of the unit being issued
+  int64_t p_pb = 0, p_pbf = 1;  // next batch to issue (descending) and the unit's first batch
+  int64_t p_ua = 0, p_ub = 0, p_ntok = 0;
+  const float* p_rw = nullptr;
+  const uint8_t* p_mk = nullptr;
+  bool p_vec = false, p_done = false;
+  uint32_t p_slot = 0;     // next ring slot to issue into
+  uint32_t p_issued = 0;   // batches issued so far
+
+  // lane 0: claim one unit with sequences into the queue (or an end marker)
+  auto claim = [&]() {
+    UnitQ& e = q[p_nclaim & (kUQ - 1)];
+    for (;;) {
+      delay_inject(8);
+      const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
+      if (u >= total) { e.ri = -1; p_done = true; break; }
+      int ri = 0;
+      while (u >= rt.wbeg[ri + 1]) ++ri;
+      const int64_t k = u - rt.wbeg[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
+      const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
+      const int64_t p0 = a.unit_first[u], p1 = k + 1 < nu ? a.unit_first[u + 1] : pend;
+      if (p0 == p1) continue;  // no sequence starts in this unit's range
+      const int64_t base = cum[gs];
+      e.p0 = p0; e.p1 = p1; e.base = base; e.ri = ri;
+      e.ua = cum[p0] - base; e.ub = cum[p1] - base;
+      break;
+    }
+    ++p_nclaim;
+  };
+  // lane 0: issue batches (right to left through the queued units) until kUSlots - 1 are in
+  // flight beyond the c_n consumed, at most kUQ - 1 units ahead of the consumer's unit kc
+  auto produce = [&](int kc, uint32_t c_n) {
+   while (p_issued - c_n < (uint32_t)(kUSlots - 1)) {
+    while (p_pb < p_pbf) {  // the unit being issued is done: move to the next one
+      if (p_iu + 1 >= p_nclaim) {
+        if (p_done || p_nclaim - kc >= kUQ - 1) return;
+        claim();
+        if (p_done) return;
+      }
+      ++p_iu;
+      const UnitQ& e = q[p_iu & (kUQ - 1)];
+      if (e.ri < 0) { p_pb = 0; p_pbf = 1; return; }  // the end marker
+      const int r = rt.rank[e.ri];
+      p_ua = e.ua; p_ub = e.ub; p_ntok = rt.ntok[e.ri];
+      p_rw = a.rewards[r]; p_mk = a.mask[r];
+      p_vec = aligned(p_rw, 16) && aligned(p_mk, 16);
+      p_pbf = p_ua / kBatch;
+      p_pb = p_ua < p_ub ? (p_ub - 1) / kBatch : p_pbf - 1;  // no batches for an empty unit
+    }
+    const int64_t t0 = p_pb * kBatch;
+    const int64_t lo = max(t0, p_ua), hi = min(t0 + kBatch, p_ub);
+    const int64_t m1 = (hi + 15) & ~15LL;
+    const uint32_t b = smem_addr(&bar[p_slot]);
+    if (p_vec && m1 <= p_ntok) {
+      const int64_t r0 = lo & ~3LL, r1 = (hi + 3) & ~3LL, m0 = lo & ~15LL;
+      const uint32_t rb = (uint32_t)(r1 - r0) * 4u, mb = (uint32_t)(m1 - m0);
+      uint8_t* dst = ring + p_slot * kSlotBytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(rb + mb) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_addr(dst + (r0 - t0) * 4)), "l"(p_rw + r0), "r"(rb), "r"(b) : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+          ::"r"(smem_addr(dst + kBatch * 4 + (m0 - t0))), "l"(p_mk + m0), "r"(mb), "r"(b) : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+    }
+    p_slot = p_slot + 1 == kUSlots ? 0 : p_slot + 1;
+    --p_pb;
+    ++p_issued;
+   }
+  };
+
+  if (lane == 0) {
+    claim();
+    produce(0, 0);
+  }
+  __syncwarp();
+
+  // ---- consumer (every lane) ----
+  double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
+  uint32_t c_slot = 0, c_phase = 0;  // bit s: parity of slot s's next completion
+  uint32_t c_n = 0;                  // batches consumed
+  // sequence-start window of the current unit: lane j holds start p1 - j (relative to ua) for
+  // p1 - j > p0, else kNoStart; wq = the sorted position of lane 0's entry
+  auto load_window = [&](const UnitQ& u, int64_t top) -> int {
+    const int64_t p = top - lane;
+    return p > u.p0 ? (int)(cum[p] - u.base - u.ua) : kNoStart;
+  };
+  UnitQ cu = q[0];
+  int ws = cu.ri >= 0 ? load_window(cu, cu.p1) : kNoStart;
+  int nws = kNoStart;        // the next unit's window (loaded ahead)
+  bool nx_loaded = false;
+  for (int kc = 0; cu.ri >= 0; ++kc) {
+    const int ri = cu.ri;
+    const int r = rt.rank[ri];
+    float* G = a.returns[r];
+    const float* rw = a.rewards[r];
+    const uint8_t* mk = a.mask[r];
+    const int64_t ntok = rt.ntok[ri];
+    const bool vec = aligned(rw, 16) && aligned(mk, 16);
+    const bool vstore = aligned(G, 16);
+    const bool count_stats = rt.t[ri] == 0;
+    const int64_t ua = cu.ua, ub = cu.ub;
+    const int ulen = (int)(ub - ua);
+    int64_t wtop = cu.p1;      // sorted position of lane 0's window entry
+    float carry = 0.f;         // G right of the current batch (the unit's last token ends a sequence)
+    const int64_t bf = ua / kBatch;
+    const int64_t bl = ua < ub ? (ub - 1) / kBatch : bf - 1;
+#pragma unroll 1
+    for (int64_t bb = bl; bb >= bf; --bb) {
+      const int64_t t0 = bb * kBatch;
+      const int tb = (int)(t0 - ua);  // the batch's first token, relative to the unit
+      // sequence ends in the batch: starts s with tb < s <= tb + kBatch end a sequence at s - 1
+      uint32_t e = 0;
+      for (;;) {
+        unsigned bal = __ballot_sync(kFull, ws > tb && ws <= tb + kBatch);
+        while (bal) {
+          const int j = __ffs(bal) - 1;
+          bal &= bal - 1;
+          const int pos = __shfl_sync(kFull, ws, j) - 1 - tb;
+          if ((pos >> 4) == lane) e |= 1u << (pos & 15);
+        }
+        const int last = __shfl_sync(kFull, ws, 31);
+        if (last <= tb || wtop - 32 <= cu.p0) break;  // the window reaches left of the batch
+        wtop -= 32;
+        ws = load_window(cu, wtop);
+      }
+      // wait for the batch
+      {
+        const uint32_t b = smem_addr(&bar[c_slot]);
+        const uint32_t parity = (c_phase >> c_slot) & 1u;
+        uint32_t done;
+        do {
+          asm volatile(
+              "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+              " selp.u32 %0, 1, 0, p;\n}\n"
+              : "=r"(done) : "r"(b), "r"(parity) : "memory");
+        } while (!done);
+        c_phase ^= 1u << c_slot;
+      }
+      const int64_t lo = max(t0, ua), hi = min(t0 + kBatch, ub);
+      const bool tma = vec && (((hi + 15) & ~15LL) <= ntok);
+      const int lt = tb + kTokLane * lane;  // this lane's first token, relative to the unit
+      Batch cur;
+      if (tma) {
+        const uint8_t* rb = ring + c_slot * kSlotBytes + 64 * lane;
+        const int rot = (lane >> 1) & 3;
+        float4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
+        float4 u[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cur.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
+        cur.m = *reinterpret_cast<const uint4*>(ring + c_slot * kSlotBytes + kBatch * 4 + 16 * lane);
+      } else {
+        load_batch_in(cur, rw, mk, t0 + kTokLane * lane, lo, hi, vec);
+      }
+      c_slot = c_slot + 1 == kUSlots ? 0 : c_slot + 1;
+      ++c_n;
+      // every lane has read the slot consumed before this one: lane 0 refills it
+      __syncwarp();
+      if (lane == 0) produce(kc, c_n);
+      // the next unit's window, once it is queued (its loads complete behind this unit)
+      if (!nx_loaded) {
+        const int nc = __shfl_sync(kFull, p_nclaim, 0);
+        if (nc > kc + 1) {
+          __syncwarp();
+          const UnitQ nu = q[(kc + 1) & (kUQ - 1)];
+          if (nu.ri >= 0) nws = load_window(nu, nu.p1);
+          nx_loaded = true;
+        }
+      }
+      const uint32_t mk16 = nonzero_bytes4(cur.m.x) | nonzero_bytes4(cur.m.y) << 4 |
+                            nonzero_bytes4(cur.m.z) << 8 | nonzero_bytes4(cur.m.w) << 12;
+      const bool whole = tb >= 0 && tb + kBatch <= ulen;
+      float out[kTokLane];
+      uint32_t on16, st16 = 0xffffu;  // tokens counted / stored
+      if (__all_sync(kFull, e == 0u) && whole) {
+        // constant slopes: no sequence end, every token inside the unit
+        on16 = mk16;
+        float v[kTokLane];
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i) v[i] = (on16 >> i) & 1u ? tok_r(cur, i) : 0.f;
+        float S = 0.f;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(gamma, S, v[i]);
+        float sS = S;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const float o = __shfl_down_sync(kFull, sS, 1 << k);
+          if (lane + (1 << k) < 32) sS = fmaf(gpw[k], o, sS);
+        }
+        float rS = __shfl_down_sync(kFull, sS, 1);
+        if (lane == 31) rS = 0.f;
+        const float tS = __shfl_sync(kFull, sS, 0);
+        float g_next = fmaf(rPl, carry, rS);
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) {
+          out[i] = fmaf(gamma, g_next, v[i]);
+          g_next = out[i];
+        }
+        carry = fmaf(g512, carry, tS);
+      } else {
+        // general: sequence ends (slope 0 at a sequence's last token) and the unit's bounds
+        uint32_t in16 = 0xffffu;
+        if (lt < 0) in16 &= lt + kTokLane <= 0 ? 0u : (0xffffu << (uint32_t)(-lt)) & 0xffffu;
+        if (lt + kTokLane > ulen) in16 &= lt >= ulen ? 0u : 0xffffu >> (uint32_t)(lt + kTokLane - ulen);
+        on16 = in16 & mk16;
+        float v[kTokLane];
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i) v[i] = (on16 >> i) & 1u ? tok_r(cur, i) : 0.f;
+        float S = 0.f;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, v[i]);
+        float rS, rP, bS, bP;
+        warp_compose(S, e ? 0.f : gpw[0], lane, rS, rP, bS, bP);
+        float g_next = rS + rP * carry;
+#pragma unroll
+        for (int i = kTokLane - 1; i >= 0; --i) {
+          out[i] = fmaf(((e >> i) & 1u) ? 0.f : gamma, g_next, v[i]);
+          g_next = out[i];
+        }
+        carry = bS + bP * carry;
+        st16 = in16;
+      }
+      if (count_stats) {
+        float sg = 0.f, sg2 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i) {
+          const float o = (on16 >> i) & 1u ? out[i] : 0.f;
+          sg += o;
+          sg2 = fmaf(o, o, sg2);
+        }
+        s_m += (double)__popc(on16);
+        s_g += (double)sg;
+        s_g2 += (double)sg2;
+      }
+      if (vstore && st16 == 0xffffu) {
+        float4* gp = reinterpret_cast<float4*>(G + ua + lt);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4)
+          __stcs(gp + q4, make_float4(out[4 * q4], out[4 * q4 + 1], out[4 * q4 + 2], out[4 * q4 + 3]));
+      } else {
+        float* gp = G + ua + lt;
+#pragma unroll
+        for (int i = 0; i < kTokLane; ++i)
+          if ((st16 >> i) & 1u) gp[i] = out[i];
+      }
+    }
+    // per-sequence returns G_0 of the unit's sequences [p0, p1)
+    float* SR = a.seq_return[r];
+    if (SR != nullptr) {
+      __syncwarp();  // this warp's G stores precede the reads
+      const int64_t gs = rt.gs[ri];
+      if (wtop == cu.p1 && cu.p1 - cu.p0 <= 32) {
+        // the window still holds every start: lane j takes sequence p1 - 1 - j
+        const int64_t p = cu.p1 - 1 - lane;
+        const int s_next = ws;                                  // start of p + 1
+        int s = __shfl_down_sync(kFull, ws, 1);                 // start of p
+        if (p == cu.p0) s = 0;
+        if (p >= cu.p0) SR[p - gs] = s_next > s ? G[ua + s] : 0.f;
+      } else {
+        unit_seq_returns(SR, G, cum, cu.base, gs, cu.p0, cu.p1, lane);
+      }
+    }
+    // the next unit
+    if (lane == 0) {
+      while (p_nclaim <= kc + 1 && !p_done) claim();
+    }
+    __syncwarp();
+    cu = q[(kc + 1) & (kUQ - 1)];
+    if (cu.ri >= 0) ws = nx_loaded ? nws : load_window(cu, cu.p1);
+    nx_loaded = false;
+    // keep kUSlots - 1 batches in flight
+    if (lane == 0) produce(kc + 1, c_n);
+    __syncwarp();
+  }
+  returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
+}
+
 // A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks: one
 // flattened stream of 4-token quads over all ranks (4 quads in flight per thread), then the
 // unaligned remainders token by token.  Measured on the C5-lt batch: read-only-path loads
@@ -1122,7 +1489,15 @@ cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s)
   static bool opted[64] = {};
   e = opt_in_dynamic_smem(returns_units_kernel, (int)kRingBytes, opted);
   if (e != cudaSuccess) return e;
-  returns_units_kernel<<<sm_count * kUCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
+  static const bool v1 = getenv("EARL_UNITS_V1") != nullptr;
+  if (v1) {
+    static bool opted1[64] = {};
+    e = opt_in_dynamic_smem(returns_units_v1_kernel, (int)kRingBytes, opted1);
+    if (e != cudaSuccess) return e;
+    returns_units_v1_kernel<<<sm_count * kUCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
+  } else {
+    returns_units_kernel<<<sm_count * kU2Ctas, kWarps * 32, kRingBytes, s>>>(a);
+  }
   return cudaGetLastError();
 }
 
