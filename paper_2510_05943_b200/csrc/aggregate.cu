@@ -58,15 +58,17 @@ __device__ bool gated_out(const AggArgs& a) {
   if (threadIdx.x == 0) {
     const PlanHeader* h = a.hdr;
     const LayoutDesc& S = a.plan.lay[0];
-    int64_t units = 0;
+    int64_t units = 0, big = 0;
     for (int r = 0; r < a.world; ++r) {
       if (a.view_rank >= 0 && r != a.view_rank) continue;
       const int q = r - S.rank0;
       if (q < 0 || q >= S.dp * S.tp) continue;
-      units += (*reinterpret_cast<const volatile int64_t*>(&h->shard_tokens[0][q / S.tp]) + kUnitTok - 1) / kUnitTok;
+      const int64_t n = *reinterpret_cast<const volatile int64_t*>(&h->shard_tokens[0][q / S.tp]);
+      units += (n + kUnitTok - 1) / kUnitTok;
+      big = max(big, n);
     }
     const int64_t m = *reinterpret_cast<const volatile int64_t*>(&h->max_len);
-    const bool units_best = prefer_units(m, units, a.resident_warps);
+    const bool units_best = prefer_units(m, units, a.resident_warps, big);
     s_out = a.gate == 1 ? !units_best : units_best;
   }
   __syncthreads();
@@ -665,25 +667,20 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
 
 // ---------------------------------------------------------------------------------------
 // returns_units_kernel: single pass, no look-back.  A unit is the run of whole sequences that
-// start in [k * 4096, (k+1) * 4096) of a rank's buffer (the last unit also takes the trailing
-// zero-length ones), so no return crosses a unit boundary: a warp claims a unit and streams it
-// right to left in 512-token batches through a 3-slot TMA ring (2 batches ahead), composing each
-// batch's lane maps and applying the carry from the batch to its right in registers -- every
-// token read once from HBM and written once, no second pass, no published window maps.  Batches
-// that straddle a unit boundary are loaded lane by lane over the unit's own tokens only.  The
-// unit -> first sequence table comes from unit_table_kernel (one pass over the sequences).
-// Used when the batch's longest sequence is known to be <= kUnitMaxLen (a longer one would be
-// streamed by a single warp); otherwise returns_kernel.
+// start in [k * kUnitTok, (k+1) * kUnitTok) of a rank's buffer (the last unit also takes the
+// trailing zero-length ones), so no return crosses a unit boundary: a warp claims a unit and
+// streams it right to left in 512-token batches through a 3-slot TMA ring (2 batches ahead),
+// composing each batch's lane maps and applying the carry from the batch to its right in
+// registers -- every token read once from HBM and written once, no second pass, no published
+// window maps.  The unit -> first sequence table comes from unit_table_kernel (one pass over the
+// sequences).  Used when the batch's longest sequence is known to be <= kUnitMaxLen (a longer one
+// would be streamed by a single warp); otherwise returns_kernel.
 // ---------------------------------------------------------------------------------------
 
 #ifndef EARL_AGG_USLOTS
 #define EARL_AGG_USLOTS 3
 #endif
 constexpr int kUSlots = EARL_AGG_USLOTS;
-#ifndef EARL_AGG_UCTAS
-#define EARL_AGG_UCTAS 3
-#endif
-constexpr int kUCtasPerSm = EARL_AGG_UCTAS;
 
 // this lane's 16 tokens [t, t+16) restricted to [lo, hi): vector loads when whole and aligned
 __device__ __forceinline__ void load_batch_in(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
@@ -716,91 +713,6 @@ __device__ __forceinline__ uint32_t nonzero_bytes4(uint32_t w) {
   const uint32_t nz = (((w & 0x7f7f7f7fu) + 0x7f7f7f7fu) | w) & 0x80808080u;
   return (nz * 0x00204081u) >> 28;  // bytes' high bits 7, 15, 23, 31 -> bits 28..31
 }
-
-// Per-warp ring of SLOTS batches.  A batch's tokens inside [lo, hi) arrive by TMA bulk copies
-// (rewards from a 4-token boundary, mask from a 16-token boundary: the extra tokens of the
-// granules are masked by the consumer), so the boundary batches of a unit are prefetched like
-// the others; an unaligned buffer, or a granule past the rank buffer's end, falls back to lane
-// loads in get().
-template <int SLOTS>
-struct UnitRing {
-  uint8_t* mem;
-  uint64_t* bar;
-  uint32_t issued, got;
-  bool tma[SLOTS];
-
-  __device__ __forceinline__ void init(uint8_t* m, uint64_t* b, int lane) {
-    mem = m; bar = b; issued = got = 0;
-    for (int s = 0; s < SLOTS; ++s) tma[s] = false;
-    if (lane == 0) {
-      for (int s = 0; s < SLOTS; ++s)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[s])) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-  }
-  // batch [t0, t0 + kBatch) of a rank buffer of ntok tokens, restricted to [lo, hi)
-  __device__ __forceinline__ void issue(const float* rw, const uint8_t* mk, int64_t t0, int64_t lo,
-                                        int64_t hi, int64_t ntok, bool vec, int lane) {
-    const int s = issued % SLOTS;
-    const int64_t a = max(t0, lo), b = min(t0 + kBatch, hi);
-    const int64_t r0 = a & ~3LL, r1 = (b + 3) & ~3LL, m0 = a & ~15LL, m1 = (b + 15) & ~15LL;
-    const bool ok = vec && a < b && r1 <= ntok && m1 <= ntok;
-    tma[s] = ok;
-    __syncwarp();
-    if (lane == 0) {
-      const uint32_t bar_s = smem_addr(&bar[s]);
-      if (ok) {
-        uint8_t* dst = mem + s * kSlotBytes;
-        const uint32_t rb = (uint32_t)(r1 - r0) * 4u, mb = (uint32_t)(m1 - m0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s),
-                     "r"(rb + mb) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_addr(dst + (r0 - t0) * 4)), "l"(rw + r0), "r"(rb), "r"(bar_s) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-            ::"r"(smem_addr(dst + kBatch * 4 + (m0 - t0))), "l"(mk + m0), "r"(mb), "r"(bar_s)
-            : "memory");
-      } else {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s) : "memory");
-      }
-    }
-    ++issued;
-  }
-  // this lane's 16 tokens (starting at t) of the oldest issued batch; tokens outside [lo, hi)
-  // may hold anything (the caller masks them)
-  __device__ __forceinline__ void get(Batch& B, const float* rw, const uint8_t* mk, int64_t t,
-                                      int64_t lo, int64_t hi, bool vec, int lane) {
-    const int s = got % SLOTS;
-    const uint32_t parity = (got / SLOTS) & 1;
-    const uint32_t b = smem_addr(&bar[s]);
-    uint32_t done;
-    do {
-      asm volatile(
-          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-          " selp.u32 %0, 1, 0, p;\n}\n"
-          : "=r"(done) : "r"(b), "r"(parity) : "memory");
-    } while (!done);
-    ++got;
-    if (!tma[s]) {
-      load_batch_in(B, rw, mk, t, lo, hi, vec);
-      return;
-    }
-    const uint8_t* rb = mem + s * kSlotBytes + 64 * lane;
-    const int rot = (lane >> 1) & 3;
-    float4 v[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
-    float4 u[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) B.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
-    B.m = *reinterpret_cast<const uint4*>(mem + s * kSlotBytes + kBatch * 4 + 16 * lane);
-  }
-};
 
 // unit -> first sequence (sorted position p in [gs, pend]) of every unit of every source rank of
 // the launch: unit k of a rank starts at the first sequence whose start is >= k * kUnitTok.
@@ -840,209 +752,9 @@ __device__ __forceinline__ void unit_seq_returns(float* SR, const float* G, cons
   }
 }
 
-// One claimed unit as the warp sees it.
-struct UnitInfo {
-  int64_t p0, p1, ua, ub, bf, bl, base;
-  int ri, r, valid;
-};
-
-__global__ void __launch_bounds__(kWarps * 32, kUCtasPerSm) returns_units_v1_kernel(const __grid_constant__ AggArgs a) {
-  __shared__ RankTable rt;
-  __shared__ uint32_t ends_bm[kWarps][kMaxWin / 32];
-  __shared__ double red[3][32];
-  extern __shared__ __align__(128) uint8_t uring_mem[];  // [kWarps][kUSlots][kSlotBytes]
-  __shared__ uint64_t uring_bar[kWarps][kUSlots];
-  __shared__ int s_ok;
-  __shared__ UnitInfo s_next[kWarps];  // every warp's early-claimed unit (lane 0 writes it)
-  if (gated_out(a)) return;
-  if (threadIdx.x == 0) {
-    rank_table(a, rt, 1, kUnitTok / kBatch);
-    s_ok = rt.wbeg[rt.n] <= a.win_cap;
-    if (!s_ok && blockIdx.x == 0)
-      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(rt.wbeg[rt.n], (int64_t)INT32_MAX));
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
-  const float gamma = a.gamma;
-  const float g16 = a.gamma16;
-  uint32_t* bm = ends_bm[wid];
-  double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
-  UnitRing<kUSlots> ring;
-  ring.init(uring_mem + (size_t)wid * kUSlots * kSlotBytes, uring_bar[wid], lane);
-  const int64_t* cum = a.plan.cum[0];
-  UnitInfo& nx = s_next[wid];
-
-  // lane 0 claims the next unit and resolves its token range into this warp's shared slot
-  auto claim_next = [&]() {
-    delay_inject(8);
-    __syncwarp();  // every lane's reads of the previous claim precede lane 0's writes
-    if (lane == 0) {
-      const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
-      nx.valid = u < total;
-      if (u < total) {
-        int ri = 0;
-        while (u >= rt.wbeg[ri + 1]) ++ri;
-        const int64_t k = u - rt.wbeg[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
-        const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
-        const int64_t p0 = a.unit_first[u], p1 = k + 1 < nu ? a.unit_first[u + 1] : pend;
-        const int64_t base = cum[gs];
-        const int64_t ua = cum[p0] - base, ub = cum[p1] - base;
-        nx.ri = ri;
-        nx.r = rt.rank[ri];
-        nx.p0 = p0;
-        nx.p1 = p1;
-        nx.base = base;
-        nx.ua = ua;
-        nx.ub = ub;
-        nx.bf = ua / kBatch;
-        nx.bl = ua < ub ? (ub - 1) / kBatch : ua / kBatch - 1;  // no batches for an empty unit
-      }
-    }
-    __syncwarp();
-  };
-
-  // Producer: issues batches right to left through the claimed units, kUSlots - 1 ahead of the
-  // consumer; it claims the next unit as soon as the current one is fully issued, so the next
-  // unit's first batches load while this one finishes (units carry nothing between them: there
-  // is no look-back to wait for).
-  claim_next();
-  UnitInfo cu = nx;  // the unit being consumed
-  bool nx_claimed = false;
-  bool p_next = false;   // producer: issuing nx (else cu)
-  int64_t pb = cu.bl;    // producer: next batch to issue
-  auto produce = [&]() {
-    if (!p_next) {
-      if (!cu.valid) return;
-      if (pb >= cu.bf) {
-        const int r = cu.r;
-        const bool vec = aligned(a.rewards[r], 16) && aligned(a.mask[r], 16);
-        ring.issue(a.rewards[r], a.mask[r], pb * kBatch, cu.ua, cu.ub, rt.ntok[cu.ri], vec, lane);
-        --pb;
-        return;
-      }
-      if (!nx_claimed) { claim_next(); nx_claimed = true; }
-      p_next = true;
-      pb = nx.bl;
-    }
-    if (!nx.valid || pb < nx.bf) return;
-    const int r = nx.r;
-    const bool vec = aligned(a.rewards[r], 16) && aligned(a.mask[r], 16);
-    ring.issue(a.rewards[r], a.mask[r], pb * kBatch, nx.ua, nx.ub, rt.ntok[nx.ri], vec, lane);
-    --pb;
-  };
-  for (int d = 0; d < kUSlots - 1; ++d) produce();
-
-  while (cu.valid) {
-    const int r = cu.r;
-    const int64_t ntok_r = rt.ntok[cu.ri];
-    (void)ntok_r;
-    float* G = a.returns[r];
-    const float* rw = a.rewards[r];
-    const uint8_t* mk = a.mask[r];
-    const bool vec = aligned(rw, 16) && aligned(G, 16) && aligned(mk, 16);
-    const bool count_stats = rt.t[cu.ri] == 0;
-    const int64_t ua = cu.ua, ub = cu.ub;
-    float carry = 0.f;  // G right of the unit: its last token ends a sequence
-    int64_t seg_lo = 0;
-#pragma unroll 1
-    for (int64_t bb = cu.bl; bb >= cu.bf; --bb) {
-      if ((cu.bl - bb) % kMaxNB == 0) {  // a new segment of <= 8 batches: its sequence ends
-        seg_lo = max(cu.bf, bb - (kMaxNB - 1));
-        const int nb = (int)(bb - seg_lo + 1);
-        mark_ends(bm, nb * (kBatch / 32), cum, cu.base, cu.p0, cu.p1, seg_lo * kBatch,
-                  min(ub, (bb + 1) * kBatch), lane);
-      }
-      const int64_t lt = bb * kBatch + (int64_t)kTokLane * lane;
-      Batch cur;
-      ring.get(cur, rw, mk, lt, ua, ub, vec, lane);
-      produce();
-      const int bi = (int)(bb - seg_lo);
-      const uint32_t e = (bm[16 * bi + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu;
-      // this lane's tokens inside the unit, and the masked-in ones among them
-      uint32_t in16 = 0xffffu;
-      if (lt < ua) in16 &= lt + kTokLane <= ua ? 0u : (0xffffu << (uint32_t)(ua - lt)) & 0xffffu;
-      if (lt + kTokLane > ub) in16 &= lt >= ub ? 0u : 0xffffu >> (uint32_t)(lt + kTokLane - ub);
-      const uint32_t on16 = in16 & (nonzero_bytes4(cur.m.x) | nonzero_bytes4(cur.m.y) << 4 |
-                                    nonzero_bytes4(cur.m.z) << 8 | nonzero_bytes4(cur.m.w) << 12);
-      float v[kTokLane];
-#pragma unroll
-      for (int i = 0; i < kTokLane; ++i) v[i] = (on16 >> i) & 1u ? tok_r(cur, i) : 0.f;
-      float out[kTokLane];
-      float rS, rP, bS, bP;
-      if (!__any_sync(kFull, e != 0u)) {
-        // no sequence ends in the batch (most batches: sequences are ~thousands of tokens):
-        // every slope is gamma, no per-token selects
-        float S = 0.f;
-#pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(gamma, S, v[i]);
-        warp_compose(S, g16, lane, rS, rP, bS, bP);
-        float g_next = rS + rP * carry;
-#pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) {
-          out[i] = fmaf(gamma, g_next, v[i]);
-          g_next = out[i];
-        }
-      } else {
-        float S = 0.f;
-#pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, v[i]);
-        warp_compose(S, e ? 0.f : g16, lane, rS, rP, bS, bP);
-        float g_next = rS + rP * carry;
-#pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) {
-          out[i] = fmaf(((e >> i) & 1u) ? 0.f : gamma, g_next, v[i]);
-          g_next = out[i];
-        }
-      }
-      if (count_stats) {
-        float sg = 0.f, sg2 = 0.f;
-#pragma unroll
-        for (int i = 0; i < kTokLane; ++i) {
-          const float o = (on16 >> i) & 1u ? out[i] : 0.f;
-          sg += o;
-          sg2 = fmaf(o, o, sg2);
-        }
-        s_m += (double)__popc(on16);
-        s_g += (double)sg;
-        s_g2 += (double)sg2;
-      }
-      if (vec && in16 == 0xffffu) {
-        float4* gp = reinterpret_cast<float4*>(G + lt);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          __stcs(gp + q, make_float4(out[4 * q], out[4 * q + 1], out[4 * q + 2], out[4 * q + 3]));
-      } else {
-#pragma unroll
-        for (int i = 0; i < kTokLane; ++i)
-          if ((in16 >> i) & 1u) G[lt + i] = out[i];
-      }
-      carry = bS + bP * carry;
-    }
-    __syncwarp();
-    unit_seq_returns(a.seq_return[r], G, cum, cu.base, rt.gs[cu.ri], cu.p0, cu.p1, lane);
-    __syncwarp();
-    // move on to the early-claimed unit (or claim one now)
-    if (!nx_claimed) { claim_next(); pb = nx.bl; p_next = true; }
-    cu = nx;
-    nx_claimed = false;
-    p_next = false;  // pb continues where the producer was in this unit
-    // keep kUSlots - 1 batches in flight
-    while (cu.valid && (int)(ring.issued - ring.got) < kUSlots - 1) {
-      const uint32_t before = ring.issued;
-      produce();
-      if (ring.issued == before) break;
-    }
-  }
-  returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
-}
-
 // ---------------------------------------------------------------------------------------
-// returns_units_kernel (v2): the unit kernel with a lean per-batch path.  Same units, same ring,
-// same arithmetic; what changed is the bookkeeping around a 512-token batch (the v1 kernel spent
-// ~670 warp instructions per batch, two thirds of them outside the recurrence, ncu source
-// counters in profiles/r02_units_sass.txt):
+// The per-batch path is kept lean (an earlier version spent ~670 warp instructions per batch,
+// two thirds of them outside the recurrence, by ncu's source counters):
 //  * lane 0 alone produces: it claims units into a per-warp queue in shared memory (skipping
 //    units that hold no sequence), tracks its own issue cursor and issues the TMA copies; the
 //    other lanes never execute producer code;
@@ -1068,15 +780,17 @@ constexpr int kUQ = EARL_AGG_UQ;  // claimed units queued per warp (power of two
 constexpr int kU2Ctas = EARL_AGG_U2CTAS;  // CTAs per SM (8 warps each)
 
 struct UnitQ {
-  int64_t p0, p1;     // sequences [p0, p1) (sorted positions)
-  int64_t ua, ub;     // the unit's tokens [ua, ub) of the rank buffer
-  int64_t base;       // cum[gs] of the rank
+  int64_t base;       // cum[gs] of the rank + ua: the unit's first token as a global prefix
+  int32_t p0, p1;     // sequences [p0, p1) (sorted positions)
+  int32_t ua, ub;     // the unit's tokens [ua, ub) of the rank buffer
   int32_t ri;         // rank index in the RankTable; -1: no more units
   int32_t pad;
 };
 
 constexpr int kNoStart = INT32_MIN / 2;  // an empty window entry (left of every batch)
 
+// Positions inside a rank buffer are int32 here: the kernel refuses (CAPACITY) a rank of more
+// than kU2MaxTok tokens, and prefer_units never picks it for one.
 __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(const __grid_constant__ AggArgs a) {
   __shared__ RankTable rt;
   __shared__ double red[3][32];
@@ -1087,27 +801,27 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   if (gated_out(a)) return;
   if (threadIdx.x == 0) {
     rank_table(a, rt, 1, kUnitTok / kBatch);
-    s_ok = rt.wbeg[rt.n] <= a.win_cap;
+    bool ok = rt.wbeg[rt.n] <= a.win_cap;
+    int64_t big = 0;
+    for (int ri = 0; ri < rt.n; ++ri) big = max(big, rt.ntok[ri]);
+    s_ok = ok && big <= kU2MaxTok;
     if (!s_ok && blockIdx.x == 0)
-      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(rt.wbeg[rt.n], (int64_t)INT32_MAX));
+      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(ok ? big : rt.wbeg[rt.n], (int64_t)INT32_MAX));
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
+  const uint32_t total = s_ok ? (uint32_t)rt.wbeg[rt.n] : 0u;
   const int64_t* cum = a.plan.cum[0];
   const float gamma = a.gamma;
-  // slopes of the constant-slope path: gpw[k] = gamma^(16 * 2^k) (a lane run of 2^k lanes),
-  // rPl = gamma^(16 * (31 - lane)) (the lanes right of this one), g512 = gamma^512 (a batch)
-  float gpw[5];
-  gpw[0] = a.gamma16;
-#pragma unroll
-  for (int k = 1; k < 5; ++k) gpw[k] = gpw[k - 1] * gpw[k - 1];
-  const float g512 = gpw[4] * gpw[4];
+  // slopes of the constant-slope path (kernel parameters: constant-bank operands):
+  // a.gpw[k] = gamma^(16 * 2^k) (a run of 2^k lanes), a.g4 (a 4-token chunk), a.g512 (a batch);
+  // rPl = gamma^(16 * (31 - lane)) (the lanes right of this one)
   float rPl = 1.f;
 #pragma unroll
   for (int k = 0; k < 5; ++k)
-    if (((31 - lane) >> k) & 1) rPl *= gpw[k];
+    if (((31 - lane) >> k) & 1) rPl *= a.gpw[k];
+  const int rot = (lane >> 1) & 3;  // ring read order: lanes 2j, 2j+1 of a quarter-warp start at chunk j
 
   uint8_t* ring = uring_mem + (size_t)wid * kUSlots * kSlotBytes;
   uint64_t* bar = uring_bar[wid];
@@ -1122,8 +836,8 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   // ---- producer state (lane 0 only) ----
   int p_nclaim = 0;        // units queued so far
   int p_iu = -1;           // queue index of the unit being issued
-  int64_t p_pb = 0, p_pbf = 1;  // next batch to issue (descending) and the unit's first batch
-  int64_t p_ua = 0, p_ub = 0, p_ntok = 0;
+  int p_pb = 0, p_pbf = 1; // next batch to issue (descending) and the unit's first batch
+  int p_ua = 0, p_ub = 0, p_ntok = 0;
   const float* p_rw = nullptr;
   const uint8_t* p_mk = nullptr;
   bool p_vec = false, p_done = false;
@@ -1138,14 +852,15 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
       const uint32_t u = atomicAdd(&a.ws->work_ctr, 1u);
       if (u >= total) { e.ri = -1; p_done = true; break; }
       int ri = 0;
-      while (u >= rt.wbeg[ri + 1]) ++ri;
-      const int64_t k = u - rt.wbeg[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
-      const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri];
-      const int64_t p0 = a.unit_first[u], p1 = k + 1 < nu ? a.unit_first[u + 1] : pend;
+      while (u >= (uint32_t)rt.wbeg[ri + 1]) ++ri;
+      const int64_t gs = rt.gs[ri];
+      const int64_t p0 = a.unit_first[u];
+      const int64_t p1 = u + 1 < (uint32_t)rt.wbeg[ri + 1] ? a.unit_first[u + 1] : gs + rt.cnt[ri];
       if (p0 == p1) continue;  // no sequence starts in this unit's range
-      const int64_t base = cum[gs];
-      e.p0 = p0; e.p1 = p1; e.base = base; e.ri = ri;
-      e.ua = cum[p0] - base; e.ub = cum[p1] - base;
+      const int64_t base = cum[gs], s0 = cum[p0], s1 = cum[p1];
+      e.p0 = (int)p0; e.p1 = (int)p1; e.ri = ri;
+      e.ua = (int)(s0 - base); e.ub = (int)(s1 - base);
+      e.base = s0;
       break;
     }
     ++p_nclaim;
@@ -1153,46 +868,56 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   // lane 0: issue batches (right to left through the queued units) until kUSlots - 1 are in
   // flight beyond the c_n consumed, at most kUQ - 1 units ahead of the consumer's unit kc
   auto produce = [&](int kc, uint32_t c_n) {
-   while (p_issued - c_n < (uint32_t)(kUSlots - 1)) {
-    while (p_pb < p_pbf) {  // the unit being issued is done: move to the next one
-      if (p_iu + 1 >= p_nclaim) {
-        if (p_done || p_nclaim - kc >= kUQ - 1) return;
-        claim();
-        if (p_done) return;
+    while (p_issued - c_n < (uint32_t)(kUSlots - 1)) {
+      while (p_pb < p_pbf) {  // the unit being issued is done: move to the next one
+        if (p_iu + 1 >= p_nclaim) {
+          if (p_done || p_nclaim - kc >= kUQ - 1) return;
+          claim();
+          if (p_done) return;
+        }
+        ++p_iu;
+        const UnitQ& e = q[p_iu & (kUQ - 1)];
+        if (e.ri < 0) { p_pb = 0; p_pbf = 1; return; }  // the end marker
+        const int r = rt.rank[e.ri];
+        p_ua = e.ua; p_ub = e.ub; p_ntok = (int)rt.ntok[e.ri];
+        p_rw = a.rewards[r]; p_mk = a.mask[r];
+        p_vec = aligned(p_rw, 16) && aligned(p_mk, 16);
+        p_pbf = p_ua / kBatch;
+        p_pb = p_ua < p_ub ? (p_ub - 1) / kBatch : p_pbf - 1;  // no batches for an empty unit
       }
-      ++p_iu;
-      const UnitQ& e = q[p_iu & (kUQ - 1)];
-      if (e.ri < 0) { p_pb = 0; p_pbf = 1; return; }  // the end marker
-      const int r = rt.rank[e.ri];
-      p_ua = e.ua; p_ub = e.ub; p_ntok = rt.ntok[e.ri];
-      p_rw = a.rewards[r]; p_mk = a.mask[r];
-      p_vec = aligned(p_rw, 16) && aligned(p_mk, 16);
-      p_pbf = p_ua / kBatch;
-      p_pb = p_ua < p_ub ? (p_ub - 1) / kBatch : p_pbf - 1;  // no batches for an empty unit
+      const int t0 = p_pb * kBatch;
+      const uint32_t b = smem_addr(&bar[p_slot]);
+      // the batch's tokens inside the unit (rewards from a 4-token, the mask from a 16-token
+      // granule); a whole batch inside the unit and the buffer is the common case
+      bool ok = p_vec;
+      int r0 = t0, m0 = t0;
+      uint32_t rb = kBatch * 4, mb = kBatch;
+      if (!(t0 >= p_ua && t0 + kBatch <= p_ub && t0 + kBatch <= p_ntok)) {
+        const int lo = max(t0, p_ua), hi = min(t0 + kBatch, p_ub);
+        const int m1 = (hi + 15) & ~15;
+        ok = ok && m1 <= p_ntok;
+        r0 = lo & ~3;
+        m0 = lo & ~15;
+        rb = (uint32_t)(((hi + 3) & ~3) - r0) * 4u;
+        mb = (uint32_t)(m1 - m0);
+      }
+      if (ok) {
+        const uint32_t dst = smem_addr(ring + p_slot * kSlotBytes);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(rb + mb) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst + (uint32_t)(r0 - t0) * 4u), "l"(p_rw + r0), "r"(rb), "r"(b) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(dst + kBatch * 4 + (uint32_t)(m0 - t0)), "l"(p_mk + m0), "r"(mb), "r"(b) : "memory");
+      } else {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+      }
+      p_slot = p_slot + 1 == kUSlots ? 0 : p_slot + 1;
+      --p_pb;
+      ++p_issued;
     }
-    const int64_t t0 = p_pb * kBatch;
-    const int64_t lo = max(t0, p_ua), hi = min(t0 + kBatch, p_ub);
-    const int64_t m1 = (hi + 15) & ~15LL;
-    const uint32_t b = smem_addr(&bar[p_slot]);
-    if (p_vec && m1 <= p_ntok) {
-      const int64_t r0 = lo & ~3LL, r1 = (hi + 3) & ~3LL, m0 = lo & ~15LL;
-      const uint32_t rb = (uint32_t)(r1 - r0) * 4u, mb = (uint32_t)(m1 - m0);
-      uint8_t* dst = ring + p_slot * kSlotBytes;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(rb + mb) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          ::"r"(smem_addr(dst + (r0 - t0) * 4)), "l"(p_rw + r0), "r"(rb), "r"(b) : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-          ::"r"(smem_addr(dst + kBatch * 4 + (m0 - t0))), "l"(p_mk + m0), "r"(mb), "r"(b) : "memory");
-    } else {
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
-    }
-    p_slot = p_slot + 1 == kUSlots ? 0 : p_slot + 1;
-    --p_pb;
-    ++p_issued;
-   }
   };
 
   if (lane == 0) {
@@ -1205,11 +930,11 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
   uint32_t c_slot = 0, c_phase = 0;  // bit s: parity of slot s's next completion
   uint32_t c_n = 0;                  // batches consumed
-  // sequence-start window of the current unit: lane j holds start p1 - j (relative to ua) for
-  // p1 - j > p0, else kNoStart; wq = the sorted position of lane 0's entry
-  auto load_window = [&](const UnitQ& u, int64_t top) -> int {
-    const int64_t p = top - lane;
-    return p > u.p0 ? (int)(cum[p] - u.base - u.ua) : kNoStart;
+  // sequence-start window of a unit: lane j holds the start of sequence top - j relative to the
+  // unit (for top - j > p0), else kNoStart
+  auto load_window = [&](const UnitQ& u, int top) -> int {
+    const int p = top - lane;
+    return p > u.p0 ? (int)(cum[p] - u.base) : kNoStart;
   };
   UnitQ cu = q[0];
   int ws = cu.ri >= 0 ? load_window(cu, cu.p1) : kNoStart;
@@ -1218,23 +943,21 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   for (int kc = 0; cu.ri >= 0; ++kc) {
     const int ri = cu.ri;
     const int r = rt.rank[ri];
-    float* G = a.returns[r];
+    const int ua = cu.ua, ulen = cu.ub - cu.ua, ntok = (int)rt.ntok[ri];
+    float* G = a.returns[r] + ua;            // the unit's tokens
     const float* rw = a.rewards[r];
     const uint8_t* mk = a.mask[r];
-    const int64_t ntok = rt.ntok[ri];
     const bool vec = aligned(rw, 16) && aligned(mk, 16);
-    const bool vstore = aligned(G, 16);
+    const bool vstore = aligned(a.returns[r], 16);  // G + lt = returns + t0 + 16 lane
     const bool count_stats = rt.t[ri] == 0;
-    const int64_t ua = cu.ua, ub = cu.ub;
-    const int ulen = (int)(ub - ua);
-    int64_t wtop = cu.p1;      // sorted position of lane 0's window entry
+    int wtop = cu.p1;          // sorted position of lane 0's window entry
     float carry = 0.f;         // G right of the current batch (the unit's last token ends a sequence)
-    const int64_t bf = ua / kBatch;
-    const int64_t bl = ua < ub ? (ub - 1) / kBatch : bf - 1;
+    const int bf = ua / kBatch;
+    const int bl = ulen > 0 ? (cu.ub - 1) / kBatch : bf - 1;
 #pragma unroll 1
-    for (int64_t bb = bl; bb >= bf; --bb) {
-      const int64_t t0 = bb * kBatch;
-      const int tb = (int)(t0 - ua);  // the batch's first token, relative to the unit
+    for (int bb = bl; bb >= bf; --bb) {
+      const int t0 = bb * kBatch;
+      const int tb = t0 - ua;  // the batch's first token, relative to the unit
       // sequence ends in the batch: starts s with tb < s <= tb + kBatch end a sequence at s - 1
       uint32_t e = 0;
       for (;;) {
@@ -1263,24 +986,22 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
         } while (!done);
         c_phase ^= 1u << c_slot;
       }
-      const int64_t lo = max(t0, ua), hi = min(t0 + kBatch, ub);
-      const bool tma = vec && (((hi + 15) & ~15LL) <= ntok);
+      const int lo = max(t0, ua), hi = min(t0 + kBatch, cu.ub);
+      const bool tma = vec && ((hi + 15) & ~15) <= ntok;
       const int lt = tb + kTokLane * lane;  // this lane's first token, relative to the unit
+      // cur.r[k] = physical chunk k of the lane's 16 tokens = logical chunk (k + prot) & 3
+      // (tokens 4c .. 4c+3): the ring is read in a rotated chunk order (conflict-free), and the
+      // constant-slope path works in that order (chunk maps, no per-token de-rotation)
       Batch cur;
+      int prot = 0;
       if (tma) {
         const uint8_t* rb = ring + c_slot * kSlotBytes + 64 * lane;
-        const int rot = (lane >> 1) & 3;
-        float4 v[4];
+        prot = rot;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
-        float4 u[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cur.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
+        for (int k = 0; k < 4; ++k) cur.r[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
         cur.m = *reinterpret_cast<const uint4*>(ring + c_slot * kSlotBytes + kBatch * 4 + 16 * lane);
       } else {
-        load_batch_in(cur, rw, mk, t0 + kTokLane * lane, lo, hi, vec);
+        load_batch_in(cur, rw, mk, (int64_t)t0 + kTokLane * lane, lo, hi, vec);
       }
       c_slot = c_slot + 1 == kUSlots ? 0 : c_slot + 1;
       ++c_n;
@@ -1300,35 +1021,65 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
       const uint32_t mk16 = nonzero_bytes4(cur.m.x) | nonzero_bytes4(cur.m.y) << 4 |
                             nonzero_bytes4(cur.m.z) << 8 | nonzero_bytes4(cur.m.w) << 12;
       const bool whole = tb >= 0 && tb + kBatch <= ulen;
-      float out[kTokLane];
-      uint32_t on16, st16 = 0xffffu;  // tokens counted / stored
+      float out[kTokLane];  // physical order when fast, else logical
+      uint32_t on16, st16 = 0xffffu;  // tokens counted / stored (same order as out)
+      bool phys;
       if (__all_sync(kFull, e == 0u) && whole) {
-        // constant slopes: no sequence end, every token inside the unit
-        on16 = mk16;
+        // constant slopes: no sequence end, every token inside the unit.  Chunk k's map is
+        // x -> S_k + gamma^4 x; the lane map composes the chunks in logical order.
+        phys = true;
+        on16 = ((mk16 | mk16 << 16) >> (4 * prot)) & 0xffffu;  // physical mask nibbles
         float v[kTokLane];
 #pragma unroll
         for (int i = 0; i < kTokLane; ++i) v[i] = (on16 >> i) & 1u ? tok_r(cur, i) : 0.f;
-        float S = 0.f;
+        float Sk[4];
 #pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(gamma, S, v[i]);
+        for (int k = 0; k < 4; ++k)
+          Sk[k] = fmaf(gamma, fmaf(gamma, fmaf(gamma, v[4 * k + 3], v[4 * k + 2]), v[4 * k + 1]), v[4 * k]);
+        float u[4], L[4];  // L[c] = Sk[(c - prot) & 3]
+#pragma unroll
+        for (int c = 0; c < 4; ++c) u[c] = (prot & 1) ? Sk[(c + 3) & 3] : Sk[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) L[c] = (prot & 2) ? u[(c + 2) & 3] : u[c];
+        const float S = fmaf(a.g4, fmaf(a.g4, fmaf(a.g4, L[3], L[2]), L[1]), L[0]);
         float sS = S;
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const float o = __shfl_down_sync(kFull, sS, 1 << k);
-          if (lane + (1 << k) < 32) sS = fmaf(gpw[k], o, sS);
+          if (lane + (1 << k) < 32) sS = fmaf(a.gpw[k], o, sS);
         }
         float rS = __shfl_down_sync(kFull, sS, 1);
         if (lane == 31) rS = 0.f;
         const float tS = __shfl_sync(kFull, sS, 0);
-        float g_next = fmaf(rPl, carry, rS);
+        float C[4];  // G right of logical chunk c
+        C[3] = fmaf(rPl, carry, rS);
+        C[2] = fmaf(a.g4, C[3], L[3]);
+        C[1] = fmaf(a.g4, C[2], L[2]);
+        C[0] = fmaf(a.g4, C[1], L[1]);
+        float D[4];  // D[k] = C[(k + prot) & 3]
 #pragma unroll
-        for (int i = kTokLane - 1; i >= 0; --i) {
-          out[i] = fmaf(gamma, g_next, v[i]);
-          g_next = out[i];
+        for (int k = 0; k < 4; ++k) u[k] = (prot & 1) ? C[(k + 1) & 3] : C[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) D[k] = (prot & 2) ? u[(k + 2) & 3] : u[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          out[4 * k + 3] = fmaf(gamma, D[k], v[4 * k + 3]);
+          out[4 * k + 2] = fmaf(gamma, out[4 * k + 3], v[4 * k + 2]);
+          out[4 * k + 1] = fmaf(gamma, out[4 * k + 2], v[4 * k + 1]);
+          out[4 * k] = fmaf(gamma, out[4 * k + 1], v[4 * k]);
         }
-        carry = fmaf(g512, carry, tS);
+        carry = fmaf(a.g512, carry, tS);
       } else {
-        // general: sequence ends (slope 0 at a sequence's last token) and the unit's bounds
+        // general: sequence ends (slope 0 at a sequence's last token) and the unit's bounds,
+        // token by token in logical order
+        phys = false;
+        {
+          float4 u4[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) u4[c] = (prot & 1) ? cur.r[(c + 3) & 3] : cur.r[c];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) cur.r[c] = (prot & 2) ? u4[(c + 2) & 3] : u4[c];
+        }
         uint32_t in16 = 0xffffu;
         if (lt < 0) in16 &= lt + kTokLane <= 0 ? 0u : (0xffffu << (uint32_t)(-lt)) & 0xffffu;
         if (lt + kTokLane > ulen) in16 &= lt >= ulen ? 0u : 0xffffu >> (uint32_t)(lt + kTokLane - ulen);
@@ -1340,7 +1091,7 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
 #pragma unroll
         for (int i = kTokLane - 1; i >= 0; --i) S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, v[i]);
         float rS, rP, bS, bP;
-        warp_compose(S, e ? 0.f : gpw[0], lane, rS, rP, bS, bP);
+        warp_compose(S, e ? 0.f : a.gpw[0], lane, rS, rP, bS, bP);
         float g_next = rS + rP * carry;
 #pragma unroll
         for (int i = kTokLane - 1; i >= 0; --i) {
@@ -1351,27 +1102,31 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
         st16 = in16;
       }
       if (count_stats) {
-        float sg = 0.f, sg2 = 0.f;
+        float sa = 0.f, sb = 0.f, qa = 0.f, qb = 0.f;
 #pragma unroll
-        for (int i = 0; i < kTokLane; ++i) {
-          const float o = (on16 >> i) & 1u ? out[i] : 0.f;
-          sg += o;
-          sg2 = fmaf(o, o, sg2);
+        for (int i = 0; i < kTokLane; i += 2) {
+          const float o0 = (on16 >> i) & 1u ? out[i] : 0.f;
+          const float o1 = (on16 >> (i + 1)) & 1u ? out[i + 1] : 0.f;
+          sa += o0;
+          qa = fmaf(o0, o0, qa);
+          sb += o1;
+          qb = fmaf(o1, o1, qb);
         }
         s_m += (double)__popc(on16);
-        s_g += (double)sg;
-        s_g2 += (double)sg2;
+        s_g += (double)(sa + sb);
+        s_g2 += (double)(qa + qb);
       }
+      const int srot = phys ? prot : 0;  // out chunk k holds logical chunk (k + srot) & 3
       if (vstore && st16 == 0xffffu) {
-        float4* gp = reinterpret_cast<float4*>(G + ua + lt);
+        float4* gp = reinterpret_cast<float4*>(G + lt);
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4)
-          __stcs(gp + q4, make_float4(out[4 * q4], out[4 * q4 + 1], out[4 * q4 + 2], out[4 * q4 + 3]));
+        for (int k = 0; k < 4; ++k)
+          __stcs(gp + ((k + srot) & 3), make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]));
       } else {
-        float* gp = G + ua + lt;
+        float* gp = G + lt;
 #pragma unroll
         for (int i = 0; i < kTokLane; ++i)
-          if ((st16 >> i) & 1u) gp[i] = out[i];
+          if ((st16 >> i) & 1u) gp[4 * (((i >> 2) + srot) & 3) + (i & 3)] = out[i];
       }
     }
     // per-sequence returns G_0 of the unit's sequences [p0, p1)
@@ -1381,13 +1136,13 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
       const int64_t gs = rt.gs[ri];
       if (wtop == cu.p1 && cu.p1 - cu.p0 <= 32) {
         // the window still holds every start: lane j takes sequence p1 - 1 - j
-        const int64_t p = cu.p1 - 1 - lane;
+        const int p = cu.p1 - 1 - lane;
         const int s_next = ws;                                  // start of p + 1
         int s = __shfl_down_sync(kFull, ws, 1);                 // start of p
         if (p == cu.p0) s = 0;
-        if (p >= cu.p0) SR[p - gs] = s_next > s ? G[ua + s] : 0.f;
+        if (p >= cu.p0) SR[p - gs] = s_next > s ? G[s] : 0.f;
       } else {
-        unit_seq_returns(SR, G, cum, cu.base, gs, cu.p0, cu.p1, lane);
+        unit_seq_returns(SR, G - ua, cum, cum[gs], gs, cu.p0, cu.p1, lane);
       }
     }
     // the next unit
@@ -1489,15 +1244,7 @@ cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s)
   static bool opted[64] = {};
   e = opt_in_dynamic_smem(returns_units_kernel, (int)kRingBytes, opted);
   if (e != cudaSuccess) return e;
-  static const bool v1 = getenv("EARL_UNITS_V1") != nullptr;
-  if (v1) {
-    static bool opted1[64] = {};
-    e = opt_in_dynamic_smem(returns_units_v1_kernel, (int)kRingBytes, opted1);
-    if (e != cudaSuccess) return e;
-    returns_units_v1_kernel<<<sm_count * kUCtasPerSm, kWarps * 32, kRingBytes, s>>>(a);
-  } else {
-    returns_units_kernel<<<sm_count * kU2Ctas, kWarps * 32, kRingBytes, s>>>(a);
-  }
+  returns_units_kernel<<<sm_count * kU2Ctas, kWarps * 32, kRingBytes, s>>>(a);
   return cudaGetLastError();
 }
 

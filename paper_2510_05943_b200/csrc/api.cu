@@ -1840,6 +1840,10 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   a.gamma = gamma;
   a.gamma16 = 1.f;
   for (int i = 0; i < 16; ++i) a.gamma16 *= gamma;
+  a.gpw[0] = a.gamma16;
+  for (int k = 1; k < 5; ++k) a.gpw[k] = a.gpw[k - 1] * a.gpw[k - 1];
+  a.g4 = (gamma * gamma) * (gamma * gamma);
+  a.g512 = a.gpw[4] * a.gpw[4];
   a.partial = partial;
   if ((st = set_per_rank<const float>(p, a.rewards, rewards, "rewards", true)) != EARL_OK) return st;
   if ((st = set_per_rank<const uint8_t>(p, a.mask, mask, "mask", true)) != EARL_OK) return st;
@@ -1863,14 +1867,16 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   int which = 3;
   if (p->synced) {
     const earl_layout_t& S = p->lay[0];
-    int64_t units = 0;
+    int64_t units = 0, big = 0;
     for (int r = 0; r < p->comm->world; ++r) {
       if (!p->comm->emulated && r != p->comm->rank) continue;
       const int q = r - S.rank0;
       if (q < 0 || q >= S.dp * S.tp) continue;
-      units += (p->host_hdr.shard_tokens[0][q / S.tp] + kUnitTok - 1) / kUnitTok;
+      const int64_t n = p->host_hdr.shard_tokens[0][q / S.tp];
+      units += (n + kUnitTok - 1) / kUnitTok;
+      big = std::max(big, n);
     }
-    which = prefer_units(p->host_hdr.max_len, units, a.resident_warps) ? 1 : 2;
+    which = prefer_units(p->host_hdr.max_len, units, a.resident_warps, big) ? 1 : 2;
   }
   if (force && std::strcmp(force, "units") == 0) which = 1;
   if (force && std::strcmp(force, "windows") == 0) which = 2;

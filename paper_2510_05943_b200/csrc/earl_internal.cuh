@@ -208,15 +208,22 @@ struct AggWork {
   uint32_t epoch;     // launches so far: flags of older launches never match
   uint32_t pad;
 };
-constexpr int kUnitTok = 4096;  // returns unit kernel: a unit = the sequences starting in [k*4096, (k+1)*4096)
+#ifndef EARL_UNIT_TOK
+#define EARL_UNIT_TOK 8192
+#endif
+constexpr int kUnitTok = EARL_UNIT_TOK;  // returns unit kernel: a unit = the sequences starting in [k*kUnitTok, (k+1)*kUnitTok)
 constexpr int64_t kUnitMaxLen = int64_t(1) << 17;  // ... used when no sequence is longer than this
 // The unit kernel pays off when the batch has no very long sequence (one warp streams a unit)
 // and enough units to keep every warp busy: at least kUnitsPerWarp units per resident warp
-// (measured: C5-lt, 83K units, 0.60 ms against 0.71 windowed; C2, 322 units, 54 against 24 us).
+// (measured with 4096-token units: C5-lt, 83K units, 0.60 ms against 0.71 windowed; C2, 322
+// units, 54 against 24 us).
 constexpr int64_t kUnitsPerWarp = 4;
-constexpr int kUnitWarpsPerSm = 24;  // returns_units_kernel: 3 CTAs x 8 warps
-__host__ __device__ inline bool prefer_units(int64_t max_len, int64_t units, int64_t warps) {
-  return max_len <= kUnitMaxLen && units >= kUnitsPerWarp * warps;
+constexpr int kUnitWarpsPerSm = 16;  // returns_units_kernel: 2 CTAs x 8 warps
+// The unit kernel keeps positions inside a rank buffer in int32: ranks of at most kU2MaxTok tokens.
+constexpr int64_t kU2MaxTok = (int64_t(1) << 31) - 4 * kUnitTok;
+__host__ __device__ inline bool prefer_units(int64_t max_len, int64_t units, int64_t warps,
+                                             int64_t max_rank_tokens) {
+  return max_len <= kUnitMaxLen && units >= kUnitsPerWarp * warps && max_rank_tokens <= kU2MaxTok;
 }
 
 struct AggArgs {
@@ -232,6 +239,8 @@ struct AggArgs {
   int32_t view_rank;       // -1: every source rank (emulated comm); else this rank
   float gamma, eps;
   float gamma16;            // gamma^16 (product of 16 fp32 factors, as a lane of 16 tokens)
+  float gpw[5];             // gamma^(16 * 2^k), k = 0..4 (gpw[0] = gamma16, then squares)
+  float g4, g512;           // gamma^4 (a 4-token chunk), gamma^512 (a 512-token batch)
   const float* rewards[kMaxWorld];   // per source comm rank: token rewards (fp32)
   const uint8_t* mask[kMaxWorld];    // token mask (u8, 1 = counted)
   float* returns[kMaxWorld];         // token returns G (fp32)

@@ -787,6 +787,57 @@ def test_returns_repeat_and_graph(graph, kernel, monkeypatch):
     _adv_case(lens, W.layout(dp=4, tp=2, assign="lpt"), 0.99, 8, repeats=5, graph=graph)
 
 
+def test_returns_source_rank_above_int32_tokens(monkeypatch):
+    """Maximum size (reading n5): one source rank holding 2^31 + 2^20 tokens (2049 sequences of
+    2^20 on DP1; the destination DP4 shards stay under INT32_MAX).  The unit kernel keeps rank
+    positions in int32, so the automatic choice takes the windowed kernel (int64 positions): the
+    returns of the sequences around token 2^31 equal the oracle's per-sequence recurrence, and the
+    masked-token count is exact.  Forcing the unit kernel latches EARL_ERR_CAPACITY."""
+    import torch
+    from paper_2510_05943_b200.dispatch import EmulatedDispatch
+    from paper_2510_05943_b200.earl import EarlError
+    L, n = 2**20, 2049
+    T = L * n
+    free = torch.cuda.mem_get_info()[0]
+    if free < 24 * 2**30:
+        pytest.skip("needs ~20 GB of device memory")
+    ed = EmulatedDispatch(4)
+    plan = ed.plan(W.layout(dp=1), W.layout(dp=4, assign="contig"), [L] * n, W.field_set("tiny3"))
+    plan.sync()
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    r = torch.randn(T, device="cuda", generator=gen)
+    m = (torch.rand(T, device="cuda", generator=gen) < 0.8).to(torch.uint8)
+    G = torch.empty(T, device="cuda")
+    dummy_f = torch.zeros(4, device="cuda")
+    dummy_m = torch.zeros(4, dtype=torch.uint8, device="cuda")
+    part = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gamma = 0.99
+    plan.returns(gamma, [r, dummy_f, dummy_f, dummy_f], [m, dummy_m, dummy_m, dummy_m],
+                 [G, dummy_f.clone(), dummy_f.clone(), dummy_f.clone()], part)
+    torch.cuda.synchronize()
+    plan.sync()
+    assert part[0].item() == float(m.sum(dtype=torch.int64).item())
+    atol = 4 * 2.0 ** -24 * (1.0 / (1.0 - gamma)) * 8.0 + 1e-6
+    for p in (0, 2047, 2048):  # 2048 starts at token 2^31
+        lo = p * L
+        rr = r[lo:lo + L].cpu().numpy()
+        mm = m[lo:lo + L].cpu().numpy()
+        want = O.discounted_returns(rr, mm, gamma)
+        gmax = max(1.0, float(np.abs(want).max()))
+        got = G[lo:lo + L].cpu().numpy()
+        assert np.allclose(got, want, rtol=0, atol=atol * gmax), p
+    monkeypatch.setenv("EARL_RETURNS", "units")
+    plan.returns(gamma, [r, dummy_f, dummy_f, dummy_f], [m, dummy_m, dummy_m, dummy_m],
+                 [G, dummy_f.clone(), dummy_f.clone(), dummy_f.clone()], part)
+    torch.cuda.synchronize()
+    with pytest.raises(EarlError) as e:
+        plan.sync()
+    assert e.value.name == "EARL_ERR_CAPACITY"
+    plan.destroy()
+    del r, m, G
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("seed", range(40))
 def test_sp1_fast_planner_equals_general_planner(seed, monkeypatch):
     """The SP = 1 single-pass planner (planner_sp1_kernel) and the general phased planner give
