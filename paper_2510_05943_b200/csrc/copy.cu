@@ -306,6 +306,7 @@ __device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
 // indexed, local memory) is consulted only when a warp changes block, and the kernel parameter
 // is passed by reference into every (inlined) method so its fields are constant-bank loads.
 struct Walker {
+  int vn;  // the view's block count (a register copy; the View itself lives in local memory)
   int b;  // current view block and its fields
   int64_t b_rbeg, b_rend, b_tbeg;
   uint64_t b_cbase;
@@ -328,7 +329,7 @@ struct Walker {
 
   __device__ __forceinline__ void set_block(const View& v, int bb) {
     b = bb;
-    if (bb < v.n) {
+    if (bb < vn) {
       b_rbeg = v.rbeg[bb]; b_rend = v.rend[bb]; b_tbeg = v.tbeg[bb]; b_cbase = v.cbase[bb];
       b_msg = v.msg[bb];
     } else {
@@ -338,6 +339,7 @@ struct Walker {
 
   __device__ __forceinline__ void setup(const CopyArgs& a, const View& v, uint64_t c0_,
                                         uint64_t first_dyn_) {
+    vn = v.n;
     c0 = c0_; unit = 0; n_units = 0; first_dyn = first_dyn_; total = v.cbase[v.n];
     prem = 0; R = 0; xpos = x1 = 0; f = 0;
     set_block(v, 0);
@@ -388,7 +390,7 @@ struct Walker {
     prem = 0;
     if (xpos >= x1) return;
     int bb = 0;
-    while (bb + 1 < v.n && v.cbase[bb + 1] <= xpos) ++bb;
+    while (bb + 1 < vn && v.cbase[bb + 1] <= xpos) ++bb;
     set_block(v, bb);
     int64_t lo = b_rbeg, hi = b_rend - 1;  // last record whose cost starts <= xpos
     while (lo < hi) {
@@ -470,7 +472,7 @@ struct Walker {
           next_field(a);
         } else if (j + 1 < b_rend) {
           load_record(a, j + 1);
-        } else if (b + 1 < v.n) {
+        } else if (b + 1 < vn) {
           set_block(v, b + 1);
           load_record(a, b_rbeg);
         } else {
