@@ -23,6 +23,8 @@
 // sequence end), pass 2 re-reads the window from L2 and writes G with float4 stores.  HBM sees
 // every token read and written once; long sequences are spread over many warps (decoupled
 // look-back).
+#include <cooperative_groups.h>
+
 #include "earl_internal.cuh"
 
 namespace earl {
@@ -50,26 +52,36 @@ __device__ __forceinline__ void latch(PlanHeader* h, int code, int detail) {
   if (atomicCAS(&h->err, 0, code) == 0) h->err_detail = detail;
 }
 
-// gate (AggArgs::gate) on the batch, read on the device: lets the host launch both returns
-// kernels when it does not know the batch (one of them exits at once).  Whole-CTA decision.
+// gate (AggArgs::gate) on the batch, read on the device: lets the host launch every returns
+// kernel when it does not know the batch (all but the chosen one exit at once).  gate = id + 1
+// runs kernel id (ReturnsKernel) only if choose_returns picks it.  Whole-CTA decision.
+// Warp-collective (warp 0): lane r reads source rank r's token count, so the header costs one
+// round trip (a loop in one thread had serialised them: ~1 us per rank at every launch).
+__device__ int device_choice(const AggArgs& a, int* coop_nb) {
+  const PlanHeader* h = a.hdr;
+  const LayoutDesc& S = a.plan.lay[0];
+  const int lane = threadIdx.x & 31;
+  const int q = lane - S.rank0;
+  const bool in = lane < a.world && (a.view_rank < 0 || lane == a.view_rank) && q >= 0 &&
+                  q < S.dp * S.tp;
+  const int64_t mine = in ? *reinterpret_cast<const volatile int64_t*>(&h->shard_tokens[0][q / S.tp]) : 0;
+  const int64_t m = *reinterpret_cast<const volatile int64_t*>(&h->max_len);
+  const unsigned mask = __ballot_sync(kFull, in);
+  int64_t nt[kMaxWorld];
+  int n = 0;
+  for (int r = 0; r < kMaxWorld; ++r) {
+    const int64_t v = __shfl_sync(kFull, mine, r);
+    if (mask >> r & 1u) nt[n++] = v;
+  }
+  return choose_returns(nt, n, m, a.resident_warps, a.coop_warps, coop_nb);
+}
+
 __device__ bool gated_out(const AggArgs& a) {
   if (a.gate == 0) return false;
   __shared__ int s_out;
-  if (threadIdx.x == 0) {
-    const PlanHeader* h = a.hdr;
-    const LayoutDesc& S = a.plan.lay[0];
-    int64_t units = 0, big = 0;
-    for (int r = 0; r < a.world; ++r) {
-      if (a.view_rank >= 0 && r != a.view_rank) continue;
-      const int q = r - S.rank0;
-      if (q < 0 || q >= S.dp * S.tp) continue;
-      const int64_t n = *reinterpret_cast<const volatile int64_t*>(&h->shard_tokens[0][q / S.tp]);
-      units += (n + kUnitTok - 1) / kUnitTok;
-      big = max(big, n);
-    }
-    const int64_t m = *reinterpret_cast<const volatile int64_t*>(&h->max_len);
-    const bool units_best = prefer_units(m, units, a.resident_warps, big);
-    s_out = a.gate == 1 ? !units_best : units_best;
+  if (threadIdx.x < 32) {
+    const int c = device_choice(a, nullptr);
+    if (threadIdx.x == 0) s_out = c != a.gate - 1;
   }
   __syncthreads();
   return s_out != 0;
@@ -124,29 +136,49 @@ struct RankTable {
 
 // The window size adapts to the batch: 4096 tokens once there are two windows per warp of
 // the grid, down to one 512-token batch for small batches (every warp busy, short chains).
+// Warp-collective (warp 0): lane r reads source rank r's header fields, one round trip.
 __device__ void rank_table(const AggArgs& a, RankTable& rt, int64_t warps, int nb_fixed = 0) {
   const PlanHeader* h = a.hdr;
   const LayoutDesc& S = a.plan.lay[0];
-  rt.n = 0;
-  int64_t batches = 0;
-  for (int r = 0; r < a.world; ++r) {
-    if (a.view_rank >= 0 && r != a.view_rank) continue;
-    const int q = r - S.rank0;
-    if (q < 0 || q >= S.dp * S.tp) continue;
+  const int lane = threadIdx.x & 31;
+  const int q = lane - S.rank0;
+  const bool in = lane < a.world && (a.view_rank < 0 || lane == a.view_rank) && q >= 0 &&
+                  q < S.dp * S.tp;
+  const unsigned mask = __ballot_sync(kFull, in);
+  const int idx = __popc(mask & ((1u << lane) - 1u));
+  int64_t nt = 0;
+  if (in) {
     const int g = q / S.tp;
-    const int n = rt.n;
-    rt.rank[n] = r;
-    rt.t[n] = q % S.tp;
-    rt.gs[n] = h->group_start[0][g];
-    rt.cnt[n] = h->group_count[0][g];
-    rt.ntok[n] = h->shard_tokens[0][g];
-    batches += (rt.ntok[n] + kBatch - 1) / kBatch;
-    rt.n = n + 1;
+    rt.rank[idx] = lane;
+    rt.t[idx] = q % S.tp;
+    rt.gs[idx] = h->group_start[0][g];
+    rt.cnt[idx] = h->group_count[0][g];
+    nt = h->shard_tokens[0][g];
+    rt.ntok[idx] = nt;
   }
-  rt.nb = nb_fixed > 0 ? nb_fixed : (int)max((int64_t)1, min((int64_t)kMaxNB, batches / (2 * warps)));
-  const int64_t win = (int64_t)kBatch * rt.nb;
-  rt.wbeg[0] = 0;
-  for (int n = 0; n < rt.n; ++n) rt.wbeg[n + 1] = rt.wbeg[n] + (rt.ntok[n] + win - 1) / win;
+  int64_t batches = (nt + kBatch - 1) / kBatch;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) batches += __shfl_xor_sync(kFull, batches, o);
+  const int n = __popc(mask);
+  const int nb = nb_fixed > 0 ? nb_fixed : (int)max((int64_t)1, min((int64_t)kMaxNB, batches / (2 * warps)));
+  const int64_t win = (int64_t)kBatch * nb;
+  // window prefix in rank order (idx grows with the lane among the ranks taking part)
+  const int64_t cnt = in ? (nt + win - 1) / win : 0;
+  int64_t inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (in) rt.wbeg[idx] = inc - cnt;
+  const int64_t all = __shfl_sync(kFull, inc, 31);
+  if (lane == 0) {
+    rt.n = n;
+    rt.nb = nb;
+    rt.wbeg[n] = all;
+    if (n == 0) rt.wbeg[0] = 0;
+  }
+  __syncwarp();
 }
 
 // Smallest p in [lo, hi] with cum[p] - base >= key (cum[hi] - base >= key holds): 32-ary
@@ -478,8 +510,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) returns_kernel(const 
   extern __shared__ __align__(128) uint8_t ring_mem[];  // [kWarps][kSlots][kSlotBytes]
   __shared__ uint64_t ring_bar[kWarps][kSlots];
 #endif
+  if (threadIdx.x < 32) rank_table(a, rt, (int64_t)gridDim.x * kWarps);
   if (threadIdx.x == 0) {
-    rank_table(a, rt, (int64_t)gridDim.x * kWarps);
     s_tag = (*(volatile uint32_t*)&a.ws->epoch + 1u) << 2;  // | 1 aggregate, | 2 inclusive
     s_ok = rt.wbeg[rt.n] <= a.win_cap;
     if (!s_ok && blockIdx.x == 0)
@@ -719,7 +751,7 @@ __device__ __forceinline__ uint32_t nonzero_bytes4(uint32_t w) {
 __global__ void unit_table_kernel(const __grid_constant__ AggArgs a) {
   if (gated_out(a)) return;
   __shared__ RankTable rt;
-  if (threadIdx.x == 0) rank_table(a, rt, 1, kUnitTok / kBatch);
+  if (threadIdx.x < 32) rank_table(a, rt, 1, kUnitTok / kBatch);
   __syncthreads();
   if (rt.wbeg[rt.n] > a.win_cap) return;  // the unit kernel latches CAPACITY
   const int64_t* cum = a.plan.cum[0];
@@ -799,8 +831,8 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   __shared__ UnitQ s_q[kWarps][kUQ];
   __shared__ int s_ok;
   if (gated_out(a)) return;
+  if (threadIdx.x < 32) rank_table(a, rt, 1, kUnitTok / kBatch);
   if (threadIdx.x == 0) {
-    rank_table(a, rt, 1, kUnitTok / kBatch);
     bool ok = rt.wbeg[rt.n] <= a.win_cap;
     int64_t big = 0;
     for (int ri = 0; ri < rt.n; ++ri) big = max(big, rt.ntok[ri]);
@@ -1160,6 +1192,227 @@ __global__ void __launch_bounds__(kWarps * 32, kU2Ctas) returns_units_kernel(con
   returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
 }
 
+// ---------------------------------------------------------------------------------------
+// returns_coop_kernel: small and mid batches (C2, C4), where the look-back chains of the
+// windowed kernel are latency-bound.  A co-resident grid gives every window of 512 * nb tokens
+// (nb = 1, 2 or 4: the smallest that fits) its own warp.  The warp loads its window into shared
+// memory once (TMA bulk copies; the buffer's last few tokens by lanes), composes the window's map
+// (pass 1) and publishes it; after one grid barrier every window's map is final, so the carry into
+// a window is the composition of the maps to its right up to the first zero slope (a sequence end
+// or the rank's end), read 32 windows per round trip with no waiting; pass 2 turns the lane maps
+// into the returns from the same shared-memory copy.  Each token is read from HBM once and written
+// once.  Chosen by choose_returns when the windows fit the grid.
+// ---------------------------------------------------------------------------------------
+
+constexpr int kCWinMax = kBatch * kCoopMaxNB;       // 2048 tokens
+constexpr int kCBytes = kCWinMax * 4 + kCWinMax;    // a window's rewards, then its mask bytes
+#ifndef EARL_AGG_CCTAS
+#define EARL_AGG_CCTAS 2
+#endif
+constexpr int kCCtas = EARL_AGG_CCTAS;
+
+__global__ void __launch_bounds__(kWarps * 32, kCCtas) returns_coop_kernel(const __grid_constant__ AggArgs a) {
+  __shared__ RankTable rt;
+  __shared__ uint32_t ends_bm[kWarps][kCWinMax / 32];
+  __shared__ float2 lmap[kWarps][kCoopMaxNB][32];  // per batch and lane: exclusive suffix map
+  __shared__ float2 bmap[kWarps][kCoopMaxNB];      // per batch: its map
+  __shared__ double red[3][32];
+  __shared__ uint64_t cbar[kWarps];
+  __shared__ int s_ok;
+  extern __shared__ __align__(128) uint8_t cmem[];  // [kWarps][kCBytes]
+  if (gated_out(a)) return;
+  if (threadIdx.x < 32) {
+    int nb = a.coop_nb;
+    if (nb <= 0) device_choice(a, &nb);
+    rank_table(a, rt, 1, nb > 0 ? nb : kCoopMaxNB);
+    const int64_t total = rt.wbeg[rt.n];
+    const bool ok = nb > 0 && total <= (int64_t)gridDim.x * kWarps && total <= a.win_cap;
+    if (threadIdx.x == 0) s_ok = ok;
+    if (!ok && threadIdx.x == 0 && blockIdx.x == 0)
+      latch(a.plan.hdr, EARL_ERR_CAPACITY, (int)min(total, (int64_t)INT32_MAX));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t total = s_ok ? rt.wbeg[rt.n] : 0;
+  const int64_t win = (int64_t)kBatch * rt.nb;
+  const float gamma = a.gamma;
+  const float g16 = a.gamma16;
+  float2* agg = reinterpret_cast<float2*>(a.win);  // the window maps (no tags: a barrier orders them)
+  uint32_t* bm = ends_bm[wid];
+  uint8_t* buf = cmem + (size_t)wid * kCBytes;
+  const uint32_t bar = smem_addr(&cbar[wid]);
+  double s_m = 0.0, s_g = 0.0, s_g2 = 0.0;
+
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + wid;  // this warp's window
+  const bool has = gw < total;
+  int ri = 0;
+  if (has) while (gw >= rt.wbeg[ri + 1]) ++ri;
+  const int r = has ? rt.rank[ri] : 0;
+  const int64_t ntok = has ? rt.ntok[ri] : 0;
+  const int64_t w0 = has ? (gw - rt.wbeg[ri]) * win : 0;
+  const int64_t w1 = has ? min(ntok, w0 + win) : 0;
+  const int n = (int)(w1 - w0);                     // tokens of the window
+  const int nb = (n + kBatch - 1) / kBatch;
+  const float* rw = has ? a.rewards[r] : nullptr;
+  const uint8_t* mk = has ? a.mask[r] : nullptr;
+  float* G = has ? a.returns[r] : nullptr;
+  const int64_t* cum = a.plan.cum[0];
+  const int64_t gs = has ? rt.gs[ri] : 0, pend = has ? gs + rt.cnt[ri] : 0;
+  const int64_t base = has ? cum[gs] : 0;
+
+  // ---- the window into shared memory: rewards [0, 4n) B, mask [4 * kCWinMax, + n) B -------
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const bool vec = has && aligned(rw, 16) && aligned(mk, 16);
+  const int nr = vec ? (n & ~3) : 0, nm = vec ? (n & ~15) : 0;  // by TMA (whole 16-B granules)
+  if (lane == 0) {
+    if (nr + nm > 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((uint32_t)(nr * 4 + nm)) : "memory");
+      if (nr > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(buf)), "l"(rw + w0), "r"((uint32_t)(nr * 4)), "r"(bar) : "memory");
+      if (nm > 0)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+            ::"r"(smem_addr(buf + kCWinMax * 4)), "l"(mk + w0), "r"((uint32_t)nm), "r"(bar) : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+  }
+  float* sr = reinterpret_cast<float*>(buf);
+  uint8_t* sm = buf + kCWinMax * 4;
+  for (int t = nr + lane; t < n; t += 32) sr[t] = rw[w0 + t];
+  for (int t = nm + lane; t < n; t += 32) sm[t] = mk[w0 + t];
+  // sequence ends inside the window (token s - 1 for every start s in (w0, w1]) while the copy lands
+  const int64_t lo = has ? mark_ends(bm, nb * (kBatch / 32), cum, base, gs, pend, w0, w1, lane) : 0;
+  {
+    uint32_t done;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+          " selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done) : "r"(bar), "r"(0u) : "memory");
+    } while (!done);
+  }
+  __syncwarp();
+
+  // batch b of the window from shared memory (rotated chunk order: conflict-free), tokens past
+  // the window's end masked off
+  const int rot = (lane >> 1) & 3;
+  auto get = [&](Batch& B, int b, uint32_t& on16) {
+    const uint8_t* rb = buf + b * (kBatch * 4) + 64 * lane;
+    float4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = *reinterpret_cast<const float4*>(rb + 16 * ((k + rot) & 3));
+    float4 u[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[c] = (rot & 1) ? v[(c + 3) & 3] : v[c];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) B.r[c] = (rot & 2) ? u[(c + 2) & 3] : u[c];
+    B.m = *reinterpret_cast<const uint4*>(sm + b * kBatch + 16 * lane);
+    const int lt = b * kBatch + kTokLane * lane;
+    uint32_t in16 = 0xffffu;
+    if (lt + kTokLane > n) in16 = lt >= n ? 0u : 0xffffu >> (uint32_t)(lt + kTokLane - n);
+    on16 = in16 & (nonzero_bytes4(B.m.x) | nonzero_bytes4(B.m.y) << 4 | nonzero_bytes4(B.m.z) << 8 |
+                   nonzero_bytes4(B.m.w) << 12);
+  };
+  auto ends16 = [&](int b) { return (bm[16 * b + (lane >> 1)] >> (16 * (lane & 1))) & 0xffffu; };
+
+  // ---- pass 1: lane maps, batch maps, the window's map -------------------------------------
+  float wS = 0.f, wP = 1.f;
+#pragma unroll 1
+  for (int b = nb - 1; b >= 0; --b) {
+    Batch cur;
+    uint32_t on16;
+    get(cur, b, on16);
+    const uint32_t e = ends16(b);
+    float S = 0.f;
+#pragma unroll
+    for (int i = kTokLane - 1; i >= 0; --i)
+      S = fmaf(((e >> i) & 1u) ? 0.f : gamma, S, (on16 >> i) & 1u ? tok_r(cur, i) : 0.f);
+    float rS, rP, bS, bP;
+    warp_compose(S, e ? 0.f : g16, lane, rS, rP, bS, bP);
+    lmap[wid][b][lane] = make_float2(rS, rP);
+    if (lane == 0) bmap[wid][b] = make_float2(bS, bP);
+    wS = bS + bP * wS;
+    wP = bP * wP;
+  }
+  if (has && lane == 0) agg[gw] = make_float2(wS, wP);
+  delay_inject(9);
+  // every window's map is published
+  if (gridDim.x == 1) __syncthreads();
+  else cooperative_groups::this_grid().sync();
+
+  if (has) {
+    // ---- carry: the maps of the windows to the right (same rank) up to the first zero slope
+    const int64_t wend = rt.wbeg[ri + 1];
+    float cS = 0.f, cP = 1.f;
+    for (int64_t j0 = gw + 1; j0 < wend && cP != 0.f; j0 += 32) {
+      const int64_t j = j0 + lane;
+      const float2 m = j < wend ? __ldcg(&agg[j]) : make_float2(0.f, 1.f);
+      float rS, rP, tS, tP;
+      warp_compose(m.x, m.y, lane, rS, rP, tS, tP);
+      cS = cS + cP * tS;
+      cP = cP * tP;
+    }
+    // ---- pass 2: the returns, float4 stores, statistics
+    const bool count_stats = rt.t[ri] == 0;
+    float c = cS;  // G right of batch b (right to left)
+#pragma unroll 1
+    for (int b = nb - 1; b >= 0; --b) {
+      Batch cur;
+      uint32_t on16;
+      get(cur, b, on16);
+      const uint32_t e = ends16(b);
+      const float2 rm = lmap[wid][b][lane];
+      float g_next = rm.x + rm.y * c;
+      float out[kTokLane];
+#pragma unroll
+      for (int i = kTokLane - 1; i >= 0; --i) {
+        out[i] = fmaf(((e >> i) & 1u) ? 0.f : gamma, g_next, (on16 >> i) & 1u ? tok_r(cur, i) : 0.f);
+        g_next = out[i];
+      }
+      const float2 bmb = bmap[wid][b];
+      c = bmb.x + bmb.y * c;
+      if (count_stats) {
+        float sa = 0.f, sb = 0.f, qa = 0.f, qb = 0.f;
+#pragma unroll
+        for (int i = 0; i < kTokLane; i += 2) {
+          const float o0 = (on16 >> i) & 1u ? out[i] : 0.f;
+          const float o1 = (on16 >> (i + 1)) & 1u ? out[i + 1] : 0.f;
+          sa += o0;
+          qa = fmaf(o0, o0, qa);
+          sb += o1;
+          qb = fmaf(o1, o1, qb);
+        }
+        s_m += (double)__popc(on16);
+        s_g += (double)(sa + sb);
+        s_g2 += (double)(qa + qb);
+      }
+      const int64_t t = w0 + b * kBatch + kTokLane * lane;
+      if (aligned(G, 16) && t + kTokLane <= w1) {
+        float4* gp = reinterpret_cast<float4*>(G + t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          __stcs(gp + k, make_float4(out[4 * k], out[4 * k + 1], out[4 * k + 2], out[4 * k + 3]));
+      } else {
+        for (int i = 0; i < kTokLane; ++i)
+          if (t + i < w1) G[t + i] = out[i];
+      }
+    }
+    // per-sequence return G_0 of the sequences starting in the window
+    seq_returns(a.seq_return[r], G, cum, base, gs, pend, lo, w1, ntok, lane);
+    __syncwarp();
+  }
+  returns_epilogue(a, rt, red, s_m, s_g, s_g2, kWarps);
+}
+
 // A_t = m_t (G_t - mu) / (sigma + eps) over every token of the launch's source ranks: one
 // flattened stream of 4-token quads over all ranks (4 quads in flight per thread), then the
 // unaligned remainders token by token.  Measured on the C5-lt batch: read-only-path loads
@@ -1170,8 +1423,12 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
   __shared__ int64_t qbeg[kMaxWorld + 1];   // vector quads of the ranks (prefix)
   __shared__ int64_t tbeg[kMaxWorld + 1];   // scalar remainder tokens of the ranks (prefix)
   __shared__ float s_mu, s_inv;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // the statistics are loaded first, so their round trip overlaps the header's
+    double st[3] = {0.0, 0.0, 0.0};
+    if (threadIdx.x == 0) { st[0] = a.stats[0]; st[1] = a.stats[1]; st[2] = a.stats[2]; }
     rank_table(a, rt, 1);
+    if (threadIdx.x == 0) {
     qbeg[0] = tbeg[0] = 0;
     for (int ri = 0; ri < rt.n; ++ri) {
       const int r = rt.rank[ri];
@@ -1180,12 +1437,13 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
       qbeg[ri + 1] = qbeg[ri] + nq;
       tbeg[ri + 1] = tbeg[ri] + rt.ntok[ri] - 4 * nq;
     }
-    const double n = a.stats[0];
-    const double mu = n > 0 ? a.stats[1] / n : 0.0;
-    double var = n > 0 ? a.stats[2] / n - mu * mu : 0.0;
+    const double n = st[0];
+    const double mu = n > 0 ? st[1] / n : 0.0;
+    double var = n > 0 ? st[2] / n - mu * mu : 0.0;
     if (var < 0) var = 0;
     s_mu = (float)mu;
     s_inv = (float)(1.0 / (sqrt(var) + (double)a.eps));
+    }
   }
   __syncthreads();
   const float mu = s_mu, inv = s_inv;
@@ -1246,6 +1504,47 @@ cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s)
   if (e != cudaSuccess) return e;
   returns_units_kernel<<<sm_count * kU2Ctas, kWarps * 32, kRingBytes, s>>>(a);
   return cudaGetLastError();
+}
+
+int returns_coop_capacity_warps(int sm_count) {
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int d = dev >= 0 && dev < 64 ? dev : 0;
+  if (per_sm[d] <= 0) {
+    static bool opted[64] = {};
+    if (opt_in_dynamic_smem(returns_coop_kernel, (int)(kWarps * kCBytes), opted) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0;
+    }
+    int p = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&p, returns_coop_kernel, kWarps * 32,
+                                                      kWarps * kCBytes) != cudaSuccess)
+      p = 0;
+    (void)cudaGetLastError();
+    per_sm[d] = p > kCCtas ? kCCtas : p;
+    if (per_sm[d] <= 0) return 0;
+  }
+  return sm_count * per_sm[d] * kWarps;
+}
+
+// One warp per window: ceil(windows / 8) CTAs (windows <= 0: the whole co-resident grid, for a
+// launch that decides on the device).
+cudaError_t launch_returns_coop(const AggArgs& a, int64_t windows, int sm_count, cudaStream_t s) {
+  static bool opted[64] = {};
+  cudaError_t e = opt_in_dynamic_smem(returns_coop_kernel, (int)(kWarps * kCBytes), opted);
+  if (e != cudaSuccess) return e;
+  const int64_t cap = returns_coop_capacity_warps(sm_count) / kWarps;
+  int64_t g = windows > 0 ? (windows + kWarps - 1) / kWarps : cap;
+  if (g > cap) g = cap;
+  const int grid = (int)(g < 1 ? 1 : g);
+  if (grid <= 1) {
+    returns_coop_kernel<<<1, kWarps * 32, kWarps * kCBytes, s>>>(a);
+    return cudaGetLastError();
+  }
+  void* args[] = {const_cast<AggArgs*>(&a)};
+  return cudaLaunchCooperativeKernel((const void*)returns_coop_kernel, dim3(grid), dim3(kWarps * 32),
+                                     args, kWarps * kCBytes, s);
 }
 
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {

@@ -1857,44 +1857,59 @@ extern "C" earl_status_t earl_returns(earl_plan_t p, float gamma, const void* co
   a.win = reinterpret_cast<AggWindow*>(a.ws + 1);
   a.win_cap = p->agg_cap;
   a.unit_first = reinterpret_cast<int64_t*>(a.win + p->agg_cap);
-  // the single-pass unit kernel when the host knows the batch has no sequence longer than
-  // kUnitMaxLen tokens (one warp streams a unit); otherwise the windowed look-back kernel.
-  // EARL_RETURNS=units|windows forces one (tests).
-  // When the host does not know the batch (the plan was re-planned since its last sync), both
-  // are launched and each checks the planner's max_len on the device (one exits at once).
+  // Three returns kernels (choose_returns): the cooperative one when every window of the batch
+  // gets its own warp of a co-resident grid (small and mid batches), the single-pass unit kernel
+  // for large batches without sequences longer than kUnitMaxLen, else the windowed look-back
+  // kernel.  The host decides when it knows the batch; otherwise every kernel is launched and
+  // each evaluates the rule on the device from the plan header (all but one exit at once).
+  // EARL_RETURNS=coop|units|windows forces one (tests).
   const char* force = getenv("EARL_RETURNS");
   a.resident_warps = (int64_t)p->comm->sm_count * kUnitWarpsPerSm;
-  int which = 3;
+  a.coop_warps = returns_coop_capacity_warps(p->comm->sm_count);
+  a.coop_nb = 0;
+  int kmask = a.coop_warps > 0 ? 7 : 3;  // bit k: launch kernel k (ReturnsKernel)
+  int64_t coop_need = 0;                // the cooperative kernel's windows (0: its whole grid)
   if (p->synced) {
     const earl_layout_t& S = p->lay[0];
-    int64_t units = 0, big = 0;
+    int64_t nt[kMaxWorld];
+    int n = 0;
     for (int r = 0; r < p->comm->world; ++r) {
       if (!p->comm->emulated && r != p->comm->rank) continue;
       const int q = r - S.rank0;
       if (q < 0 || q >= S.dp * S.tp) continue;
-      const int64_t n = p->host_hdr.shard_tokens[0][q / S.tp];
-      units += (n + kUnitTok - 1) / kUnitTok;
-      big = std::max(big, n);
+      nt[n++] = p->host_hdr.shard_tokens[0][q / S.tp];
     }
-    which = prefer_units(p->host_hdr.max_len, units, a.resident_warps, big) ? 1 : 2;
+    int nb = 0;
+    const int id = choose_returns(nt, n, p->host_hdr.max_len, a.resident_warps, a.coop_warps, &nb);
+    kmask = 1 << id;
+    if (nb > 0) {
+      a.coop_nb = nb;
+      for (int i = 0; i < n; ++i) coop_need += (nt[i] + 512LL * nb - 1) / (512LL * nb);
+    }
   }
-  if (force && std::strcmp(force, "units") == 0) which = 1;
-  if (force && std::strcmp(force, "windows") == 0) which = 2;
+  if (force && std::strcmp(force, "units") == 0) kmask = 1 << kRetUnits;
+  if (force && std::strcmp(force, "windows") == 0) kmask = 1 << kRetWindows;
+  if (force && std::strcmp(force, "coop") == 0) kmask = 1 << kRetCoop;
+  const bool gated = (kmask & (kmask - 1)) != 0;
   cudaStream_t rs = static_cast<cudaStream_t>(stream);
   use_begin(p, rs);
   cudaError_t e = cudaSuccess;
-  if (which & 1) {
-    a.gate = which == 3 ? 1 : 0;
-    e = launch_returns_units(a, p->comm->sm_count, rs);
-    if (e == cudaSuccess) g_launches.fetch_add(1);  // + the unit table kernel
+  if (kmask & (1 << kRetCoop)) {
+    a.gate = gated ? kRetCoop + 1 : 0;
+    e = launch_returns_coop(a, coop_need, p->comm->sm_count, rs);
+    if (e == cudaSuccess) g_launches.fetch_add(1);
   }
-  if (e == cudaSuccess && (which & 2)) {
-    a.gate = which == 3 ? 2 : 0;
+  if (e == cudaSuccess && (kmask & (1 << kRetUnits))) {
+    a.gate = gated ? kRetUnits + 1 : 0;
+    e = launch_returns_units(a, p->comm->sm_count, rs);
+    if (e == cudaSuccess) g_launches.fetch_add(2);  // the unit table kernel, the unit kernel
+  }
+  if (e == cudaSuccess && (kmask & (1 << kRetWindows))) {
+    a.gate = gated ? kRetWindows + 1 : 0;
     e = launch_returns(a, p->comm->sm_count, rs);
-    if (e == cudaSuccess && which == 3) g_launches.fetch_add(1);
+    if (e == cudaSuccess) g_launches.fetch_add(1);
   }
   if (e != cudaSuccess) return fail(EARL_ERR_CUDA, "returns launch: %s", cudaGetErrorString(e));
-  g_launches.fetch_add(1);
   const bool synced = p->synced;
   use_end(p, static_cast<cudaStream_t>(stream));
   p->synced = synced;  // T is unchanged (a CAPACITY latch is read by the next synchronising call)

@@ -225,6 +225,31 @@ __host__ __device__ inline bool prefer_units(int64_t max_len, int64_t units, int
                                              int64_t max_rank_tokens) {
   return max_len <= kUnitMaxLen && units >= kUnitsPerWarp * warps && max_rank_tokens <= kU2MaxTok;
 }
+// The cooperative returns kernel: one window of 512 * nb tokens (nb = 1, 2 or 4) per warp of a
+// co-resident grid, so a batch fits when its windows do not outnumber the grid's warps.
+constexpr int kCoopMaxNB = 4;
+// Returns kernels (AggArgs::gate = id + 1 runs a kernel only if the device's choice is id).
+enum ReturnsKernel { kRetUnits = 0, kRetWindows = 1, kRetCoop = 2 };
+// Which returns kernel a batch gets, from its source ranks' token counts (host and device
+// evaluate the same rule): the cooperative kernel when every window gets its own warp, the
+// unit kernel for large batches without very long sequences, else the windowed look-back kernel.
+// *coop_nb: the cooperative kernel's batches per window (0: does not fit).
+__host__ __device__ inline int choose_returns(const int64_t* ntok, int n, int64_t max_len,
+                                              int64_t unit_warps, int64_t coop_warps,
+                                              int* coop_nb) {
+  int64_t units = 0, big = 0, cw[3] = {0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    units += (ntok[i] + kUnitTok - 1) / kUnitTok;
+    big = ntok[i] > big ? ntok[i] : big;
+    for (int k = 0; k < 3; ++k) cw[k] += (ntok[i] + (512 << k) - 1) / (512 << k);
+  }
+  int nb = 0;
+  for (int k = 0; k < 3 && nb == 0; ++k)
+    if (cw[k] <= coop_warps) nb = 1 << k;
+  if (coop_nb) *coop_nb = nb;
+  if (nb > 0) return kRetCoop;
+  return prefer_units(max_len, units, unit_warps, big) ? kRetUnits : kRetWindows;
+}
 
 struct AggArgs {
   AggWork* ws;
@@ -233,6 +258,8 @@ struct AggArgs {
   int64_t* unit_first;     // unit kernel: first sequence (sorted position) of every unit
   int32_t gate;            // 0: run; 1: run only if the unit kernel is preferred; 2: only if not
   int64_t resident_warps;  // the unit kernel's resident warps (prefer_units)
+  int64_t coop_warps;      // the cooperative kernel's warps (its grid; 0: not available)
+  int32_t coop_nb;         // its batches per window (0: the kernel decides from the plan header)
   PlanArgs plan;
   const PlanHeader* hdr;
   int32_t world;
@@ -301,6 +328,8 @@ void mc_free(VmmMem* mc, int device);
 // launchers (defined in the .cu files)
 cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s);
 cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s);
+int returns_coop_capacity_warps(int sm_count);  // co-resident warps of the cooperative kernel
+cudaError_t launch_returns_coop(const AggArgs& a, int64_t windows, int sm_count, cudaStream_t s);
 int64_t returns_windows(int64_t tokens);
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s);
 int planner_grid(int64_t n_seqs, int64_t max_pieces, int sm_count, size_t lpt_smem, bool fast);

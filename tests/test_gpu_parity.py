@@ -617,7 +617,7 @@ def test_seq_fields_on_gpu(seed):
 
 @pytest.mark.parametrize("gamma", [1.0, 0.97, 0.0])
 @pytest.mark.parametrize("tp", [1, 2])
-@pytest.mark.parametrize("kernel", ["units", "windows"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
 def test_distributed_advantages_on_gpu(gamma, tp, kernel, monkeypatch):
     """Reading n5 on the GPU (fp32 tokens, fp64 statistics) against the fp64 oracle, with both
     returns kernels (the single-pass unit kernel and the windowed look-back kernel).
@@ -770,7 +770,7 @@ ADV_EDGE_CASES = {
 @pytest.mark.parametrize("case", sorted(ADV_EDGE_CASES))
 @pytest.mark.parametrize("gamma", [1.0, 0.9])
 @pytest.mark.parametrize("shift", [0, 1])
-@pytest.mark.parametrize("kernel", ["units", "windows"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
 def test_returns_edge_cases(case, gamma, shift, kernel, monkeypatch):
     monkeypatch.setenv("EARL_RETURNS", kernel)
     lens, dp = ADV_EDGE_CASES[case]
@@ -779,7 +779,7 @@ def test_returns_edge_cases(case, gamma, shift, kernel, monkeypatch):
 
 
 @pytest.mark.parametrize("graph", [False, True])
-@pytest.mark.parametrize("kernel", ["units", "windows"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
 def test_returns_repeat_and_graph(graph, kernel, monkeypatch):
     """The look-back workspace / unit table is reused across launches and graph replays."""
     monkeypatch.setenv("EARL_RETURNS", kernel)
