@@ -407,7 +407,10 @@ EARL_API earl_status_t earl_dispatch_exec_staged(earl_plan_t plan, const void* c
  * ([world] in an emulated comm), seq_return (optional, NULL) fp32 [n_local_seqs] gets G_0.
  * Accumulates the fp64 partials (sum m, sum m G, sum m G^2) of TP replica 0 into the DEVICE
  * array partial[3] (caller zeroes it).  Readings n5 in DESIGN.md.  Errors: UNSUPPORTED if the
- * source layout splits sequences (sp > 1). */
+ * source layout splits sequences (sp > 1).  Three kernels serve it, chosen by the
+ * batch's size on the host, or on the device when the plan was re-planned since its last sync;
+ * EARL_RETURNS=coop|units|windows forces one (a forced kernel the batch does not fit latches
+ * CAPACITY, reported by the next synchronising call). */
 EARL_API earl_status_t earl_returns(earl_plan_t plan, float gamma, const void* const* rewards,
                                     const void* const* mask, void* const* returns,
                                     void* const* seq_return, double* partial, void* stream);
