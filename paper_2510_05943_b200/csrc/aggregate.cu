@@ -757,18 +757,24 @@ __global__ void unit_table_kernel(const __grid_constant__ AggArgs a) {
   const int64_t* cum = a.plan.cum[0];
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
-  for (int ri = 0; ri < rt.n; ++ri) {
+  // one flat pass over every rank's positions gs .. pend (a loop per rank had put one HBM round
+  // trip per rank on the critical path)
+  int64_t pre[kMaxWorld + 1];
+  pre[0] = 0;
+  for (int ri = 0; ri < rt.n; ++ri)
+    pre[ri + 1] = pre[ri] + (rt.wbeg[ri + 1] > rt.wbeg[ri] ? rt.cnt[ri] + 1 : 0);
+  for (int64_t x = tid; x < pre[rt.n]; x += nth) {
+    int ri = 0;
+    while (x >= pre[ri + 1]) ++ri;
     const int64_t gs = rt.gs[ri], pend = gs + rt.cnt[ri], nu = rt.wbeg[ri + 1] - rt.wbeg[ri];
-    if (nu == 0) continue;
+    const int64_t p = gs + (x - pre[ri]);
     const int64_t base = cum[gs];
     int64_t* tab = a.unit_first + rt.wbeg[ri];
-    for (int64_t p = gs + tid; p <= pend; p += nth) {
-      const int64_t s = cum[p] - base;                   // start of sequence p (ntok for pend)
-      const int64_t kl = p == gs ? 0 : (cum[p - 1] - base) / kUnitTok + 1;
-      int64_t kh = s / kUnitTok;
-      if (p == pend || kh > nu - 1) kh = nu - 1;
-      for (int64_t k = kl; k <= kh; ++k) tab[k] = p;
-    }
+    const int64_t s = cum[p] - base;                   // start of sequence p (ntok for pend)
+    const int64_t kl = p == gs ? 0 : (cum[p - 1] - base) / kUnitTok + 1;
+    int64_t kh = s / kUnitTok;
+    if (p == pend || kh > nu - 1) kh = nu - 1;
+    for (int64_t k = kl; k <= kh; ++k) tab[k] = p;
   }
 }
 
@@ -1495,7 +1501,7 @@ __global__ void __launch_bounds__(256) advantage_kernel(const __grid_constant__ 
 int64_t returns_windows(int64_t tokens) { return (tokens + kMaxWin - 1) / kMaxWin + 16384; }
 
 cudaError_t launch_returns_units(const AggArgs& a, int sm_count, cudaStream_t s) {
-  unit_table_kernel<<<sm_count, 256, 0, s>>>(a);
+  unit_table_kernel<<<sm_count * 4, 256, 0, s>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   constexpr size_t kRingBytes = (size_t)kWarps * kUSlots * kSlotBytes;
