@@ -617,16 +617,18 @@ def test_seq_fields_on_gpu(seed):
 
 @pytest.mark.parametrize("gamma", [1.0, 0.97, 0.0])
 @pytest.mark.parametrize("tp", [1, 2])
-@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop", "auto"])
 def test_distributed_advantages_on_gpu(gamma, tp, kernel, monkeypatch):
-    """Reading n5 on the GPU (fp32 tokens, fp64 statistics) against the fp64 oracle, with both
-    returns kernels (the single-pass unit kernel and the windowed look-back kernel).
+    """Reading n5 on the GPU (fp32 tokens, fp64 statistics) against the fp64 oracle, with every
+    returns kernel forced (the cooperative, the single-pass unit and the windowed look-back
+    kernel) and with the device's own choice (auto: all three launched, gated on the header).
     Tolerance: the fp32 recurrence G_t = v_t + gamma G_{t+1} accumulates at most
     u * min(L, 1/(1-gamma)) * max|G| rounding error (u = 2^-24), times 4 for the warp-parallel
     composition; A inherits it divided by sigma."""
     import torch
     from paper_2510_05943_b200.dispatch import EmulatedDispatch
-    monkeypatch.setenv("EARL_RETURNS", kernel)
+    if kernel != "auto":  # auto: the plan is not synchronised, every kernel launches gated
+        monkeypatch.setenv("EARL_RETURNS", kernel)
     rng = np.random.default_rng(int(gamma * 100) + tp)
     world = 8
     n = 300
@@ -770,19 +772,21 @@ ADV_EDGE_CASES = {
 @pytest.mark.parametrize("case", sorted(ADV_EDGE_CASES))
 @pytest.mark.parametrize("gamma", [1.0, 0.9])
 @pytest.mark.parametrize("shift", [0, 1])
-@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop", "auto"])
 def test_returns_edge_cases(case, gamma, shift, kernel, monkeypatch):
-    monkeypatch.setenv("EARL_RETURNS", kernel)
+    if kernel != "auto":  # auto: the plan is not synchronised, every kernel launches gated
+        monkeypatch.setenv("EARL_RETURNS", kernel)
     lens, dp = ADV_EDGE_CASES[case]
     src = W.layout(dp=dp, assign="given_counts", counts=W.near_equal_counts(len(lens), dp))
     _adv_case(list(lens), src, gamma, 8, shift=shift, seed=len(lens))
 
 
 @pytest.mark.parametrize("graph", [False, True])
-@pytest.mark.parametrize("kernel", ["units", "windows", "coop"])
+@pytest.mark.parametrize("kernel", ["units", "windows", "coop", "auto"])
 def test_returns_repeat_and_graph(graph, kernel, monkeypatch):
     """The look-back workspace / unit table is reused across launches and graph replays."""
-    monkeypatch.setenv("EARL_RETURNS", kernel)
+    if kernel != "auto":  # auto: the plan is not synchronised, every kernel launches gated
+        monkeypatch.setenv("EARL_RETURNS", kernel)
     lens = W.lognormal_lengths(200, 1500, 0.8, 1, 6000, seed=9).tolist()
     _adv_case(lens, W.layout(dp=4, tp=2, assign="lpt"), 0.99, 8, repeats=5, graph=graph)
 
