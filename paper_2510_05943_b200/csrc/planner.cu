@@ -913,7 +913,10 @@ __global__ void __launch_bounds__(NT, 1) planner_sp1_kernel(const __grid_constan
     block_excl_scan(part, tot, sm_scan);
     if (tid == 0) a.cta_sums[blockIdx.x] = tot;
   }
-  if (tid < kMaxBuckets) { fs.hcnt[tid] = 0; fs.htok[tid] = 0; }
+  if (tid < kMaxBuckets) {
+    fs.hcnt[tid] = 0; fs.htok[tid] = 0;
+    fs.run_cnt[tid] = 0; fs.tot_cnt[tid] = 0; fs.run_tok[tid] = 0; fs.tot_tok[tid] = 0;
+  }
   gsync();
   if (tid < 32) {
     int64_t before = 0, all = 0;
@@ -986,25 +989,32 @@ __global__ void __launch_bounds__(NT, 1) planner_sp1_kernel(const __grid_constan
   }
   gsync();
   stamp(a, 3);
-  // per bucket: the sum over the CTAs before this one and over all (warp q handles buckets
-  // q, q + 32, q + 64 of counts and of tokens; lanes stride over the CTAs)
-  for (int q = w; q < 2 * U; q += NT / 32) {
-    const int u = q < U ? q : q - U;
-    const int64_t* col = fh + (q < U ? 0 : (int64_t)gridDim.x * kMaxBuckets) + u;
-    int64_t before = 0, all = 0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) {
-      const int64_t v = __ldcg(col + (int64_t)b * kMaxBuckets);
-      all += v;
-      if (b < (int)blockIdx.x) before += v;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      before += __shfl_xor_sync(kFull, before, o);
-      all += __shfl_xor_sync(kFull, all, o);
-    }
-    if (lane == 0) {
-      if (q < U) { fs.run_cnt[u] = before; fs.tot_cnt[u] = all; }
-      else { fs.run_tok[u] = before; fs.tot_tok[u] = all; }
+  // per bucket: the sum over the CTAs before this one and over all.  The whole CTA reads the
+  // published histograms at once: thread t sums column t % 2U (counts, then tokens) over the
+  // CTAs r, r + R, ... (r = t / 2U, R = NT / 2U), loads unrolled, then one shared-memory atomic
+  // per thread (a warp per column had put one L2 round trip per column on the critical path).
+  {
+    const int Q = 2 * U;
+    const int R = NT / Q;
+    const int G = (int)gridDim.x;
+    if (tid < Q * R) {
+      const int q = tid % Q, r0 = tid / Q;
+      const int u = q < U ? q : q - U;
+      const int64_t* col = fh + (q < U ? 0 : (int64_t)G * kMaxBuckets) + u;
+      int64_t before = 0, all = 0;
+#pragma unroll 4
+      for (int b = r0; b < G; b += R) {
+        const int64_t x = __ldcg(col + (int64_t)b * kMaxBuckets);
+        all += x;
+        if (b < (int)blockIdx.x) before += x;
+      }
+      if (q < U) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&fs.run_cnt[u]), (unsigned long long)before);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&fs.tot_cnt[u]), (unsigned long long)all);
+      } else {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&fs.run_tok[u]), (unsigned long long)before);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&fs.tot_tok[u]), (unsigned long long)all);
+      }
     }
   }
   __syncthreads();
