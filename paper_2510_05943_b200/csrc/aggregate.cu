@@ -1567,12 +1567,16 @@ cudaError_t launch_returns(const AggArgs& a, int sm_count, cudaStream_t s) {
 }
 
 // Grid sized to the work when the plan's token count is known on the host (tokens >= 0): about
-// 8 loop trips of kU quads per thread, at least one CTA per SM and at most 64 per SM (C5-lt:
-// 0.50 ms at 64 per SM against 0.52 at 16; a small batch pays every extra CTA's prologue).
+// EARL_ADV_TRIPS loop trips of kU quads per thread, at least one CTA per SM and at most 64 per SM
+// (C5-lt: 0.50 ms at 64 per SM against 0.52 at 16).  2 trips since the rank table costs one
+// round trip per CTA (C2 / C4 12.3 -> 10.2 / 14.3 -> 12.3 us against 8 trips; 1 or 4: no better).
+#ifndef EARL_ADV_TRIPS
+#define EARL_ADV_TRIPS 2
+#endif
 cudaError_t launch_advantages(const AggArgs& a, int sm_count, int64_t tokens, cudaStream_t s) {
   int64_t grid = (int64_t)sm_count * 16;
   if (tokens >= 0) {
-    grid = (tokens / 4 + 256 * 4 * 8 - 1) / (256 * 4 * 8);
+    grid = (tokens / 4 + 256 * 4 * EARL_ADV_TRIPS - 1) / (256 * 4 * EARL_ADV_TRIPS);
     grid = grid < sm_count ? sm_count : (grid > 64LL * sm_count ? 64LL * sm_count : grid);
   }
   advantage_kernel<<<(unsigned)grid, 256, 0, s>>>(a);
