@@ -192,8 +192,7 @@ constexpr uint32_t kMinSpace = 256;  // close a stage when less than this is lef
 
 struct __align__(16) StageDesc {
   uint32_t n;
-  uint32_t used;   // stage bytes taken so far (a fill interrupted by a claim resumes here)
-  uint32_t pad_[2];
+  uint32_t pad_[3];
   SubDesc sub[kSubs];
 };
 
@@ -314,7 +313,6 @@ __device__ void build_view(const CopyArgs& a, uint64_t c0, View& v) {
 // is passed by reference into every (inlined) method so its fields are constant-bank loads.
 struct Walker {
   int vn;  // the view's block count (a register copy; the View itself lives in local memory)
-  bool done;  // a claim found no unit left
   int b;  // current view block and its fields
   int64_t b_rbeg, b_rend, b_tbeg;
   uint64_t b_cbase;
@@ -348,7 +346,6 @@ struct Walker {
   __device__ __forceinline__ void setup(const CopyArgs& a, const View& v, uint64_t c0_,
                                         uint64_t first_dyn_) {
     vn = v.n;
-    done = false;
     c0 = c0_; unit = 0; n_units = 0; first_dyn = first_dyn_; total = v.cbase[v.n];
     prem = 0; R = 0; xpos = x1 = 0; f = 0;
     set_block(v, 0);
@@ -392,9 +389,25 @@ struct Walker {
     ++f;
   }
 
-  // Position the walker at cost x0 (a unit's start) with the whole warp: lane 0 holds the walker (and the View); every lane takes part
-  // in a 32-ary search for the record whose cost starts at or before x0 (one L2 round trip per
-  // 32-fold narrowing instead of one per halving).  Called where the warp is converged.
+  __device__ __forceinline__ void start(const CopyArgs& a, const View& v, uint64_t x0,
+                                        uint64_t x1_) {
+    x1 = x1_ < total ? x1_ : total;
+    xpos = x0;
+    prem = 0;
+    if (xpos >= x1) return;
+    int bb = 0;
+    while (bb + 1 < vn && v.cbase[bb + 1] <= xpos) ++bb;
+    set_block(v, bb);
+    int64_t lo = b_rbeg, hi = b_rend - 1;  // last record whose cost starts <= xpos
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (cost(a, mid) <= xpos) lo = mid; else hi = mid - 1;
+    }
+    load_record(a, lo);
+    while (f + 1 < a.n_fields && cj + fo + n * a.Bf[f] + c0 <= xpos) next_field(a);
+  }
+
+  // Position the walker at cost x0 with the whole warp (32-ary search; lane 0 holds the walker)
   __device__ __forceinline__ void start_warp(const CopyArgs& a, const View& v, uint64_t x0,
                                              uint64_t x1_, uint64_t c0w, int lane) {
     int64_t rb = 0, re = 0, tb = 0;
@@ -419,7 +432,7 @@ struct Walker {
     cb = __shfl_sync(kFull, cb, 0);
     const int F = a.n_fields;
     const uint64_t B = a.Bpre[F];
-    int64_t lo = rb, hi = re - 1;  // cost(lo) <= x0 holds: the block starts at or before x0
+    int64_t lo = rb, hi = re - 1;
     while (hi > lo) {
       const int64_t step = (hi - lo + 31) / 32;
       const int64_t pj = lo + (int64_t)lane * step;
@@ -436,6 +449,13 @@ struct Walker {
     }
   }
 
+  // Claim the next unit: returns false when the launch's work is exhausted.
+  __device__ __forceinline__ bool claim(const CopyArgs& a, const View& v) {
+    const uint64_t u = first_dyn + atomicAdd(a.work_ctr, 1u);
+    if (u >= n_units) return false;
+    start(a, v, u * unit, (u + 1) * unit);
+    return true;
+  }
 
   __device__ __forceinline__ bool next_piece(const CopyArgs& a, const View& v) {
     const bool unpack_rank = a.mode == kUnpack && a.view_rank >= 0;
@@ -514,12 +534,12 @@ struct Walker {
     return false;
   }
 
-  // Next source range of at most `space` stage bytes (space >= kMinSpace): 1 when one was
-  // taken, 0 when the launch's work is exhausted, 2 when the current unit is done and the next
-  // one must be claimed (by the whole warp: claim_warp).
-  __device__ __forceinline__ int next_sub(const CopyArgs& a, const View& v, SubDesc& d,
-                                          uint32_t space) {
-    if (prem == 0 && !next_piece(a, v)) return done ? 0 : 2;
+  // Next source range of at most `space` stage bytes (space >= kMinSpace): false when the
+  // launch's work is exhausted.
+  __device__ __forceinline__ bool next_sub(const CopyArgs& a, const View& v, SubDesc& d,
+                                           uint32_t space) {
+    while (prem == 0 && !next_piece(a, v))
+      if (!claim(a, v)) return false;
     const uint32_t off = (uint32_t)((uintptr_t)psrc & 15);
     const uint64_t room = space - off;
     uint32_t len = (uint32_t)(prem < room ? prem : room);
@@ -541,36 +561,28 @@ struct Walker {
     psrc += len;
     pdst += len;
     prem -= len;
-    return 1;
+    return true;
   }
 };
 
 // Fill stage `st` (lane 0): pack source ranges until the stage is full, then one expect_tx for
-// the total and one TMA load per range, all completing on the stage's mbarrier.  Returns 1 when
-// the stage was issued, 0 when there was nothing left, 2 when the walker needs the warp for a
-// claim: the ranges taken so far stay in the descriptor and the next call (resume) appends.
+// the total and one TMA load per range, all completing on the stage's mbarrier.
 template <int CHUNK>
-__device__ __forceinline__ int fill_stage(const CopyArgs& a, const View& v, Walker& wk,
-                                          StageDesc& sd, uint8_t* stage, uint64_t* bar, bool resume) {
-  uint32_t used = resume ? sd.used : 0, n = resume ? sd.n : 0;
+__device__ __forceinline__ bool fill_stage(const CopyArgs& a, const View& v, Walker& wk,
+                                           StageDesc& sd, uint8_t* stage, uint64_t* bar) {
+  uint32_t used = 0, n = 0;
   while (n < (uint32_t)kSubs && CHUNK - used >= kMinSpace) {
-    const int r = wk.next_sub(a, v, sd.sub[n], CHUNK - used);
-    if (r == 2) {
-      sd.n = n;
-      sd.used = used;
-      return 2;
-    }
-    if (r == 0) break;
+    if (!wk.next_sub(a, v, sd.sub[n], CHUNK - used)) break;
     sd.sub[n].so = used;
     used += sd.sub[n].load_bytes;
     ++n;
   }
   sd.n = n;
-  if (n == 0) return 0;
+  if (n == 0) return false;
   mbar_expect_tx(bar, used);
   for (uint32_t k = 0; k < n; ++k)
     tma_load(stage + sd.sub[k].so, sd.sub[k].src_al, sd.sub[k].load_bytes, bar);
-  return 1;
+  return true;
 }
 
 // The realigning warp-store loop of a non-congruent range: 16-B outputs k = lane, lane + 32, ...
@@ -806,35 +818,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       wk.unit = unit;
       wk.n_units = (total + unit - 1) / unit;
     }
-    {  // every warp's first unit, searched by the whole warp
+    {
       const uint64_t nu = __shfl_sync(kFull, lane == 0 ? wk.n_units : 0ull, 0);
       const uint64_t un = __shfl_sync(kFull, lane == 0 ? wk.unit : 0ull, 0);
       if (wid < nu) wk.start_warp(a, v, wid * un, (wid + 1) * un, c0, lane);
     }
-    // fill stage s (whole warp): lane 0 walks; a claim of the next unit is done by the warp
-    // (atomic by lane 0, then a 32-ary search by every lane) and the fill resumes
-    const uint64_t nu_w = __shfl_sync(kFull, lane == 0 ? wk.n_units : 0ull, 0);
-    const uint64_t un_w = __shfl_sync(kFull, lane == 0 ? wk.unit : 0ull, 0);
-    auto fill = [&](int s) -> bool {
-      bool resume = false;
-      for (;;) {
-        int st = 0;
-        if (lane == 0) st = fill_stage<CHUNK>(a, v, wk, desc[s], data + (size_t)s * CHUNK, &bar[s], resume);
-        st = __shfl_sync(kFull, st, 0);
-        if (st != 2) return st == 1;
-        uint64_t u = 0;
-        if (lane == 0) u = wk.first_dyn + atomicAdd(a.work_ctr, 1u);
-        u = __shfl_sync(kFull, u, 0);
-        if (u >= nu_w) {
-          if (lane == 0) wk.done = true;
-        } else {
-          wk.start_warp(a, v, u * un_w, (u + 1) * un_w, c0, lane);
-        }
-        resume = true;
-      }
-    };
     for (int s = 0; s < STAGES - 1; ++s) {
-      if (!fill(s)) break;
+      int ok = 0;
+      if (lane == 0) ok = fill_stage<CHUNK>(a, v, wk, desc[s], data + (size_t)s * CHUNK, &bar[s]);
+      ok = __shfl_sync(kFull, ok, 0);
+      if (!ok) break;
       ++nprod;
     }
     for (int c = 0; c < nprod; ++c) {
@@ -850,8 +843,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) copy_kernel(const __grid_consta
       }
       if (lane == 0) { bulk_commit(); bulk_wait_read1(); }
       __syncwarp();
-      if (lane == 0) fence_proxy_async_smem();
-      if (fill((c + STAGES - 1) % STAGES)) ++nprod;
+      int ok = 0;
+      if (lane == 0) {
+        const int ns = (c + STAGES - 1) % STAGES;
+        fence_proxy_async_smem();
+        ok = fill_stage<CHUNK>(a, v, wk, desc[ns], data + (size_t)ns * CHUNK, &bar[ns]);
+      }
+      ok = __shfl_sync(kFull, ok, 0);
+      if (ok) ++nprod;
     }
     if (lane == 0) bulk_wait_all();
     if (lane == 0 && a.trace) {

@@ -64,12 +64,15 @@ def main():
     flush = torch.empty(512 * MiB, dtype=torch.uint8, device=dev)
     ed = EmulatedDispatch(R)
     rows = []
+    only = os.environ.get("SWEEP_ONLY", "")  # e.g. "B:longtail:1024" (re-measure one point)
     for series, fname in (("A", "scalar6-fp32"), ("B", "scalar6-fp32+hidden2560")):
         fields = W.field_set(fname)
         F = len(fields)
         for kind in ("uniform", "longtail"):
             for p_mib in (1, 4, 16, 64, 256, 1024, 4096):
                 if series == "B" and p_mib < 64:
+                    continue
+                if only and only != f"{series}:{kind}:{p_mib}":
                     continue
                 n = n_for(kind, fields, p_mib * MiB)
                 lens = lengths(kind, n)
